@@ -1,0 +1,101 @@
+/* Stage-body kernels for DARIS on B200 (sm_100a) — C ABI.
+ *
+ * The reference (stagesim) has no tensor code: a stage is an opaque work
+ * quantum `StageProfile(nominal_time, width)` (/root/reference/pkg/src/stagesim/model.py:24-27)
+ * whose execution is the rate model `allocate_rates/next_completion/advance_progress`
+ * (/root/reference/pkg/src/stagesim/gpu.py:167-240).  These entry points are
+ * what replaces that rate model on real hardware: each DNN stage is a short
+ * sequence of these launches, captured into one CUDA graph per (task, stage,
+ * partition) by the executor (daris_exec.h).
+ *
+ * Layout conventions (all device pointers):
+ *   activations  NHWC bf16, contiguous
+ *   conv weights [Cout][KH][KW][Cin] bf16 (K-major rows for the tensor cores)
+ *   folded BN    per-Cout fp32 scale and bias  (y = conv(x)*scale + bias)
+ * All functions return 0 on success, a negative daris_kstatus on bad
+ * arguments, or a positive cudaError_t from the launch.
+ */
+#ifndef DARIS_KERNELS_H
+#define DARIS_KERNELS_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum daris_kstatus {
+  DARIS_K_OK = 0,
+  DARIS_K_BAD_SHAPE = -1,   /* a dimension the kernel cannot tile */
+  DARIS_K_BAD_ARG = -2,     /* null pointer / misaligned buffer */
+  DARIS_K_NO_DRIVER = -3,   /* cuTensorMapEncodeTiled unavailable */
+  DARIS_K_WORKSPACE = -4    /* split-K scratch too small */
+};
+
+/* Implicit-GEMM convolution on tcgen05 (TMEM accumulators, TMA-fed weights,
+ * cp.async-gathered activations) with a fused epilogue:
+ *   y = act(conv(x, w) * scale + bias [+ residual])
+ * Requirements: cin % 64 == 0, cout % 64 == 0.
+ * Split-K is used when the output tile count is small against `sm_budget`
+ * (the SM count of the partition the stage runs in). */
+typedef struct daris_conv_desc {
+  const void* x;          /* [n][h][w][cin] bf16 */
+  void* y;                /* [n][ho][wo][cout] bf16 */
+  const void* residual;   /* like y, or NULL */
+  const void* weight;     /* [cout][kh][kw][cin] bf16 */
+  const float* scale;     /* [cout] */
+  const float* bias;      /* [cout] */
+  float* workspace;       /* split-K partials, daris_conv_plan() floats */
+  int32_t* counters;      /* split-K tile counters, zero-initialised, self-resetting */
+  int32_t n, h, w, cin, cout, kh, kw, stride, pad, ho, wo;
+  int32_t relu;           /* 1: ReLU, 6: ReLU6, 0: none */
+  int32_t block_n;        /* 0 = auto, else 64/128/256 */
+  int32_t splits;         /* 0 = auto, else forced split-K factor */
+  int32_t sm_budget;      /* SMs available to this launch (0 = whole device) */
+} daris_conv_desc;
+
+typedef struct daris_conv_plan_t {
+  int32_t block_n, splits, kb_per_split, tiles_m, tiles_n;
+  int64_t workspace_floats; /* needed in desc.workspace */
+  int32_t counters;         /* needed in desc.counters */
+  int32_t ctas;
+} daris_conv_plan_t;
+
+int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out);
+int daris_conv2d(const daris_conv_desc* d, void* stream);
+
+/* ResNet/VGG stem input pack: x fp32 NCHW [n][c][h][w] -> im2col rows
+ * [n*ho*wo][kpad] bf16 with k = ci*kh*kw + r*kw + s (torch weight order),
+ * zero-padded to kpad (a multiple of 64). Turns the c=3 stem into a GEMM. */
+int daris_stem_im2col(const float* x, void* out, int32_t n, int32_t c, int32_t h, int32_t w, int32_t kh,
+                      int32_t kw, int32_t stride, int32_t pad, int32_t ho, int32_t wo, int32_t kpad, void* stream);
+
+/* NCHW fp32 -> NHWC bf16 with channels zero-padded to cpad (multiple of 8). */
+int daris_pack_nhwc(const float* x, void* out, int32_t n, int32_t c, int32_t h, int32_t w, int32_t cpad,
+                    void* stream);
+
+/* Max pooling, NHWC bf16, c % 8 == 0. */
+int daris_maxpool(const void* x, void* y, int32_t n, int32_t h, int32_t w, int32_t c, int32_t k, int32_t stride,
+                  int32_t pad, int32_t ho, int32_t wo, void* stream);
+
+/* Global average pooling NHWC bf16 [n][hw][c] -> fp32 [n][c]. */
+int daris_avgpool(const void* x, float* y, int32_t n, int32_t hw, int32_t c, void* stream);
+
+/* Linear layer for small batches (weight-streaming GEMV, HBM bound):
+ * y[b][o] = act(sum_k x[b][k] * w[o][k] + bias[o]); x fp32 or bf16 (x_bf16=1),
+ * y fp32 (y_bf16=0) or bf16. k % 8 == 0. */
+int daris_linear(const void* x, int32_t x_bf16, const void* w, const float* bias, void* y, int32_t y_bf16,
+                 int32_t batch, int32_t k, int32_t o, int32_t relu, void* stream);
+
+/* Depthwise 3x3 conv + folded BN + ReLU6/ReLU, NHWC bf16, c % 8 == 0,
+ * weight [kh][kw][c] bf16. */
+int daris_dwconv(const void* x, void* y, const void* weight, const float* scale, const float* bias, int32_t n,
+                 int32_t h, int32_t w, int32_t c, int32_t k, int32_t stride, int32_t pad, int32_t ho, int32_t wo,
+                 int32_t relu, void* stream);
+
+/* Number of SMs on the current device (cached). */
+int daris_device_sms(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

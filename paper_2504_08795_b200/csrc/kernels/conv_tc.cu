@@ -1,0 +1,421 @@
+// Implicit-GEMM convolution on the sm_100a tensor cores (tcgen05 + TMEM + TMA).
+//
+// GEMM view: M = n*ho*wo output pixels, N = cout, K = kh*kw*cin with K ordered
+// (kh, kw, cin) so one 64-wide K block is 64 contiguous NHWC channels of one
+// input pixel (128 B). Per CTA: a 128 x BN output tile, fp32 accumulator in
+// TMEM (BN columns), a STAGES-deep smem ring.
+//
+//   warps 0-3  activation producers: cp.async gather of 128 rows x 128 B per
+//              K block straight into the 128B-swizzled UMMA layout (zero-fill
+//              for padding / tail rows), then the epilogue (TMEM -> regs ->
+//              scale/bias/residual/act -> bf16 NHWC stores).
+//   warp 4     weight producer: one TMA 2D box {64, BN} per K block; owns TMEM.
+//   warp 5     MMA issuer: one thread, 4 x tcgen05.mma (K=16) per K block.
+//
+// Split-K (small-M layers at batch 1): each split writes fp32 partials to a
+// workspace; the last CTA of a tile (atomic ticket) reduces them in split
+// order (deterministic) and runs the epilogue, then re-arms the ticket.
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+#include <cstdio>
+#include <mutex>
+#include "sm100.cuh"
+#include "../../../include/daris_kernels.h"
+
+namespace daris {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;            // bf16 elements per K block = 128 B rows
+constexpr int kStages = 4;
+constexpr int kLag = 2;            // cp.async groups kept in flight per producer thread
+constexpr int kThreads = 192;
+
+struct ConvArgs {
+  const __nv_bfloat16* x;
+  __nv_bfloat16* y;
+  const __nv_bfloat16* res;
+  const float* scale;
+  const float* bias;
+  float* ws;
+  int* counters;
+  int n, h, w, cin, cout, kh, kw, stride, pad, ho, wo;
+  int M, relu, num_kb, kb_per_split, splits, cin_blocks;
+};
+
+template <int BN>
+struct SmemLayout {
+  static constexpr int kABytes = kBM * 128;
+  static constexpr int kBBytes = BN * 128;
+  static constexpr int kAOff = 0;
+  static constexpr int kBOff = kStages * kABytes;
+  static constexpr int kBarOff = kBOff + kStages * kBBytes;
+  static constexpr int kTotal = kBarOff + 256 + 1024;  // + barriers + alignment slack
+};
+
+__device__ __forceinline__ float act_apply(float v, int relu) {
+  if (relu == 1) return fmaxf(v, 0.f);
+  if (relu == 6) return fminf(fmaxf(v, 0.f), 6.f);
+  return v;
+}
+
+// 32 accumulator columns of one output row -> scale/bias/residual/act -> bf16.
+__device__ __forceinline__ void finalize_row32(const ConvArgs& a, int m, int col0, const float* v) {
+  if (m >= a.M) return;
+  const float4* sc = reinterpret_cast<const float4*>(a.scale + col0);
+  const float4* bi = reinterpret_cast<const float4*>(a.bias + col0);
+  float o[32];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    float4 s = __ldg(sc + q), b = __ldg(bi + q);
+    o[4 * q + 0] = v[4 * q + 0] * s.x + b.x;
+    o[4 * q + 1] = v[4 * q + 1] * s.y + b.y;
+    o[4 * q + 2] = v[4 * q + 2] * s.z + b.z;
+    o[4 * q + 3] = v[4 * q + 3] * s.w + b.w;
+  }
+  const size_t off = static_cast<size_t>(m) * a.cout + col0;
+  if (a.res != nullptr) {
+    const uint4* rp = reinterpret_cast<const uint4*>(a.res + off);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 r = __ldg(rp + q);
+      uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float2 f = unpack_bf16x2(rr[e]);
+        o[8 * q + 2 * e] += f.x;
+        o[8 * q + 2 * e + 1] += f.y;
+      }
+    }
+  }
+  uint4* yp = reinterpret_cast<uint4*>(a.y + off);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 pk;
+    pk.x = pack_bf16x2(act_apply(o[8 * q + 0], a.relu), act_apply(o[8 * q + 1], a.relu));
+    pk.y = pack_bf16x2(act_apply(o[8 * q + 2], a.relu), act_apply(o[8 * q + 3], a.relu));
+    pk.z = pack_bf16x2(act_apply(o[8 * q + 4], a.relu), act_apply(o[8 * q + 5], a.relu));
+    pk.w = pack_bf16x2(act_apply(o[8 * q + 6], a.relu), act_apply(o[8 * q + 7], a.relu));
+    yp[q] = pk;
+  }
+}
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_igemm_tc_kernel(const __grid_constant__ CUtensorMap wmap, const ConvArgs a) {
+  using L = SmemLayout<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem + L::kAOff;
+  uint8_t* sB = smem + L::kBOff;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  uint64_t* empty = full + kStages;
+  uint64_t* tmem_full = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int tile_m = blockIdx.x, tile_n = blockIdx.y, split = blockIdx.z;
+  const int m0 = tile_m * kBM, n0 = tile_n * BN;
+  const int kb_begin = split * a.kb_per_split;
+  const int kb_end = min(a.num_kb, kb_begin + a.kb_per_split);
+  const int nkb = kb_end - kb_begin;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 128 + 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 4) {
+    tmem_alloc<BN>(tmem_slot);
+    if (lane == 0) tma_prefetch_desc(&wmap);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < 4) {
+    // ---------------- activation producer ----------------
+    const int t = threadIdx.x;
+    const int row_sub = t >> 3, chunk = t & 7;
+    int pix_base[8], ih0[8], iw0[8];
+    const int howo = a.ho * a.wo;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      const int m = m0 + p * 16 + row_sub;
+      if (m < a.M) {
+        const int img = m / howo;
+        const int rem = m - img * howo;
+        const int oh = rem / a.wo, ow = rem - (rem / a.wo) * a.wo;
+        pix_base[p] = img * a.h * a.w;
+        ih0[p] = oh * a.stride - a.pad;
+        iw0[p] = ow * a.stride - a.pad;
+      } else {
+        pix_base[p] = 0;
+        ih0[p] = -1 << 20;  // forces the bounds test to fail
+        iw0[p] = -1 << 20;
+      }
+    }
+    const uint32_t sA_u32 = smem_u32(sA);
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % kStages;
+      if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
+      const int kb = kb_begin + i;
+      const int kpos = kb / a.cin_blocks;
+      const int cb = kb - kpos * a.cin_blocks;
+      const int r_ = kpos / a.kw, s_ = kpos - (kpos / a.kw) * a.kw;
+      const uint32_t stage_base = sA_u32 + s * L::kABytes;
+#pragma unroll
+      for (int p = 0; p < 8; ++p) {
+        const int r = p * 16 + row_sub;
+        const int ih = ih0[p] + r_, iw = iw0[p] + s_;
+        const bool valid = (unsigned)ih < (unsigned)a.h && (unsigned)iw < (unsigned)a.w;
+        const __nv_bfloat16* src =
+            valid ? a.x + (static_cast<size_t>(pix_base[p] + ih * a.w + iw) * a.cin + cb * kBK + chunk * 8) : a.x;
+        const uint32_t dst = stage_base + r * 128 + ((chunk ^ (r & 7)) << 4);
+        cp_async_16(dst, src, valid);
+      }
+      cp_async_commit();
+      if (i >= kLag) {
+        cp_async_wait<kLag>();
+        fence_proxy_async_smem();
+        mbar_arrive(&full[(i - kLag) % kStages]);
+      }
+    }
+    cp_async_wait<0>();
+    fence_proxy_async_smem();
+    for (int i = max(0, nkb - kLag); i < nkb; ++i) mbar_arrive(&full[i % kStages]);
+
+    // ---------------- epilogue ----------------
+    __syncwarp();
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int row = warp * 32 + lane;
+    const int m = m0 + row;
+    const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
+    if (a.splits == 1) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_row + c0, r);
+        finalize_row32(a, m, n0 + c0, reinterpret_cast<const float*>(r));
+      }
+    } else {
+      const int tile = tile_m * gridDim.y + tile_n;
+      float* part = a.ws + (static_cast<size_t>(tile) * a.splits + split) * (kBM * BN) + static_cast<size_t>(row) * BN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_row + c0, r);
+        float4* dst = reinterpret_cast<float4*>(part + c0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                               __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+      }
+      __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 0) {
+        const int ticket = atomicAdd(&a.counters[tile], 1);
+        *last_flag = (ticket == a.splits - 1);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (*last_flag) {
+        __threadfence();
+        const float* base = a.ws + static_cast<size_t>(tile) * a.splits * (kBM * BN) + static_cast<size_t>(row) * BN;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float acc[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+          for (int sp = 0; sp < a.splits; ++sp) {
+            const float4* src = reinterpret_cast<const float4*>(base + static_cast<size_t>(sp) * (kBM * BN) + c0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float4 f = __ldcg(src + q);
+              acc[4 * q] += f.x;
+              acc[4 * q + 1] += f.y;
+              acc[4 * q + 2] += f.z;
+              acc[4 * q + 3] += f.w;
+            }
+          }
+          finalize_row32(a, m, n0 + c0, acc);
+        }
+        if (threadIdx.x == 0) a.counters[tile] = 0;  // re-arm for the next launch
+      }
+    }
+  } else if (warp == 4) {
+    // ---------------- weight producer (TMA) ----------------
+    if (lane == 0) {
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % kStages;
+        if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], L::kBBytes);
+        tma_load_2d(&wmap, &full[s], sB + s * L::kBBytes, (kb_begin + i) * kBK, n0);
+      }
+    }
+  } else {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(kBM, BN);
+      const uint32_t sA_u32 = smem_u32(sA), sB_u32 = smem_u32(sB);
+      for (int i = 0; i < nkb; ++i) {
+        const int s = i % kStages;
+        mbar_wait(&full[s], (i / kStages) & 1);
+        tc_fence_after();
+        const uint64_t adesc = umma_desc_k_sw128(sA_u32 + s * L::kABytes);
+        const uint64_t bdesc = umma_desc_k_sw128(sB_u32 + s * L::kBBytes);
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k) {
+          // +32 B along K inside the 128 B swizzle atom = +2 in the encoded start address
+          umma_bf16(tmem_base, adesc + 2 * k, bdesc + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(&empty[s]);
+      }
+      umma_commit(tmem_full);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc<BN>(tmem_base);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+template <int BN>
+static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cudaStream_t st) {
+  using L = SmemLayout<BN>;
+  auto encode = get_encode_fn();
+  if (!encode) return DARIS_K_NO_DRIVER;
+  const int K = d->kh * d->kw * d->cin;
+  CUtensorMap map;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(d->cout)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(K) * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(BN)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(d->weight), dims, strides, box,
+                      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return DARIS_K_BAD_ARG;
+
+  static bool attr_set = false;  // per template instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(conv_igemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         L::kTotal);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  ConvArgs a;
+  a.x = static_cast<const __nv_bfloat16*>(d->x);
+  a.y = static_cast<__nv_bfloat16*>(d->y);
+  a.res = static_cast<const __nv_bfloat16*>(d->residual);
+  a.scale = d->scale;
+  a.bias = d->bias;
+  a.ws = d->workspace;
+  a.counters = d->counters;
+  a.n = d->n; a.h = d->h; a.w = d->w; a.cin = d->cin; a.cout = d->cout;
+  a.kh = d->kh; a.kw = d->kw; a.stride = d->stride; a.pad = d->pad; a.ho = d->ho; a.wo = d->wo;
+  a.M = d->n * d->ho * d->wo;
+  a.relu = d->relu;
+  a.cin_blocks = d->cin / kBK;
+  a.num_kb = d->kh * d->kw * a.cin_blocks;
+  a.kb_per_split = pl.kb_per_split;
+  a.splits = pl.splits;
+  dim3 grid(pl.tiles_m, pl.tiles_n, pl.splits);
+  conv_igemm_tc_kernel<BN><<<grid, kThreads, L::kTotal, st>>>(map, a);
+  return static_cast<int>(cudaGetLastError());
+}
+
+}  // namespace daris
+
+extern "C" int daris_device_sms(void) {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out) {
+  using namespace daris;
+  if (!d || !out) return DARIS_K_BAD_ARG;
+  if (d->cin % kBK != 0 || d->cout % 64 != 0 || d->n < 1 || d->ho < 1 || d->wo < 1 || d->kh < 1 || d->kw < 1 ||
+      d->stride < 1)
+    return DARIS_K_BAD_SHAPE;
+  const int M = d->n * d->ho * d->wo;
+  const int num_kb = d->kh * d->kw * (d->cin / kBK);
+  const int budget = d->sm_budget > 0 ? d->sm_budget : daris_device_sms();
+  const int tiles_m = (M + kBM - 1) / kBM;
+  int bn = d->block_n;
+  if (bn == 0) {
+    bn = (d->cout % 128 == 0) ? 128 : 64;
+    // prefer narrower tiles when the grid would not cover the partition
+    if (bn == 128 && tiles_m * (d->cout / 128) < budget) bn = 64;
+  }
+  if (bn != 64 && bn != 128 && bn != 256) return DARIS_K_BAD_SHAPE;
+  if (d->cout % bn != 0) return DARIS_K_BAD_SHAPE;
+  const int tiles_n = d->cout / bn;
+  const int tiles = tiles_m * tiles_n;
+  int splits = d->splits;
+  if (splits <= 0) {
+    splits = 1;
+    if (tiles * 2 <= budget) {
+      splits = budget / tiles;
+      const int max_by_k = num_kb / 2 > 0 ? num_kb / 2 : 1;  // keep >= 2 K blocks per split
+      if (splits > max_by_k) splits = max_by_k;
+      if (splits > 32) splits = 32;
+      if (splits < 1) splits = 1;
+    }
+  }
+  if (splits > num_kb) splits = num_kb;
+  int kbps = (num_kb + splits - 1) / splits;
+  splits = (num_kb + kbps - 1) / kbps;  // no empty splits
+  out->block_n = bn;
+  out->splits = splits;
+  out->kb_per_split = kbps;
+  out->tiles_m = tiles_m;
+  out->tiles_n = tiles_n;
+  out->workspace_floats = splits > 1 ? static_cast<int64_t>(tiles) * splits * kBM * bn : 0;
+  out->counters = splits > 1 ? tiles : 0;
+  out->ctas = tiles * splits;
+  return DARIS_K_OK;
+}
+
+extern "C" int daris_conv2d(const daris_conv_desc* d, void* stream) {
+  using namespace daris;
+  daris_conv_plan_t pl;
+  int rc = daris_conv_plan(d, &pl);
+  if (rc != DARIS_K_OK) return rc;
+  if (!d->x || !d->y || !d->weight || !d->scale || !d->bias) return DARIS_K_BAD_ARG;
+  if (pl.splits > 1 && (!d->workspace || !d->counters)) return DARIS_K_WORKSPACE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (pl.block_n) {
+    case 64: return launch_bn<64>(d, pl, st);
+    case 128: return launch_bn<128>(d, pl, st);
+    case 256: return launch_bn<256>(d, pl, st);
+  }
+  return DARIS_K_BAD_SHAPE;
+}

@@ -1,0 +1,188 @@
+"""ctypes binding of the sm_100a stage kernels (include/daris_kernels.h).
+
+Torch tensors are used only as device-memory owners: every call passes raw
+pointers and sizes across the C ABI. There is no fallback path — if the
+native library is missing these functions raise.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+import torch
+
+_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libdaris_gpu.so"
+_lib = None
+
+
+class KernelError(RuntimeError):
+    pass
+
+
+class ConvDesc(C.Structure):
+    _fields_ = [
+        ("x", C.c_void_p), ("y", C.c_void_p), ("residual", C.c_void_p), ("weight", C.c_void_p),
+        ("scale", C.c_void_p), ("bias", C.c_void_p), ("workspace", C.c_void_p), ("counters", C.c_void_p),
+        ("n", C.c_int32), ("h", C.c_int32), ("w", C.c_int32), ("cin", C.c_int32), ("cout", C.c_int32),
+        ("kh", C.c_int32), ("kw", C.c_int32), ("stride", C.c_int32), ("pad", C.c_int32),
+        ("ho", C.c_int32), ("wo", C.c_int32), ("relu", C.c_int32), ("block_n", C.c_int32),
+        ("splits", C.c_int32), ("sm_budget", C.c_int32),
+    ]
+
+
+class ConvPlan(C.Structure):
+    _fields_ = [
+        ("block_n", C.c_int32), ("splits", C.c_int32), ("kb_per_split", C.c_int32),
+        ("tiles_m", C.c_int32), ("tiles_n", C.c_int32), ("workspace_floats", C.c_int64),
+        ("counters", C.c_int32), ("ctas", C.c_int32),
+    ]
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            raise KernelError(f"native stage-kernel library missing: {_LIB_PATH} "
+                              "(run `python -m paper_2504_08795_b200.build`)")
+        L = C.CDLL(str(_LIB_PATH))
+        vp, i32 = C.c_void_p, C.c_int32
+        L.daris_conv_plan.argtypes = [C.POINTER(ConvDesc), C.POINTER(ConvPlan)]
+        L.daris_conv2d.argtypes = [C.POINTER(ConvDesc), vp]
+        L.daris_stem_im2col.argtypes = [vp, vp] + [i32] * 11 + [vp]
+        L.daris_pack_nhwc.argtypes = [vp, vp] + [i32] * 5 + [vp]
+        L.daris_maxpool.argtypes = [vp, vp] + [i32] * 9 + [vp]
+        L.daris_avgpool.argtypes = [vp, vp, i32, i32, i32, vp]
+        L.daris_linear.argtypes = [vp, i32, vp, vp, vp, i32, i32, i32, i32, i32, vp]
+        L.daris_dwconv.argtypes = [vp, vp, vp, vp, vp] + [i32] * 10 + [vp]
+        L.daris_device_sms.argtypes = []
+        for name in ("daris_conv_plan", "daris_conv2d", "daris_stem_im2col", "daris_pack_nhwc",
+                     "daris_maxpool", "daris_avgpool", "daris_linear", "daris_dwconv", "daris_device_sms"):
+            getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != 0:
+        raise KernelError(f"{what} failed with status {rc}")
+
+
+def conv_desc(x_shape, cout, kh, kw, stride, pad, *, relu=1, block_n=0, splits=0, sm_budget=0) -> ConvDesc:
+    n, h, w, cin = x_shape
+    ho = (h + 2 * pad - kh) // stride + 1
+    wo = (w + 2 * pad - kw) // stride + 1
+    d = ConvDesc()
+    d.n, d.h, d.w, d.cin, d.cout = n, h, w, cin, cout
+    d.kh, d.kw, d.stride, d.pad, d.ho, d.wo = kh, kw, stride, pad, ho, wo
+    d.relu, d.block_n, d.splits, d.sm_budget = relu, block_n, splits, sm_budget
+    return d
+
+
+def conv_plan(d: ConvDesc) -> ConvPlan:
+    p = ConvPlan()
+    _check(lib().daris_conv_plan(C.byref(d), C.byref(p)), "daris_conv_plan")
+    return p
+
+
+def conv2d(x: torch.Tensor, weight: torch.Tensor, scale: torch.Tensor, bias: torch.Tensor, *,
+           stride: int = 1, pad: int = 0, relu: int = 1, residual: torch.Tensor | None = None,
+           out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+           counters: torch.Tensor | None = None, block_n: int = 0, splits: int = 0,
+           sm_budget: int = 0, stream=None) -> torch.Tensor:
+    """x: [n,h,w,cin] bf16 NHWC; weight: [cout,kh,kw,cin] bf16."""
+    cout, kh, kw, cin = weight.shape
+    d = conv_desc(tuple(x.shape), cout, kh, kw, stride, pad, relu=relu, block_n=block_n,
+                  splits=splits, sm_budget=sm_budget)
+    p = conv_plan(d)
+    if out is None:
+        out = torch.empty((d.n, d.ho, d.wo, cout), dtype=torch.bfloat16, device=x.device)
+    if p.splits > 1:
+        if workspace is None or workspace.numel() < p.workspace_floats:
+            workspace = torch.empty(p.workspace_floats, dtype=torch.float32, device=x.device)
+        if counters is None or counters.numel() < p.counters:
+            counters = torch.zeros(p.counters, dtype=torch.int32, device=x.device)
+    d.x, d.y, d.residual, d.weight = _ptr(x), _ptr(out), _ptr(residual), _ptr(weight)
+    d.scale, d.bias = _ptr(scale), _ptr(bias)
+    d.workspace, d.counters = _ptr(workspace), _ptr(counters)
+    _check(lib().daris_conv2d(C.byref(d), _stream(stream)), "daris_conv2d")
+    return out
+
+
+def stem_im2col(x: torch.Tensor, kh: int, kw: int, stride: int, pad: int, kpad: int,
+                out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    n, c, h, w = x.shape
+    ho = (h + 2 * pad - kh) // stride + 1
+    wo = (w + 2 * pad - kw) // stride + 1
+    if out is None:
+        out = torch.empty((n, ho, wo, kpad), dtype=torch.bfloat16, device=x.device)
+    _check(lib().daris_stem_im2col(_ptr(x), _ptr(out), n, c, h, w, kh, kw, stride, pad, ho, wo, kpad,
+                                   _stream(stream)), "daris_stem_im2col")
+    return out
+
+
+def pack_nhwc(x: torch.Tensor, cpad: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    n, c, h, w = x.shape
+    if out is None:
+        out = torch.empty((n, h, w, cpad), dtype=torch.bfloat16, device=x.device)
+    _check(lib().daris_pack_nhwc(_ptr(x), _ptr(out), n, c, h, w, cpad, _stream(stream)), "daris_pack_nhwc")
+    return out
+
+
+def maxpool(x: torch.Tensor, k: int, stride: int, pad: int, out: torch.Tensor | None = None,
+            stream=None) -> torch.Tensor:
+    n, h, w, c = x.shape
+    ho = (h + 2 * pad - k) // stride + 1
+    wo = (w + 2 * pad - k) // stride + 1
+    if out is None:
+        out = torch.empty((n, ho, wo, c), dtype=torch.bfloat16, device=x.device)
+    _check(lib().daris_maxpool(_ptr(x), _ptr(out), n, h, w, c, k, stride, pad, ho, wo, _stream(stream)),
+           "daris_maxpool")
+    return out
+
+
+def avgpool(x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    n, h, w, c = x.shape
+    if out is None:
+        out = torch.empty((n, c), dtype=torch.float32, device=x.device)
+    _check(lib().daris_avgpool(_ptr(x), _ptr(out), n, h * w, c, _stream(stream)), "daris_avgpool")
+    return out
+
+
+def linear(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None, *, relu: int = 0,
+           out_bf16: bool = False, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    b, k = x.shape[0], x[0].numel()
+    o = weight.shape[0]
+    if out is None:
+        out = torch.empty((b, o), dtype=torch.bfloat16 if out_bf16 else torch.float32, device=x.device)
+    _check(lib().daris_linear(_ptr(x), int(x.dtype == torch.bfloat16), _ptr(weight), _ptr(bias), _ptr(out),
+                              int(out.dtype == torch.bfloat16), b, k, o, relu, _stream(stream)), "daris_linear")
+    return out
+
+
+def dwconv(x: torch.Tensor, weight: torch.Tensor, scale: torch.Tensor, bias: torch.Tensor, *, stride: int,
+           pad: int, relu: int = 6, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """weight: [k,k,c] bf16."""
+    n, h, w, c = x.shape
+    k = weight.shape[0]
+    ho = (h + 2 * pad - k) // stride + 1
+    wo = (w + 2 * pad - k) // stride + 1
+    if out is None:
+        out = torch.empty((n, ho, wo, c), dtype=torch.bfloat16, device=x.device)
+    _check(lib().daris_dwconv(_ptr(x), _ptr(out), _ptr(weight), _ptr(scale), _ptr(bias), n, h, w, c, k, stride,
+                              pad, ho, wo, relu, _stream(stream)), "daris_dwconv")
+    return out
+
+
+def device_sms() -> int:
+    return lib().daris_device_sms()

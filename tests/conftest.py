@@ -1,0 +1,13 @@
+"""Shared pytest configuration: registers the `gpu` marker and puts the repo
+root on sys.path so `paper_2504_08795_b200` and `oracle` import from the tree."""
+
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")

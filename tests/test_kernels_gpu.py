@@ -1,0 +1,165 @@
+"""Numerics of the sm_100a stage kernels against a plain PyTorch fp32
+reference of the same op (inputs rounded to bf16 first, so the only error
+left is fp32-vs-tensor-core accumulation order and the bf16 output rounding).
+
+Tolerance (stated per SURVEY §8c P3): max |err| <= 1e-2 * max |ref| and
+relative L2 error <= 1e-2.
+"""
+
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+TOL_MAX = 1e-2
+TOL_L2 = 1e-2
+
+
+def _close(out, ref):
+    out = out.float().cpu()
+    ref = ref.float().cpu()
+    err = (out - ref).abs().max().item()
+    scale = ref.abs().max().item() + 1e-6
+    l2 = ((out - ref).norm() / (ref.norm() + 1e-6)).item()
+    assert err <= TOL_MAX * scale, f"max err {err} vs scale {scale}"
+    assert l2 <= TOL_L2, f"rel l2 {l2}"
+
+
+def _conv_case(n, h, w, cin, cout, k, stride, pad, relu=1, residual=False, block_n=0, splits=0,
+               sm_budget=0, seed=0):
+    from paper_2504_08795_b200 import kernels as K
+    g = torch.Generator().manual_seed(seed)
+    x = torch.randn(n, h, w, cin, generator=g).bfloat16()
+    wt = (torch.randn(cout, k, k, cin, generator=g) / (k * k * cin) ** 0.5).bfloat16()
+    scale = torch.rand(cout, generator=g) + 0.5
+    bias = torch.randn(cout, generator=g) * 0.1
+    ho = (h + 2 * pad - k) // stride + 1
+    wo = (w + 2 * pad - k) // stride + 1
+    res = torch.randn(n, ho, wo, cout, generator=g).bfloat16() if residual else None
+    ref = F.conv2d(x.float().permute(0, 3, 1, 2), wt.float().permute(0, 3, 1, 2), stride=stride, padding=pad)
+    ref = ref.permute(0, 2, 3, 1) * scale + bias
+    if res is not None:
+        ref = ref + res.float()
+    if relu == 1:
+        ref = ref.clamp_min(0)
+    elif relu == 6:
+        ref = ref.clamp(0, 6)
+    dev = torch.device("cuda")
+    out = K.conv2d(x.to(dev), wt.to(dev), scale.to(dev), bias.to(dev), stride=stride, pad=pad, relu=relu,
+                   residual=None if res is None else res.to(dev), block_n=block_n, splits=splits,
+                   sm_budget=sm_budget)
+    torch.cuda.synchronize()
+    _close(out, ref)
+
+
+@pytest.mark.parametrize("bn", [64, 128, 256])
+def test_conv3x3_layer1_shapes(bn):
+    _conv_case(1, 56, 56, 64, 256 if bn == 256 else 128, 3, 1, 1, block_n=bn, splits=1)
+
+
+def test_conv3x3_resnet18_layer1_auto():
+    _conv_case(1, 56, 56, 64, 64, 3, 1, 1)
+
+
+def test_conv3x3_stride2():
+    _conv_case(1, 56, 56, 64, 128, 3, 2, 1)
+
+
+def test_conv1x1_downsample_stride2_no_relu():
+    _conv_case(1, 56, 56, 256, 512, 1, 2, 0, relu=0)
+
+
+def test_conv_residual_relu():
+    _conv_case(1, 28, 28, 128, 128, 3, 1, 1, residual=True)
+
+
+def test_conv_relu6():
+    _conv_case(1, 14, 14, 64, 128, 1, 1, 0, relu=6)
+
+
+@pytest.mark.parametrize("splits", [2, 3, 8])
+def test_conv_split_k_forced(splits):
+    _conv_case(1, 7, 7, 512, 512, 3, 1, 1, splits=splits, residual=True)
+
+
+def test_conv_split_k_auto_small_m():
+    _conv_case(1, 7, 7, 512, 512, 3, 1, 1, sm_budget=74)
+
+
+def test_conv_batch_tail_tile():
+    _conv_case(3, 13, 11, 64, 64, 3, 1, 1, seed=3)
+
+
+def test_conv_split_k_repeat_resets_counters():
+    # the same workspace/counters reused by back-to-back launches (CUDA-graph pattern)
+    from paper_2504_08795_b200 import kernels as K
+    dev = torch.device("cuda")
+    g = torch.Generator().manual_seed(5)
+    x = torch.randn(1, 7, 7, 512, generator=g).bfloat16().to(dev)
+    wt = (torch.randn(512, 3, 3, 512, generator=g) / 48).bfloat16().to(dev)
+    s = torch.ones(512, device=dev)
+    b = torch.zeros(512, device=dev)
+    d = K.conv_desc((1, 7, 7, 512), 512, 3, 3, 1, 1, sm_budget=148)
+    p = K.conv_plan(d)
+    assert p.splits > 1
+    ws = torch.empty(p.workspace_floats, device=dev)
+    ctr = torch.zeros(p.counters, dtype=torch.int32, device=dev)
+    outs = [K.conv2d(x, wt, s, b, pad=1, workspace=ws, counters=ctr, sm_budget=148) for _ in range(3)]
+    torch.cuda.synchronize()
+    assert int(ctr.abs().sum()) == 0
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+
+
+def test_stem_im2col_gemm_matches_conv7x7():
+    from paper_2504_08795_b200 import kernels as K
+    dev = torch.device("cuda")
+    g = torch.Generator().manual_seed(1)
+    x = torch.randn(2, 3, 224, 224, generator=g)
+    wt = torch.randn(64, 3, 7, 7, generator=g) / 12
+    scale = torch.rand(64, generator=g) + 0.5
+    bias = torch.randn(64, generator=g) * 0.1
+    xb = x.bfloat16().float()
+    wb = wt.bfloat16().float()
+    ref = F.conv2d(xb, wb, stride=2, padding=3).permute(0, 2, 3, 1) * scale + bias
+    ref = ref.clamp_min(0)
+    a = K.stem_im2col(x.to(dev), 7, 7, 2, 3, 192)
+    wmat = torch.zeros(64, 192)
+    wmat[:, :147] = wt.reshape(64, 147)
+    out = K.conv2d(a, wmat.bfloat16().reshape(64, 1, 1, 192).to(dev), scale.to(dev), bias.to(dev))
+    torch.cuda.synchronize()
+    _close(out, ref)
+
+
+def test_maxpool_avgpool_linear_dwconv():
+    from paper_2504_08795_b200 import kernels as K
+    dev = torch.device("cuda")
+    g = torch.Generator().manual_seed(2)
+    x = torch.randn(2, 112, 112, 64, generator=g).bfloat16()
+    ref = F.max_pool2d(x.float().permute(0, 3, 1, 2), 3, 2, 1).permute(0, 2, 3, 1)
+    out = K.maxpool(x.to(dev), 3, 2, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(out.float().cpu(), ref.bfloat16().float())
+
+    x = torch.randn(3, 7, 7, 2048, generator=g).bfloat16()
+    pooled = K.avgpool(x.to(dev))
+    torch.cuda.synchronize()
+    _close(pooled, x.float().mean(dim=(1, 2)))
+
+    w = (torch.randn(1000, 2048, generator=g) / 45).bfloat16()
+    bias = torch.randn(1000, generator=g)
+    xin = torch.randn(5, 2048, generator=g)
+    y = K.linear(xin.to(dev), w.to(dev), bias.to(dev))
+    torch.cuda.synchronize()
+    _close(y, xin @ w.float().t() + bias)
+
+    x = torch.randn(1, 56, 56, 96, generator=g).bfloat16()
+    wd = (torch.randn(3, 3, 96, generator=g) / 3).bfloat16()
+    sc = torch.rand(96, generator=g) + 0.5
+    bi = torch.randn(96, generator=g) * 0.1
+    ref = F.conv2d(x.float().permute(0, 3, 1, 2), wd.float().permute(2, 0, 1).unsqueeze(1), stride=2, padding=1,
+                   groups=96).permute(0, 2, 3, 1) * sc + bi
+    out = K.dwconv(x.to(dev), wd.to(dev), sc.to(dev), bi.to(dev), stride=2, pad=1, relu=6)
+    torch.cuda.synchronize()
+    _close(out, ref.clamp(0, 6))
