@@ -1,0 +1,369 @@
+"""ctypes binding of the native dispatcher (include/daris.h, lib/libdaris_core.so).
+
+``Handle`` is the only object that crosses into C++: it owns one dispatcher
+instance and exposes the C ABI one-to-one. Structures mirror the header.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from pathlib import Path
+from typing import Sequence
+
+import numpy as np
+
+from .errors import raise_status
+
+_LIB_PATH = Path(__file__).resolve().parent / "lib" / "libdaris_core.so"
+_lib = None
+
+KIND_NAMES = ("release", "admit", "reject", "stage_start", "stage_complete", "job_complete", "sim_end")
+POLICY_CODES = {"str": 0, "mps": 1, "mps-str": 2}
+
+
+class GpuConfigC(C.Structure):
+    _fields_ = [("total_sms", C.c_int32), ("n_contexts", C.c_int32), ("n_streams", C.c_int32),
+                ("policy", C.c_int32), ("oversubscription", C.c_double), ("kappa", C.c_double)]
+
+
+class StageSpecC(C.Structure):
+    _fields_ = [("nominal_time", C.c_double), ("width", C.c_int32), ("_pad", C.c_int32)]
+
+
+class TaskSpecC(C.Structure):
+    _fields_ = [("id", C.c_int32), ("priority", C.c_int32), ("period", C.c_double), ("deadline", C.c_double),
+                ("first_stage", C.c_int32), ("n_stages", C.c_int32), ("batch_size", C.c_int32),
+                ("curve_ref_batch", C.c_int32), ("curve_ref_gain", C.c_double)]
+
+
+class OptionsC(C.Structure):
+    _fields_ = [("window_size", C.c_int32), ("no_staging", C.c_int32), ("no_last", C.c_int32),
+                ("no_prior", C.c_int32), ("no_fixed", C.c_int32), ("hpa", C.c_int32),
+                ("placement_insertion", C.c_int32), ("edf_on_job_deadline", C.c_int32),
+                ("check_invariants", C.c_int32), ("stage_migration", C.c_int32)]
+
+
+class StageRefC(C.Structure):
+    _fields_ = [("task", C.c_int32), ("job", C.c_int32), ("stage", C.c_int32), ("context", C.c_int32),
+                ("stream", C.c_int32), ("started_at", C.c_double), ("virtual_deadline", C.c_double)]
+
+
+class PlacementC(C.Structure):
+    _fields_ = [("context", C.c_int32), ("migrated_from", C.c_int32), ("n_audits", C.c_int32),
+                ("_pad", C.c_int32)]
+
+
+class LedgerC(C.Structure):
+    _fields_ = [("hp_total", C.c_double), ("lp_total", C.c_double), ("lp_active", C.c_double),
+                ("hp_active", C.c_double)]
+
+
+class AuditC(C.Structure):
+    _fields_ = [("time", C.c_double), ("active_util", C.c_double), ("job_util", C.c_double),
+                ("limit", C.c_double), ("job", C.c_int32), ("task", C.c_int32), ("priority", C.c_int32),
+                ("context", C.c_int32), ("admitted", C.c_int32), ("_pad", C.c_int32)]
+
+
+class LogRecordC(C.Structure):
+    _fields_ = [("time", C.c_double), ("kind", C.c_int32), ("task", C.c_int32), ("job", C.c_int32),
+                ("stage", C.c_int32), ("context", C.c_int32), ("stream", C.c_int32), ("rate", C.c_double)]
+
+
+class ResponseStatsC(C.Structure):
+    _fields_ = [("mean", C.c_double), ("min", C.c_double), ("max", C.c_double), ("p95", C.c_double),
+                ("p99", C.c_double), ("count", C.c_int64)]
+
+
+class ReportC(C.Structure):
+    _fields_ = [("duration", C.c_double), ("warmup", C.c_double), ("jps", C.c_double), ("dmr_hp", C.c_double),
+                ("dmr_lp", C.c_double), ("response_hp", ResponseStatsC), ("response_lp", ResponseStatsC)] + \
+               [(n, C.c_int64) for n in ("released_hp", "released_lp", "accepted_hp", "accepted_lp",
+                                         "rejected_hp", "rejected_lp", "completed_hp", "completed_lp",
+                                         "missed_hp", "missed_lp")]
+
+
+class TraceEntryC(C.Structure):
+    _fields_ = [("task", C.c_int32), ("job", C.c_int32), ("stage", C.c_int32), ("_pad", C.c_int32),
+                ("duration", C.c_double)]
+
+
+LOG_DTYPE = np.dtype([("time", "<f8"), ("kind", "<i4"), ("task", "<i4"), ("job", "<i4"), ("stage", "<i4"),
+                      ("context", "<i4"), ("stream", "<i4"), ("rate", "<f8")])
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not _LIB_PATH.exists():
+            raise ImportError(f"native dispatcher library missing: {_LIB_PATH} "
+                              "(run `python -m paper_2504_08795_b200.build`)")
+        L = C.CDLL(str(_LIB_PATH))
+        P, i32, i64, f64, vp = C.POINTER, C.c_int32, C.c_int64, C.c_double, C.c_void_p
+        sig = {
+            "daris_create": [P(GpuConfigC), P(TaskSpecC), i32, P(StageSpecC), i32, P(OptionsC), P(vp),
+                             C.c_char_p, C.c_size_t],
+            "daris_last_error": [vp],
+            "daris_sm_per_context": [P(GpuConfigC), P(i32)],
+            "daris_n_tasks": [vp, P(i32)],
+            "daris_task_ids": [vp, P(i32)],
+            "daris_task_stage_count": [vp, i32, P(i32)],
+            "daris_full_load_sim": [vp, i32, i32, P(i32), P(f64)],
+            "daris_set_full_load": [vp, P(f64)],
+            "daris_populate": [vp],
+            "daris_home_context": [vp, i32, P(i32)],
+            "daris_release": [vp, i32, f64, i32, P(f64), P(PlacementC)],
+            "daris_dispatch": [vp, i32, i32, f64, P(StageRefC), P(i32)],
+            "daris_complete": [vp, i32, i32, f64, P(i32), P(i32)],
+            "daris_ready_count": [vp, i32, P(i32)],
+            "daris_ledger": [vp, i32, P(LedgerC)],
+            "daris_admission_test": [vp, i32, i32, i32, f64, P(AuditC)],
+            "daris_predicted_finish": [vp, i32, i32, f64, P(f64)],
+            "daris_stage_estimate": [vp, i32, i32, P(f64)],
+            "daris_task_estimate": [vp, i32, P(f64)],
+            "daris_utilization": [vp, i32, P(f64)],
+            "daris_deadline_shares": [vp, i32, P(f64)],
+            "daris_record_execution": [vp, i32, i32, f64],
+            "daris_note_job_complete": [vp, i32],
+            "daris_sim_run": [vp, f64, f64, P(f64), i32, P(ReportC)],
+            "daris_trace_run": [vp, f64, f64, P(f64), P(TraceEntryC), i64, i32, P(ReportC)],
+            "daris_log_count": [vp],
+            "daris_log_copy": [vp, vp, i64],
+            "daris_audit_count": [vp],
+            "daris_audit_copy": [vp, P(AuditC), i64],
+            "daris_log_clear": [vp],
+            "daris_water_fill": [P(i32), i32, f64, P(f64), P(i32), P(f64), P(i32)],
+            "daris_allocate_rates": [P(GpuConfigC), P(i32), P(i32), i32, P(f64), P(f64), P(f64)],
+            "daris_py_sum": [P(f64), P(i32), i64],
+            "daris_destroy": [vp],
+        }
+        for name, args in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        L.daris_last_error.restype = C.c_char_p
+        L.daris_log_count.restype = C.c_int64
+        L.daris_log_copy.restype = C.c_int64
+        L.daris_audit_count.restype = C.c_int64
+        L.daris_audit_copy.restype = C.c_int64
+        L.daris_py_sum.restype = C.c_double
+        L.daris_destroy.restype = None
+        L.daris_log_clear.restype = None
+        _lib = L
+    return _lib
+
+
+EXPORTED_SYMBOLS = (
+    "daris_create", "daris_destroy", "daris_last_error", "daris_sm_per_context", "daris_n_tasks",
+    "daris_task_ids", "daris_task_stage_count", "daris_full_load_sim", "daris_set_full_load",
+    "daris_populate", "daris_home_context", "daris_release", "daris_dispatch", "daris_complete",
+    "daris_ready_count", "daris_ledger", "daris_admission_test", "daris_predicted_finish",
+    "daris_stage_estimate", "daris_task_estimate", "daris_utilization", "daris_deadline_shares",
+    "daris_record_execution", "daris_note_job_complete", "daris_sim_run", "daris_trace_run",
+    "daris_log_count", "daris_log_copy", "daris_audit_count", "daris_audit_copy", "daris_log_clear",
+    "daris_water_fill", "daris_allocate_rates", "daris_py_sum",
+)
+
+
+def gpu_struct(total_sms, n_contexts, n_streams, oversubscription, policy="mps-str", kappa=0.0) -> GpuConfigC:
+    return GpuConfigC(int(total_sms), int(n_contexts), int(n_streams), POLICY_CODES[policy],
+                      float(oversubscription), float(kappa))
+
+
+def options_struct(*, window_size=5, no_staging=False, no_last=False, no_prior=False, no_fixed=False, hpa=False,
+                   placement_order="descending_util", edf_on_job_deadline=False, check_invariants=False,
+                   stage_migration=False) -> OptionsC:
+    return OptionsC(int(window_size), int(no_staging), int(no_last), int(no_prior), int(no_fixed), int(hpa),
+                    int(placement_order == "insertion"), int(edf_on_job_deadline), int(check_invariants),
+                    int(stage_migration))
+
+
+def task_structs(tasks: Sequence[dict]):
+    """tasks: dicts {id, hp, period, deadline, stages[(nominal, width)], batch, curve(ref_b, ref_g)|None}."""
+    n_st = sum(len(t["stages"]) for t in tasks)
+    tarr = (TaskSpecC * max(1, len(tasks)))()
+    sarr = (StageSpecC * max(1, n_st))()
+    k = 0
+    for i, t in enumerate(tasks):
+        curve = t.get("curve")
+        tarr[i] = TaskSpecC(int(t["id"]), 0 if t["hp"] else 1, float(t["period"]), float(t["deadline"]), k,
+                            len(t["stages"]), int(t.get("batch", 1)), 0 if curve is None else int(curve[0]),
+                            1.0 if curve is None else float(curve[1]))
+        for nom, w in t["stages"]:
+            sarr[k] = StageSpecC(float(nom), int(w), 0)
+            k += 1
+    return tarr, sarr, n_st
+
+
+def check(code: int, handle=None, what: str = "") -> None:
+    if code != 0:
+        msg = lib().daris_last_error(handle).decode() if handle else what
+        raise_status(code, msg or what)
+
+
+class Handle:
+    """One native dispatcher instance (not thread-safe)."""
+
+    def __init__(self, gpu: GpuConfigC, tasks: Sequence[dict], opts: OptionsC):
+        L = lib()
+        tarr, sarr, n_st = task_structs(tasks)
+        err = C.create_string_buffer(512)
+        h = C.c_void_p()
+        rc = L.daris_create(C.byref(gpu), tarr, len(tasks), sarr, n_st, C.byref(opts), C.byref(h), err, 512)
+        if rc != 0:
+            raise_status(rc, err.value.decode())
+        self._h = h
+        self.n_contexts = gpu.n_contexts
+        n = C.c_int32()
+        L.daris_n_tasks(h, C.byref(n))
+        ids = (C.c_int32 * max(1, n.value))()
+        L.daris_task_ids(h, ids)
+        self.task_ids = list(ids)[: n.value]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().daris_destroy(h)
+            self._h = None
+
+    def _c(self, rc: int) -> None:
+        check(rc, self._h)
+
+    # --- offline ---
+    def full_load_sim(self, task_id: int, reps: int, draws: Sequence[int]) -> float:
+        arr = (C.c_int32 * max(1, len(draws)))(*draws)
+        out = C.c_double()
+        self._c(lib().daris_full_load_sim(self._h, task_id, reps, arr, C.byref(out)))
+        return out.value
+
+    def set_full_load(self, per_task: Sequence[float]) -> None:
+        arr = (C.c_double * len(per_task))(*per_task)
+        self._c(lib().daris_set_full_load(self._h, arr))
+
+    def populate(self) -> None:
+        self._c(lib().daris_populate(self._h))
+
+    def home_context(self, task_id: int) -> int:
+        out = C.c_int32()
+        self._c(lib().daris_home_context(self._h, task_id, C.byref(out)))
+        return out.value
+
+    # --- online ---
+    def release(self, task_id: int, t: float, job_id: int, stage_work=None) -> PlacementC:
+        pl = PlacementC()
+        w = None if stage_work is None else (C.c_double * len(stage_work))(*stage_work)
+        self._c(lib().daris_release(self._h, task_id, t, job_id, w, C.byref(pl)))
+        return pl
+
+    def dispatch(self, context: int, stream: int, t: float):
+        ref = StageRefC()
+        found = C.c_int32()
+        self._c(lib().daris_dispatch(self._h, context, stream, t, C.byref(ref), C.byref(found)))
+        return ref if found.value else None
+
+    def complete(self, job_id: int, stage: int, t: float) -> tuple[bool, bool]:
+        done, missed = C.c_int32(), C.c_int32()
+        self._c(lib().daris_complete(self._h, job_id, stage, t, C.byref(done), C.byref(missed)))
+        return bool(done.value), bool(missed.value)
+
+    def ready_count(self, context: int) -> int:
+        out = C.c_int32()
+        self._c(lib().daris_ready_count(self._h, context, C.byref(out)))
+        return out.value
+
+    def ledger(self, context: int) -> LedgerC:
+        out = LedgerC()
+        self._c(lib().daris_ledger(self._h, context, C.byref(out)))
+        return out
+
+    def admission_test(self, task_id: int, job_id: int, context: int, t: float) -> AuditC:
+        out = AuditC()
+        self._c(lib().daris_admission_test(self._h, task_id, job_id, context, t, C.byref(out)))
+        return out
+
+    def predicted_finish(self, task_id: int, context: int, t: float) -> float:
+        out = C.c_double()
+        self._c(lib().daris_predicted_finish(self._h, task_id, context, t, C.byref(out)))
+        return out.value
+
+    def stage_estimate(self, task_id: int, stage: int) -> float:
+        out = C.c_double()
+        self._c(lib().daris_stage_estimate(self._h, task_id, stage, C.byref(out)))
+        return out.value
+
+    def task_estimate(self, task_id: int) -> float:
+        out = C.c_double()
+        self._c(lib().daris_task_estimate(self._h, task_id, C.byref(out)))
+        return out.value
+
+    def utilization(self, task_id: int) -> float:
+        out = C.c_double()
+        self._c(lib().daris_utilization(self._h, task_id, C.byref(out)))
+        return out.value
+
+    def deadline_shares(self, task_id: int, n_stages: int) -> list[float]:
+        out = (C.c_double * n_stages)()
+        self._c(lib().daris_deadline_shares(self._h, task_id, out))
+        return list(out)
+
+    def record_execution(self, task_id: int, stage: int, observed: float) -> None:
+        self._c(lib().daris_record_execution(self._h, task_id, stage, observed))
+
+    def note_job_complete(self, task_id: int) -> None:
+        self._c(lib().daris_note_job_complete(self._h, task_id))
+
+    # --- engines ---
+    def sim_run(self, duration: float, warmup_frac: float, phases: Sequence[float], collect_log=True) -> ReportC:
+        rep = ReportC()
+        ph = (C.c_double * max(1, len(phases)))(*phases)
+        self._c(lib().daris_sim_run(self._h, duration, warmup_frac, ph, int(collect_log), C.byref(rep)))
+        return rep
+
+    def trace_run(self, duration: float, warmup_frac: float, phases: Sequence[float], trace: dict,
+                  collect_log=True) -> ReportC:
+        rep = ReportC()
+        ph = (C.c_double * max(1, len(phases)))(*phases)
+        items = list(trace.items())
+        arr = (TraceEntryC * max(1, len(items)))()
+        for i, ((task, job, stage), dur) in enumerate(items):
+            arr[i] = TraceEntryC(task, job, stage, 0, dur)
+        self._c(lib().daris_trace_run(self._h, duration, warmup_frac, ph, arr, len(items), int(collect_log),
+                                      C.byref(rep)))
+        return rep
+
+    def log_array(self) -> np.ndarray:
+        n = lib().daris_log_count(self._h)
+        buf = np.empty(n, dtype=LOG_DTYPE)
+        if n:
+            lib().daris_log_copy(self._h, buf.ctypes.data, n)
+        return buf
+
+    def audits(self) -> list[AuditC]:
+        n = lib().daris_audit_count(self._h)
+        arr = (AuditC * max(1, n))()
+        if n:
+            lib().daris_audit_copy(self._h, arr, n)
+        return list(arr)[:n]
+
+    def clear_log(self) -> None:
+        lib().daris_log_clear(self._h)
+
+
+def records_from_array(arr: np.ndarray) -> list[tuple]:
+    """Native log -> reference LogRecord field tuples (None for absent fields)."""
+    out = []
+    times = arr["time"].tolist()
+    kinds = arr["kind"].tolist()
+    tasks = arr["task"].tolist()
+    jobs = arr["job"].tolist()
+    stages = arr["stage"].tolist()
+    ctxs = arr["context"].tolist()
+    streams = arr["stream"].tolist()
+    rates = arr["rate"].tolist()
+    for i in range(len(times)):
+        r = rates[i]
+        out.append((times[i], KIND_NAMES[kinds[i]],
+                    None if tasks[i] < 0 else tasks[i], None if jobs[i] < 0 else jobs[i],
+                    None if stages[i] < 0 else stages[i], None if ctxs[i] < 0 else ctxs[i],
+                    None if streams[i] < 0 else streams[i], None if math.isnan(r) else r))
+    return out

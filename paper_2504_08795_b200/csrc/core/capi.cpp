@@ -1,0 +1,283 @@
+// C ABI of the DARIS dispatcher (include/daris.h). Exceptions never cross the
+// boundary: every entry point returns a status code that the Python wrapper
+// maps back onto the reference's exception classes.
+#include <cstring>
+#include <string>
+
+#include "core/dispatcher.hpp"
+
+struct daris_handle {
+  std::unique_ptr<daris::Dispatcher> d;
+  std::string last_error;
+};
+
+namespace {
+template <class F>
+int guard(daris_handle* h, F&& f) {
+  try {
+    f();
+    if (h) h->last_error.clear();
+    return DARIS_OK;
+  } catch (const daris::Error& e) {
+    if (h) h->last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    if (h) h->last_error = e.what();
+    return DARIS_E_INTERNAL;
+  }
+}
+void copy_err(char* err, size_t errlen, const std::string& m) {
+  if (err && errlen) {
+    std::strncpy(err, m.c_str(), errlen - 1);
+    err[errlen - 1] = '\0';
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int daris_create(const daris_gpu_config* gpu, const daris_task_spec* tasks, int32_t n_tasks,
+                 const daris_stage_spec* stages, int32_t n_stages, const daris_options* opts, daris_handle** out,
+                 char* err, size_t errlen) {
+  if (!gpu || !opts || !out || (n_tasks > 0 && (!tasks || !stages))) {
+    copy_err(err, errlen, "null argument");
+    return DARIS_E_VALUE;
+  }
+  try {
+    daris::validate_gpu(*gpu);
+    auto defs = daris::build_task_defs(tasks, n_tasks, stages, n_stages, opts->no_staging != 0);
+    auto* h = new daris_handle();
+    h->d = std::make_unique<daris::Dispatcher>(*gpu, std::move(defs), *opts);
+    *out = h;
+    return DARIS_OK;
+  } catch (const daris::Error& e) {
+    copy_err(err, errlen, e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    copy_err(err, errlen, e.what());
+    return DARIS_E_INTERNAL;
+  }
+}
+
+void daris_destroy(daris_handle* h) { delete h; }
+
+const char* daris_last_error(const daris_handle* h) { return h ? h->last_error.c_str() : ""; }
+
+int daris_sm_per_context(const daris_gpu_config* gpu, int32_t* out) {
+  return guard(nullptr, [&] { *out = daris::sm_per_context(*gpu); });
+}
+
+int daris_n_tasks(const daris_handle* h, int32_t* out) {
+  *out = h->d->n_tasks();
+  return DARIS_OK;
+}
+
+int daris_task_ids(const daris_handle* h, int32_t* out) {
+  for (int i = 0; i < h->d->n_tasks(); ++i) out[i] = h->d->tasks()[i].id;
+  return DARIS_OK;
+}
+
+int daris_task_stage_count(const daris_handle* h, int32_t task_id, int32_t* out) {
+  return guard(const_cast<daris_handle*>(h),
+               [&] { *out = static_cast<int32_t>(h->d->task(task_id).nominal.size()); });
+}
+
+int daris_full_load_sim(daris_handle* h, int32_t task_id, int32_t repetitions, const int32_t* draws, double* out) {
+  return guard(h, [&] { *out = daris::full_load_time(*h->d, task_id, repetitions, draws); });
+}
+
+int daris_set_full_load(daris_handle* h, const double* per_task) {
+  return guard(h, [&] {
+    for (int i = 0; i < h->d->n_tasks(); ++i) {
+      auto& r = h->d->rt(h->d->tasks()[i].id);
+      r.full_load = per_task[i];
+      r.ucache_valid = false;
+    }
+  });
+}
+
+int daris_populate(daris_handle* h) {
+  return guard(h, [&] { h->d->populate(); });
+}
+
+int daris_home_context(const daris_handle* h, int32_t task_id, int32_t* out) {
+  return guard(const_cast<daris_handle*>(h), [&] { *out = h->d->rt(task_id).home; });
+}
+
+int daris_release(daris_handle* h, int32_t task_id, double t, int32_t job_id, const double* stage_work,
+                  daris_placement* out) {
+  return guard(h, [&] { h->d->release(task_id, t, job_id, stage_work, out); });
+}
+
+int daris_dispatch(daris_handle* h, int32_t context, int32_t stream, double t, daris_stage_ref* out, int32_t* found) {
+  return guard(h, [&] {
+    if (context < 1 || context > h->d->gpu().n_contexts) throw daris::Error(DARIS_E_VALUE, "bad context");
+    daris::StageJob* st = h->d->dispatch(context, stream, t);
+    *found = st ? 1 : 0;
+    if (st && out) {
+      out->task = st->job->task;
+      out->job = st->job->id;
+      out->stage = st->j;
+      out->context = st->ctx;
+      out->stream = st->stream;
+      out->started_at = st->start;
+      out->virtual_deadline = st->vdl;
+    }
+  });
+}
+
+int daris_complete(daris_handle* h, int32_t job_id, int32_t stage, double t, int32_t* job_done, int32_t* missed) {
+  return guard(h, [&] {
+    daris::StageJob* st = h->d->find_stage(job_id, stage);
+    if (!st) throw daris::Error(DARIS_E_NOT_FOUND, "unknown stage reference");
+    bool m = false;
+    const bool done = h->d->complete(st, t, &m);
+    *job_done = done ? 1 : 0;
+    *missed = m ? 1 : 0;
+  });
+}
+
+int daris_ready_count(const daris_handle* h, int32_t context, int32_t* out) {
+  return guard(const_cast<daris_handle*>(h), [&] { *out = h->d->ready_count(context); });
+}
+
+int daris_ledger(daris_handle* h, int32_t context, daris_ledger_t* out) {
+  return guard(h, [&] {
+    if (context < 1 || context > h->d->gpu().n_contexts) throw daris::Error(DARIS_E_VALUE, "bad context");
+    *out = h->d->ledger(context);
+  });
+}
+
+int daris_admission_test(daris_handle* h, int32_t task_id, int32_t job_id, int32_t context, double t,
+                         daris_audit* out) {
+  return guard(h, [&] {
+    daris::Job probe;
+    probe.id = job_id;
+    probe.task = task_id;
+    const daris::Audit a = h->d->admission_test(probe, context, t);
+    *out = daris_audit{a.time, a.active, a.u, a.limit, a.job, a.task, a.prio, a.ctx, a.admitted ? 1 : 0, 0};
+  });
+}
+
+int daris_predicted_finish(daris_handle* h, int32_t task_id, int32_t context, double t, double* out) {
+  return guard(h, [&] { *out = h->d->predicted_finish(task_id, context, t); });
+}
+
+int daris_stage_estimate(daris_handle* h, int32_t task_id, int32_t stage, double* out) {
+  return guard(h, [&] { *out = h->d->stage_estimate(task_id, stage); });
+}
+
+int daris_task_estimate(daris_handle* h, int32_t task_id, double* out) {
+  return guard(h, [&] { *out = h->d->task_estimate(task_id); });
+}
+
+int daris_utilization(daris_handle* h, int32_t task_id, double* out) {
+  return guard(h, [&] { *out = h->d->utilization(task_id); });
+}
+
+int daris_deadline_shares(daris_handle* h, int32_t task_id, double* out) {
+  return guard(h, [&] {
+    auto s = h->d->deadline_shares(task_id);
+    for (size_t i = 0; i < s.size(); ++i) out[i] = s[i];
+  });
+}
+
+int daris_record_execution(daris_handle* h, int32_t task_id, int32_t stage, double observed) {
+  return guard(h, [&] { h->d->record_execution(task_id, stage, observed); });
+}
+
+int daris_note_job_complete(daris_handle* h, int32_t task_id) {
+  return guard(h, [&] { h->d->note_job_complete(task_id); });
+}
+
+int daris_sim_run(daris_handle* h, double duration, double warmup_frac, const double* phases, int32_t collect_log,
+                  daris_report* out) {
+  return guard(h, [&] {
+    h->d->collect_log = collect_log != 0;
+    daris::sim_run(*h->d, duration, warmup_frac, phases, out, nullptr);
+  });
+}
+
+int daris_trace_run(daris_handle* h, double duration, double warmup_frac, const double* phases,
+                    const daris_trace_entry* trace, int64_t n_trace, int32_t collect_log, daris_report* out) {
+  return guard(h, [&] {
+    std::unordered_map<long long, double> m;
+    m.reserve(static_cast<size_t>(n_trace) * 2 + 1);
+    for (int64_t i = 0; i < n_trace; ++i)
+      m[(static_cast<long long>(trace[i].job) << 8) | static_cast<long long>(trace[i].stage)] = trace[i].duration;
+    h->d->collect_log = collect_log != 0;
+    daris::sim_run(*h->d, duration, warmup_frac, phases, out, &m);
+  });
+}
+
+int64_t daris_log_count(const daris_handle* h) { return static_cast<int64_t>(h->d->log.size()); }
+
+int64_t daris_log_copy(const daris_handle* h, daris_log_record* buf, int64_t cap) {
+  const auto& L = h->d->log;
+  int64_t n = static_cast<int64_t>(L.size());
+  if (cap < n) n = cap;
+  for (int64_t i = 0; i < n; ++i) {
+    const daris::LogRec& r = L[static_cast<size_t>(i)];
+    buf[i] = daris_log_record{r.time, r.kind, r.task, r.job, r.stage, r.ctx, r.stream, r.rate};
+  }
+  return n;
+}
+
+int64_t daris_audit_count(const daris_handle* h) { return static_cast<int64_t>(h->d->audits.size()); }
+
+int64_t daris_audit_copy(const daris_handle* h, daris_audit* buf, int64_t cap) {
+  const auto& A = h->d->audits;
+  int64_t n = static_cast<int64_t>(A.size());
+  if (cap < n) n = cap;
+  for (int64_t i = 0; i < n; ++i) {
+    const daris::Audit& a = A[static_cast<size_t>(i)];
+    buf[i] = daris_audit{a.time, a.active, a.u, a.limit, a.job, a.task, a.prio, a.ctx, a.admitted ? 1 : 0, 0};
+  }
+  return n;
+}
+
+void daris_log_clear(daris_handle* h) {
+  h->d->log.clear();
+  h->d->audits.clear();
+}
+
+int daris_water_fill(const int32_t* widths, int32_t n, double capacity, double* out_alloc, int32_t* out_is_int,
+                     double* out_level, int32_t* has_level) {
+  return guard(nullptr, [&] {
+    std::vector<int> w(widths, widths + n);
+    std::vector<daris::Alloc> a;
+    const double level = daris::water_fill(w, capacity, a);
+    for (int i = 0; i < n; ++i) {
+      out_alloc[i] = a[i].v;
+      out_is_int[i] = a[i].is_int ? 1 : 0;
+    }
+    *has_level = std::isnan(level) ? 0 : 1;
+    *out_level = level;
+  });
+}
+
+int daris_allocate_rates(const daris_gpu_config* gpu, const int32_t* widths, const int32_t* ctx_ids, int32_t n,
+                         double* out_alloc, double* out_rates, double* out_scale) {
+  return guard(nullptr, [&] {
+    const int per = daris::sm_per_context(*gpu);
+    std::vector<int> w(widths, widths + n), c(ctx_ids, ctx_ids + n);
+    std::vector<daris::Alloc> a;
+    std::vector<double> r;
+    *out_scale = daris::allocate_rates(*gpu, per, w, c, a, r);
+    for (int i = 0; i < n; ++i) {
+      out_alloc[i] = a[i].v;
+      out_rates[i] = r[i];
+    }
+  });
+}
+
+double daris_py_sum(const double* values, const int32_t* is_int, int64_t n) {
+  daris::PySum s;
+  for (int64_t i = 0; i < n; ++i) {
+    if (is_int && is_int[i]) s.add_int(static_cast<long long>(values[i]));
+    else s.add(values[i]);
+  }
+  return s.value();
+}
+
+}  // extern "C"
