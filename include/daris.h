@@ -156,6 +156,8 @@ int daris_sm_per_context(const daris_gpu_config* gpu, int32_t* out);
 int daris_n_tasks(const daris_handle* h, int32_t* out);
 int daris_task_ids(const daris_handle* h, int32_t* out);               /* sorted, n_tasks entries */
 int daris_task_stage_count(const daris_handle* h, int32_t task_id, int32_t* out);
+int daris_task_info(const daris_handle* h, int32_t task_id, double* period, int32_t* n_stages,
+                    int32_t* priority);
 
 int daris_full_load_sim(daris_handle* h, int32_t task_id, int32_t repetitions, const int32_t* draws,
                         double* out);
@@ -192,6 +194,10 @@ int64_t daris_log_copy(const daris_handle* h, daris_log_record* buf, int64_t cap
 int64_t daris_audit_count(const daris_handle* h);
 int64_t daris_audit_copy(const daris_handle* h, daris_audit* buf, int64_t cap);
 void daris_log_clear(daris_handle* h);
+/* append one record (used by the GPU executor so real runs log like the sim) */
+void daris_log_push(daris_handle* h, const daris_log_record* rec);
+/* pending admitted work: ready stages summed over contexts */
+int daris_ready_total(const daris_handle* h, int32_t* out);
 
 /* Rate model kernels exposed for the unit tests (gpu.py:118-205). widths are
  * ints; out_is_int marks allocations that stayed Python ints (the "fits" branch). */

@@ -1,0 +1,111 @@
+/* DARIS real-time GPU executor — C ABI.
+ *
+ * Replaces the reference engine's device side: the simulated SM partitions
+ * (`build_contexts`, `sm_per_context`, gpu.py:81-115) become CUDA green
+ * contexts carved out of the B200's 148 SMs (overlapping windows when the
+ * oversubscription OS > 1), each with `n_streams` streams; the rate model
+ * (`allocate_rates/next_completion/advance_progress`, gpu.py:167-240) becomes
+ * real execution of per-stage CUDA graphs, with completions observed through
+ * CUDA events; and the DES loop (engine.py:379-531) becomes a wall-clock loop
+ * that releases periodic jobs, calls the native dispatcher (daris.h) for
+ * admission / migration / dispatch / completion, and launches the stage graph
+ * of the dispatched (task, stage) on the (context, stream) slot it got.
+ *
+ * Times handed to the dispatcher are quantised to multiples of 2^-20 s, so
+ * every sum/difference the scheduler forms is exact and a recorded trace
+ * replays bit-exactly through the reference.
+ */
+#ifndef DARIS_EXEC_H
+#define DARIS_EXEC_H
+#include <stddef.h>
+#include <stdint.h>
+#include "daris.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum daris_partition_mode {
+  DARIS_PART_GREEN = 0, /* CUDA green contexts (hard SM partitions) */
+  DARIS_PART_SOFT = 1   /* plain streams; partitions only via kernel grid sizing */
+};
+
+typedef struct daris_exec_config {
+  int32_t device;
+  int32_t n_contexts, n_streams;
+  int32_t sm_per_context;   /* from daris_sm_per_context() */
+  int32_t partition_mode;   /* daris_partition_mode */
+  int32_t slots_per_task;   /* buffer sets per task (jobs of one task in flight) */
+  int32_t max_tasks, max_stages;
+} daris_exec_config;
+
+typedef struct daris_exec_partition {
+  int32_t context;          /* 1-based */
+  int32_t sm_count;         /* SMs the partition actually owns */
+  int32_t first_group, n_groups;
+  int32_t green;            /* 1 if a green context backs it */
+} daris_exec_partition;
+
+/* per-stage execution record (one per completed stage) */
+typedef struct daris_stage_trace {
+  int32_t task, job, stage, context, stream, slot;
+  double start, end;        /* quantised executor time (s) */
+} daris_stage_trace;
+
+typedef struct daris_exec_stats {
+  int64_t graph_launches;   /* stage graphs launched in the run */
+  int64_t copies_h2d, copies_d2h, copies_d2d;
+  int64_t h2d_bytes, d2h_bytes;
+  int64_t slot_waits;       /* dispatches that had to wait for a buffer set */
+  int64_t polls;
+  double wall_seconds;      /* host wall time of the run incl. drain */
+  double release_lag_max;   /* worst delay between a nominal release and its processing */
+} daris_exec_stats;
+
+typedef struct daris_exec daris_exec;
+
+int daris_exec_create(const daris_exec_config* cfg, daris_exec** out, char* err, size_t errlen);
+void daris_exec_destroy(daris_exec* ex);
+int daris_exec_partition_info(const daris_exec* ex, int32_t context, daris_exec_partition* out);
+
+/* stream of (context, stream) — pass to the kernel launchers while capturing */
+int daris_exec_stream(daris_exec* ex, int32_t context, int32_t stream, void** out);
+
+/* graph capture of one stage body on a context's capture stream */
+int daris_exec_capture_begin(daris_exec* ex, int32_t context, void** stream_out);
+int daris_exec_capture_end(daris_exec* ex, int32_t task, int32_t stage, int32_t context, int32_t slot);
+int daris_exec_graph_count(const daris_exec* ex, int64_t* out);
+
+/* per (task, slot) I/O buffers. input: device buffer the first stage reads;
+ * output: device buffer the last stage writes. Pools: n_inputs images of
+ * in_bytes each, either in pinned host memory (end-to-end mode, H2D each job)
+ * or in device memory (resident mode, D2D each job); NULL skips the copy. */
+int daris_exec_set_io(daris_exec* ex, int32_t task, int32_t slot, void* dev_input, void* dev_output);
+int daris_exec_set_pool(daris_exec* ex, int32_t task, const void* pool, int32_t pool_on_host, int32_t n_inputs,
+                        int64_t in_bytes, void* host_out, int64_t out_bytes);
+
+/* Run the periodic workload for `duration` seconds of wall clock on a
+ * populated dispatcher. phases[i] = release offset of the i-th task (id
+ * order); periods come from the dispatcher's tasks. Metrics cover jobs
+ * released in [warmup, duration); in-flight jobs are drained and counted. */
+int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warmup, const double* phases,
+                   int32_t collect_log, daris_report* report, daris_exec_stats* stats);
+
+int64_t daris_exec_trace_count(const daris_exec* ex);
+int64_t daris_exec_trace_copy(const daris_exec* ex, daris_stage_trace* buf, int64_t cap);
+
+/* Full-load (AFET) calibration on the real GPU: every (context, stream) slot
+ * loops jobs of the tasks in `slot_tasks` (n_contexts*n_streams entries, slot 0
+ * is the target) for `seconds`; returns the mean job time of each task id seen
+ * in slot 0 position rotations (out[i] for task id i+1, 0 if unseen). */
+int daris_exec_busy_calibrate(daris_exec* ex, const int32_t* task_stage_counts, int32_t n_tasks,
+                              const int32_t* slot_tasks, double seconds, double* out_mean_job_time);
+
+const char* daris_exec_last_error(const daris_exec* ex);
+
+/* time quantum used for every executor timestamp (2^-20 s) */
+double daris_exec_quantum(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

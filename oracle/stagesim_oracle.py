@@ -448,8 +448,8 @@ def simulate(tasks_in: list, gpu: dict, *, seed=0, duration=60.0, warmup_frac=0.
             else:
                 accd += shares[j]
                 v = accd
-            if durations is not None:
-                rem = durations[(tid, jid, j)]
+            if durations is not None:   # rejected jobs never run: placeholder
+                rem = durations.get((tid, jid, j), work_of(nom, spec["batch"], spec["curve"]))
             else:
                 rem = work_of(nom, spec["batch"], spec["curve"])
             job.stages.append(_Stage(job, j, w, rem, v))

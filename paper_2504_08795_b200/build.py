@@ -25,7 +25,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CORE_SOURCES = ["core/dispatcher.cpp", "core/sim.cpp", "core/capi.cpp"]
-GPU_SOURCES = ["kernels/conv_tc.cu", "kernels/aux.cu"]
+GPU_SOURCES = ["kernels/conv_tc.cu", "kernels/aux.cu", "exec/executor.cu"]
 
 
 def _run(cmd: list[str]) -> None:
@@ -71,7 +71,8 @@ def build_gpu(force: bool = False) -> Path:
                    f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(src), "-o", str(obj)]
             _run(cmd)
             objs.append(str(obj))
-        cmd = [NVCC, *ARCH, "-shared", "-o", str(out), *objs, "-lcudart"]
+        cmd = [NVCC, *ARCH, "-shared", "--cudart", "shared", "-o", str(out), *objs, f"-L{LIB}", "-ldaris_core",
+               "-Xlinker", "-rpath,$ORIGIN"]
         _run(cmd)
         for o in objs:
             os.remove(o)
@@ -79,8 +80,7 @@ def build_gpu(force: bool = False) -> Path:
 
 
 def build_all(force: bool = False) -> None:
-    if all((CSRC / s).exists() for s in CORE_SOURCES):
-        build_core(force)
+    build_core(force)
     build_gpu(force)
 
 

@@ -82,6 +82,15 @@ int daris_task_stage_count(const daris_handle* h, int32_t task_id, int32_t* out)
                [&] { *out = static_cast<int32_t>(h->d->task(task_id).nominal.size()); });
 }
 
+int daris_task_info(const daris_handle* h, int32_t task_id, double* period, int32_t* n_stages, int32_t* priority) {
+  return guard(const_cast<daris_handle*>(h), [&] {
+    const daris::TaskDef& t = h->d->task(task_id);
+    *period = t.period;
+    *n_stages = static_cast<int32_t>(t.nominal.size());
+    *priority = t.hp ? DARIS_HP : DARIS_LP;
+  });
+}
+
 int daris_full_load_sim(daris_handle* h, int32_t task_id, int32_t repetitions, const int32_t* draws, double* out) {
   return guard(h, [&] { *out = daris::full_load_time(*h->d, task_id, repetitions, draws); });
 }
@@ -239,6 +248,17 @@ int64_t daris_audit_copy(const daris_handle* h, daris_audit* buf, int64_t cap) {
 void daris_log_clear(daris_handle* h) {
   h->d->log.clear();
   h->d->audits.clear();
+}
+
+void daris_log_push(daris_handle* h, const daris_log_record* r) {
+  if (h->d->collect_log) h->d->log.push_back({r->time, r->kind, r->task, r->job, r->stage, r->context, r->stream, r->rate});
+}
+
+int daris_ready_total(const daris_handle* h, int32_t* out) {
+  int n = 0;
+  for (int c = 1; c <= h->d->gpu().n_contexts; ++c) n += h->d->ready_count(c);
+  *out = n;
+  return DARIS_OK;
 }
 
 int daris_water_fill(const int32_t* widths, int32_t n, double capacity, double* out_alloc, int32_t* out_is_int,

@@ -336,9 +336,8 @@ void sim_run(Dispatcher& d, double duration, double warmup_frac, const double* p
         for (size_t j = 0; j < spec.work.size(); ++j) {
           const long long key = (static_cast<long long>(job_counter) << 8) | static_cast<long long>(j);
           auto it = trace->find(key);
-          if (it == trace->end())
-            throw Error(DARIS_E_NOT_FOUND, "trace has no duration for job " + std::to_string(job_counter));
-          work_buf[j] = it->second;
+          // jobs the recorded run rejected never execute: any placeholder works
+          work_buf[j] = it == trace->end() ? spec.work[j] : it->second;
         }
         work = work_buf.data();
       }

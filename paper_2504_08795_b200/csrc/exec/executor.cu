@@ -1,0 +1,685 @@
+// DARIS real-time executor on B200: green-context SM partitions, per-partition
+// stream slots, per-(task, stage, partition, buffer-slot) CUDA graphs, and the
+// wall-clock release / dispatch / completion loop driving the native
+// dispatcher through its C ABI (include/daris.h, include/daris_exec.h).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <queue>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../../include/daris_exec.h"
+
+namespace {
+
+constexpr double kQuantum = 1.0 / 1048576.0;  // 2^-20 s
+inline double quant(double s) { return std::floor(s / kQuantum + 0.5) * kQuantum; }
+
+struct Driver {
+  PFN_cuDeviceGetDevResource_v12040 getDevResource = nullptr;
+  PFN_cuDevSmResourceSplitByCount_v12040 split = nullptr;
+  PFN_cuDevResourceGenerateDesc_v12040 genDesc = nullptr;
+  PFN_cuGreenCtxCreate_v12040 greenCreate = nullptr;
+  PFN_cuGreenCtxDestroy_v12040 greenDestroy = nullptr;
+  PFN_cuGreenCtxStreamCreate_v12050 greenStream = nullptr;
+  PFN_cuDeviceGet_v2000 deviceGet = nullptr;
+  bool ok = false;
+};
+
+template <class T>
+bool entry(const char* name, T& fn) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return false;
+  fn = reinterpret_cast<T>(p);
+  return true;
+}
+
+Driver& driver() {
+  static Driver d;
+  static bool init = false;
+  if (!init) {
+    init = true;
+    d.ok = entry("cuDeviceGetDevResource", d.getDevResource) && entry("cuDevSmResourceSplitByCount", d.split) &&
+           entry("cuDevResourceGenerateDesc", d.genDesc) && entry("cuGreenCtxCreate", d.greenCreate) &&
+           entry("cuGreenCtxDestroy", d.greenDestroy) && entry("cuGreenCtxStreamCreate", d.greenStream) &&
+           entry("cuDeviceGet", d.deviceGet);
+  }
+  return d;
+}
+
+struct Partition {
+  int sm_count = 0, first_group = 0, n_groups = 0;
+  CUgreenCtx green = nullptr;
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> done;
+  cudaStream_t capture = nullptr;
+};
+
+struct Running {
+  bool busy = false;
+  int task = 0, job = 0, stage = 0, slot = 0;
+  double start = 0;
+};
+
+struct TaskInfo {
+  int id = 0, n_stages = 0, prio = 0;
+  double period = 0;
+};
+
+}  // namespace
+
+struct daris_exec {
+  daris_exec_config cfg{};
+  std::vector<Partition> parts;
+  // graphs[((task*max_stages + stage)*n_ctx + ctx)*slots + slot]
+  std::vector<cudaGraphExec_t> graphs;
+  // per (task, slot) I/O
+  std::vector<void*> dev_in, dev_out;
+  // per task pools
+  struct Pool {
+    const char* src = nullptr;
+    bool on_host = false;
+    int n = 0;
+    int64_t in_bytes = 0;
+    char* host_out = nullptr;
+    int64_t out_bytes = 0;
+  };
+  std::vector<Pool> pools;
+  std::vector<cudaEvent_t> slot_free;  // per (task, slot)
+  std::vector<int> slot_owner;          // job id using the buffer set, 0 = free
+  std::vector<daris_stage_trace> trace;
+  std::string err;
+  int64_t graph_count = 0;
+
+  size_t gidx(int task, int stage, int ctx, int slot) const {
+    return ((static_cast<size_t>(task - 1) * cfg.max_stages + stage) * cfg.n_contexts + (ctx - 1)) *
+               cfg.slots_per_task + slot;
+  }
+  size_t sidx(int task, int slot) const { return static_cast<size_t>(task - 1) * cfg.slots_per_task + slot; }
+};
+
+namespace {
+
+int fail(daris_exec* ex, const std::string& m, int code = DARIS_E_VALUE) {
+  if (ex) ex->err = m;
+  return code;
+}
+
+#define CUDA_TRY(ex, call)                                                                 \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) return fail(ex, std::string(#call) + ": " + cudaGetErrorString(e_), DARIS_E_INTERNAL); \
+  } while (0)
+
+int build_partitions(daris_exec* ex) {
+  const daris_exec_config& c = ex->cfg;
+  int total_sms = 0;
+  cudaDeviceGetAttribute(&total_sms, cudaDevAttrMultiProcessorCount, c.device);
+  ex->parts.resize(c.n_contexts);
+  bool green = c.partition_mode == DARIS_PART_GREEN;
+  Driver& d = driver();
+  std::vector<CUdevResource> groups;
+  CUdevice dev = 0;
+  if (green) {
+    if (!d.ok) green = false;
+  }
+  if (green) {
+    d.deviceGet(&dev, c.device);
+    CUdevResource all;
+    if (d.getDevResource(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) green = false;
+    if (green) {
+      unsigned n = static_cast<unsigned>(all.sm.smCount);
+      groups.resize(n);
+      CUdevResource rem;
+      if (d.split(groups.data(), &n, &all, &rem, CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING, 2) !=
+              CUDA_SUCCESS ||
+          n == 0)
+        green = false;
+      groups.resize(n);
+    }
+  }
+  const int G = green ? static_cast<int>(groups.size()) : total_sms / 2;
+  const int gsize = green ? static_cast<int>(groups[0].sm.smCount) : 2;
+  for (int k = 0; k < c.n_contexts; ++k) {
+    Partition& p = ex->parts[k];
+    int want = (c.sm_per_context + gsize - 1) / gsize;
+    if (want > G) want = G;
+    p.n_groups = want;
+    p.first_group = static_cast<int>((static_cast<long long>(k) * G) / c.n_contexts);
+    p.sm_count = want * gsize;
+    if (green) {
+      std::vector<CUdevResource> res;
+      for (int q = 0; q < want; ++q) res.push_back(groups[(p.first_group + q) % G]);
+      CUdevResourceDesc desc;
+      if (d.genDesc(&desc, res.data(), static_cast<unsigned>(res.size())) != CUDA_SUCCESS ||
+          d.greenCreate(&p.green, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) {
+        return fail(ex, "green context creation failed", DARIS_E_INTERNAL);
+      }
+    }
+    const int n_streams = c.n_streams + 1;  // + capture stream
+    for (int s = 0; s < n_streams; ++s) {
+      cudaStream_t st;
+      if (p.green) {
+        CUstream cs;
+        if (d.greenStream(&cs, p.green, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS)
+          return fail(ex, "green stream creation failed", DARIS_E_INTERNAL);
+        st = reinterpret_cast<cudaStream_t>(cs);
+      } else {
+        CUDA_TRY(ex, cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      }
+      if (s < c.n_streams) p.streams.push_back(st);
+      else p.capture = st;
+    }
+    for (int s = 0; s < c.n_streams; ++s) {
+      cudaEvent_t e;
+      CUDA_TRY(ex, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      p.done.push_back(e);
+    }
+  }
+  if (!green) ex->cfg.partition_mode = DARIS_PART_SOFT;
+  return DARIS_OK;
+}
+
+struct Acc {
+  double warmup;
+  long long rel[2] = {0, 0}, acc[2] = {0, 0}, rej[2] = {0, 0}, cmp[2] = {0, 0}, miss[2] = {0, 0};
+  std::vector<double> resp[2];
+  long long inputs = 0;
+};
+
+daris_response_stats stats_of(std::vector<double> v) {
+  daris_response_stats s{0, 0, 0, 0, 0, 0};
+  if (v.empty()) return s;
+  std::sort(v.begin(), v.end());
+  const size_t n = v.size();
+  double sum = 0, c = 0;  // Neumaier, as CPython's sum
+  for (double x : v) {
+    const double t = sum + x;
+    if (std::fabs(sum) >= std::fabs(x)) c += (sum - t) + x;
+    else c += (x - t) + sum;
+    sum = t;
+  }
+  s.mean = (sum + c) / static_cast<double>(n);
+  s.min = v.front();
+  s.max = v.back();
+  s.p95 = v[static_cast<size_t>(std::ceil(0.95 * n)) - 1];
+  s.p99 = v[static_cast<size_t>(std::ceil(0.99 * n)) - 1];
+  s.count = static_cast<int64_t>(n);
+  return s;
+}
+
+void push_log(daris_handle* h, double t, int kind, int task = -1, int job = -1, int stage = -1, int ctx = -1,
+              int stream = -1, double rate = NAN) {
+  daris_log_record r{t, kind, task, job, stage, ctx, stream, rate};
+  daris_log_push(h, &r);
+}
+
+}  // namespace
+
+extern "C" {
+
+double daris_exec_quantum(void) { return kQuantum; }
+
+int daris_exec_create(const daris_exec_config* cfg, daris_exec** out, char* err, size_t errlen) {
+  auto ex = std::make_unique<daris_exec>();
+  auto bail = [&](int code) {
+    if (err && errlen) {
+      std::strncpy(err, ex->err.c_str(), errlen - 1);
+      err[errlen - 1] = 0;
+    }
+    return code;
+  };
+  if (!cfg || cfg->n_contexts < 1 || cfg->n_streams < 1 || cfg->slots_per_task < 1 || cfg->max_tasks < 1 ||
+      cfg->max_stages < 1 || cfg->sm_per_context < 1) {
+    ex->err = "invalid executor config";
+    return bail(DARIS_E_VALUE);
+  }
+  ex->cfg = *cfg;
+  if (cudaSetDevice(cfg->device) != cudaSuccess || cudaFree(nullptr) != cudaSuccess) {
+    ex->err = "no CUDA device";
+    return bail(DARIS_E_INTERNAL);
+  }
+  int rc = build_partitions(ex.get());
+  if (rc != DARIS_OK) return bail(rc);
+  const size_t ng = static_cast<size_t>(cfg->max_tasks) * cfg->max_stages * cfg->n_contexts * cfg->slots_per_task;
+  ex->graphs.assign(ng, nullptr);
+  const size_t ns = static_cast<size_t>(cfg->max_tasks) * cfg->slots_per_task;
+  ex->dev_in.assign(ns, nullptr);
+  ex->dev_out.assign(ns, nullptr);
+  ex->slot_owner.assign(ns, 0);
+  ex->slot_free.resize(ns);
+  for (auto& e : ex->slot_free) {
+    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+      ex->err = "event creation failed";
+      return bail(DARIS_E_INTERNAL);
+    }
+  }
+  ex->pools.resize(cfg->max_tasks);
+  *out = ex.release();
+  return DARIS_OK;
+}
+
+void daris_exec_destroy(daris_exec* ex) {
+  if (!ex) return;
+  cudaDeviceSynchronize();
+  for (auto g : ex->graphs)
+    if (g) cudaGraphExecDestroy(g);
+  for (auto e : ex->slot_free) cudaEventDestroy(e);
+  for (auto& p : ex->parts) {
+    for (auto e : p.done) cudaEventDestroy(e);
+    for (auto s : p.streams) cudaStreamDestroy(s);
+    if (p.capture) cudaStreamDestroy(p.capture);
+    if (p.green && driver().greenDestroy) driver().greenDestroy(p.green);
+  }
+  delete ex;
+}
+
+const char* daris_exec_last_error(const daris_exec* ex) { return ex ? ex->err.c_str() : ""; }
+
+int daris_exec_partition_info(const daris_exec* ex, int32_t context, daris_exec_partition* out) {
+  if (context < 1 || context > ex->cfg.n_contexts) return DARIS_E_VALUE;
+  const Partition& p = ex->parts[context - 1];
+  *out = daris_exec_partition{context, p.sm_count, p.first_group, p.n_groups, p.green ? 1 : 0};
+  return DARIS_OK;
+}
+
+int daris_exec_stream(daris_exec* ex, int32_t context, int32_t stream, void** out) {
+  if (context < 1 || context > ex->cfg.n_contexts || stream < 0 || stream >= ex->cfg.n_streams) return DARIS_E_VALUE;
+  *out = ex->parts[context - 1].streams[stream];
+  return DARIS_OK;
+}
+
+int daris_exec_capture_begin(daris_exec* ex, int32_t context, void** stream_out) {
+  if (context < 1 || context > ex->cfg.n_contexts) return fail(ex, "bad context");
+  cudaStream_t s = ex->parts[context - 1].capture;
+  CUDA_TRY(ex, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  *stream_out = s;
+  return DARIS_OK;
+}
+
+int daris_exec_capture_end(daris_exec* ex, int32_t task, int32_t stage, int32_t context, int32_t slot) {
+  if (context < 1 || context > ex->cfg.n_contexts) return fail(ex, "bad context");
+  cudaStream_t s = ex->parts[context - 1].capture;
+  cudaGraph_t g = nullptr;
+  CUDA_TRY(ex, cudaStreamEndCapture(s, &g));
+  if (task < 1 || task > ex->cfg.max_tasks || stage < 0 || stage >= ex->cfg.max_stages || slot < 0 ||
+      slot >= ex->cfg.slots_per_task) {
+    cudaGraphDestroy(g);
+    return fail(ex, "graph key out of range");
+  }
+  cudaGraphExec_t ge = nullptr;
+  cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return fail(ex, std::string("graph instantiate: ") + cudaGetErrorString(e), DARIS_E_INTERNAL);
+  cudaGraphExec_t& slotg = ex->graphs[ex->gidx(task, stage, context, slot)];
+  if (slotg) cudaGraphExecDestroy(slotg);
+  else ex->graph_count++;
+  slotg = ge;
+  return DARIS_OK;
+}
+
+int daris_exec_graph_count(const daris_exec* ex, int64_t* out) {
+  *out = ex->graph_count;
+  return DARIS_OK;
+}
+
+int daris_exec_set_io(daris_exec* ex, int32_t task, int32_t slot, void* dev_input, void* dev_output) {
+  if (task < 1 || task > ex->cfg.max_tasks || slot < 0 || slot >= ex->cfg.slots_per_task) return fail(ex, "bad key");
+  ex->dev_in[ex->sidx(task, slot)] = dev_input;
+  ex->dev_out[ex->sidx(task, slot)] = dev_output;
+  return DARIS_OK;
+}
+
+int daris_exec_set_pool(daris_exec* ex, int32_t task, const void* pool, int32_t pool_on_host, int32_t n_inputs,
+                        int64_t in_bytes, void* host_out, int64_t out_bytes) {
+  if (task < 1 || task > ex->cfg.max_tasks) return fail(ex, "bad task");
+  auto& p = ex->pools[task - 1];
+  p.src = static_cast<const char*>(pool);
+  p.on_host = pool_on_host != 0;
+  p.n = n_inputs;
+  p.in_bytes = in_bytes;
+  p.host_out = static_cast<char*>(host_out);
+  p.out_bytes = out_bytes;
+  return DARIS_OK;
+}
+
+int64_t daris_exec_trace_count(const daris_exec* ex) { return static_cast<int64_t>(ex->trace.size()); }
+
+int64_t daris_exec_trace_copy(const daris_exec* ex, daris_stage_trace* buf, int64_t cap) {
+  const int64_t n = std::min<int64_t>(cap, static_cast<int64_t>(ex->trace.size()));
+  std::memcpy(buf, ex->trace.data(), static_cast<size_t>(n) * sizeof(daris_stage_trace));
+  return n;
+}
+
+int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warmup, const double* phases,
+                   int32_t collect_log, daris_report* report, daris_exec_stats* stats) {
+  using clock = std::chrono::steady_clock;
+  const daris_exec_config& c = ex->cfg;
+  int32_t n_tasks = 0;
+  daris_n_tasks(h, &n_tasks);
+  if (n_tasks > c.max_tasks) return fail(ex, "more tasks than the executor was sized for");
+  std::vector<int32_t> ids(n_tasks);
+  daris_task_ids(h, ids.data());
+  std::vector<TaskInfo> info(n_tasks + 1);
+  for (int i = 0; i < n_tasks; ++i) {
+    TaskInfo& t = info[ids[i]];
+    t.id = ids[i];
+    daris_task_info(h, t.id, &t.period, &t.n_stages, &t.prio);
+    if (t.n_stages > c.max_stages) return fail(ex, "task has more stages than the executor supports");
+  }
+  (void)collect_log;
+  // every graph the run may need must exist: HP tasks in their home context, LP anywhere
+  for (int i = 0; i < n_tasks; ++i) {
+    const TaskInfo& t = info[ids[i]];
+    int32_t home = 0;
+    daris_home_context(h, t.id, &home);
+    for (int s = 0; s < t.n_stages; ++s)
+      for (int k = 1; k <= c.n_contexts; ++k) {
+        if (t.prio == DARIS_HP && k != home) continue;
+        for (int q = 0; q < c.slots_per_task; ++q)
+          if (!ex->graphs[ex->gidx(t.id, s, k, q)])
+            return fail(ex, "missing stage graph for task " + std::to_string(t.id) + " stage " + std::to_string(s) +
+                                " context " + std::to_string(k));
+      }
+  }
+  ex->trace.clear();
+  daris_exec_stats st{};
+  Acc acc;
+  acc.warmup = warmup;
+
+  using Rel = std::pair<double, int>;
+  std::priority_queue<Rel, std::vector<Rel>, std::greater<Rel>> heap;
+  std::vector<double> phase(n_tasks + 1), period(n_tasks + 1);
+  std::vector<long long> rel_idx(n_tasks + 1, 0), seq(n_tasks + 1, 0);
+  for (int i = 0; i < n_tasks; ++i) {
+    const int id = ids[i];
+    phase[id] = quant(phases[i]);
+    period[id] = info[id].period;  // Python quantises periods before creating the handle
+    if (phase[id] < duration) heap.push({phase[id], id});
+  }
+  std::unordered_map<int, int> job_slot;     // job -> buffer slot
+  std::unordered_map<int, double> job_rel;   // job -> release time
+  std::unordered_map<int, int> job_seq;      // job -> per-task sequence number
+  std::vector<std::vector<Running>> run(c.n_contexts, std::vector<Running>(c.n_streams));
+  int job_counter = 0;
+  int in_flight = 0;
+
+  auto launch = [&](const daris_stage_ref& r) -> int {
+    Partition& p = ex->parts[r.context - 1];
+    cudaStream_t s = p.streams[r.stream];
+    const int slot = job_slot[r.job];
+    const size_t si = ex->sidx(r.task, slot);
+    const TaskInfo& t = info[r.task];
+    if (r.stage == 0) {
+      const int owner = ex->slot_owner[si];
+      if (owner != 0 && owner != r.job) {
+        CUDA_TRY(ex, cudaStreamWaitEvent(s, ex->slot_free[si], 0));
+        st.slot_waits++;
+      }
+      ex->slot_owner[si] = r.job;
+      const auto& pool = ex->pools[r.task - 1];
+      if (pool.src && pool.n > 0 && ex->dev_in[si]) {
+        const char* src = pool.src + static_cast<int64_t>(job_seq[r.job] % pool.n) * pool.in_bytes;
+        CUDA_TRY(ex, cudaMemcpyAsync(ex->dev_in[si], src, static_cast<size_t>(pool.in_bytes),
+                                     pool.on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+        if (pool.on_host) {
+          st.copies_h2d++;
+          st.h2d_bytes += pool.in_bytes;
+        } else {
+          st.copies_d2d++;
+        }
+      }
+    }
+    cudaGraphExec_t g = ex->graphs[ex->gidx(r.task, r.stage, r.context, slot)];
+    if (!g) return fail(ex, "no graph for dispatched stage", DARIS_E_INTERNAL);
+    CUDA_TRY(ex, cudaGraphLaunch(g, s));
+    st.graph_launches++;
+    if (r.stage == t.n_stages - 1) {
+      const auto& pool = ex->pools[r.task - 1];
+      if (pool.host_out && pool.out_bytes > 0 && ex->dev_out[si]) {
+        CUDA_TRY(ex, cudaMemcpyAsync(pool.host_out, ex->dev_out[si], static_cast<size_t>(pool.out_bytes),
+                                     cudaMemcpyDeviceToHost, s));
+        st.copies_d2h++;
+        st.d2h_bytes += pool.out_bytes;
+      }
+      CUDA_TRY(ex, cudaEventRecord(ex->slot_free[si], s));
+    }
+    CUDA_TRY(ex, cudaEventRecord(p.done[r.stream], s));
+    Running& rr = run[r.context - 1][r.stream];
+    rr.busy = true;
+    rr.task = r.task;
+    rr.job = r.job;
+    rr.stage = r.stage;
+    rr.slot = slot;
+    rr.start = r.started_at;
+    in_flight++;
+    return DARIS_OK;
+  };
+
+  int status = DARIS_OK;
+  auto refill = [&](double t) -> int {
+    for (int k = 1; k <= c.n_contexts; ++k) {
+      for (int s = 0; s < c.n_streams; ++s) {
+        if (run[k - 1][s].busy) continue;
+        daris_stage_ref r;
+        int32_t found = 0;
+        int rc = daris_dispatch(h, k, s, t, &r, &found);
+        if (rc != DARIS_OK) return fail(ex, std::string("dispatch: ") + daris_last_error(h), rc);
+        if (!found) break;  // this context has nothing ready
+        push_log(h, t, DARIS_LOG_STAGE_START, r.task, r.job, r.stage, k, s, 1.0);
+        rc = launch(r);
+        if (rc != DARIS_OK) return rc;
+      }
+    }
+    return DARIS_OK;
+  };
+
+  const auto t0 = clock::now();
+  auto elapsed = [&]() { return std::chrono::duration<double>(clock::now() - t0).count(); };
+  struct Done {
+    int ctx, stream, job, stage;
+  };
+  std::vector<Done> done;
+  for (;;) {
+    const double now = quant(elapsed());
+    bool progressed = false;
+    // 1) due releases, in (time, task) order, each at its nominal instant
+    while (!heap.empty() && heap.top().first <= now) {
+      const Rel rel = heap.top();
+      heap.pop();
+      const int tid = rel.second;
+      const double tr = rel.first;
+      st.release_lag_max = std::max(st.release_lag_max, now - tr);
+      job_counter += 1;
+      daris_placement pl;
+      int rc = daris_release(h, tid, tr, job_counter, nullptr, &pl);
+      if (rc != DARIS_OK) {
+        status = fail(ex, std::string("release: ") + daris_last_error(h), rc);
+        break;
+      }
+      push_log(h, tr, DARIS_LOG_RELEASE, tid, job_counter);
+      const int hp = info[tid].prio == DARIS_HP ? 0 : 1;
+      if (tr >= acc.warmup) {
+        acc.rel[hp]++;
+        if (pl.context) acc.acc[hp]++;
+        else acc.rej[hp]++;
+      }
+      if (pl.context == 0) {
+        push_log(h, tr, DARIS_LOG_REJECT, tid, job_counter);
+      } else {
+        push_log(h, tr, DARIS_LOG_ADMIT, tid, job_counter, -1, pl.context);
+        job_slot[job_counter] = static_cast<int>(seq[tid] % c.slots_per_task);
+        job_seq[job_counter] = static_cast<int>(seq[tid]);
+        job_rel[job_counter] = tr;
+      }
+      seq[tid] += 1;
+      rel_idx[tid] += 1;
+      const double next = phase[tid] + static_cast<double>(rel_idx[tid]) * period[tid];
+      if (next < duration) heap.push({next, tid});
+      status = refill(tr);
+      if (status != DARIS_OK) break;
+      progressed = true;
+    }
+    if (status != DARIS_OK) break;
+    // 2) completions observed now, in (job, stage) order
+    done.clear();
+    for (int k = 0; k < c.n_contexts; ++k)
+      for (int s = 0; s < c.n_streams; ++s) {
+        Running& rr = run[k][s];
+        if (!rr.busy) continue;
+        st.polls++;
+        cudaError_t q = cudaEventQuery(ex->parts[k].done[s]);
+        if (q == cudaSuccess) done.push_back({k + 1, s, rr.job, rr.stage});
+        else if (q != cudaErrorNotReady) {
+          status = fail(ex, std::string("stage failed on the GPU: ") + cudaGetErrorString(q), DARIS_E_INTERNAL);
+          break;
+        }
+      }
+    if (status != DARIS_OK) break;
+    std::sort(done.begin(), done.end(), [](const Done& a, const Done& b) {
+      return a.job != b.job ? a.job < b.job : a.stage < b.stage;
+    });
+    for (const Done& d : done) {
+      Running& rr = run[d.ctx - 1][d.stream];
+      double t = now;
+      if (t <= rr.start) t = rr.start + kQuantum;  // a stage always takes at least one quantum
+      int32_t job_done = 0, missed = 0;
+      int rc = daris_complete(h, d.job, d.stage, t, &job_done, &missed);
+      if (rc != DARIS_OK) {
+        status = fail(ex, std::string("complete: ") + daris_last_error(h), rc);
+        break;
+      }
+      ex->trace.push_back(daris_stage_trace{rr.task, rr.job, rr.stage, d.ctx, d.stream, rr.slot, rr.start, t});
+      push_log(h, t, DARIS_LOG_STAGE_COMPLETE, rr.task, rr.job, rr.stage, d.ctx, d.stream, 1.0);
+      rr.busy = false;
+      in_flight--;
+      if (job_done) {
+        push_log(h, t, DARIS_LOG_JOB_COMPLETE, rr.task, rr.job, -1, d.ctx);
+        ex->slot_owner[ex->sidx(rr.task, rr.slot)] = 0;
+        const double released = job_rel[rr.job];
+        if (released >= acc.warmup) {
+          const int hp = info[rr.task].prio == DARIS_HP ? 0 : 1;
+          acc.cmp[hp]++;
+          acc.inputs += 1;
+          acc.resp[hp].push_back(t - released);
+          if (missed) acc.miss[hp]++;
+        }
+        job_slot.erase(rr.job);
+        job_rel.erase(rr.job);
+        job_seq.erase(rr.job);
+      }
+      status = refill(t);
+      if (status != DARIS_OK) break;
+      progressed = true;
+    }
+    if (status != DARIS_OK) break;
+    if (heap.empty() && in_flight == 0) {
+      int32_t ready = 0;
+      daris_ready_total(h, &ready);
+      if (ready == 0) break;
+      status = refill(now);  // (cannot happen with free streams, kept for safety)
+      if (status != DARIS_OK) break;
+    }
+    (void)progressed;
+  }
+  if (status != DARIS_OK) {
+    cudaDeviceSynchronize();
+    return status;
+  }
+  cudaDeviceSynchronize();
+  push_log(h, duration, DARIS_LOG_SIM_END);
+  st.wall_seconds = elapsed();
+
+  daris_report r{};
+  r.duration = duration;
+  r.warmup = warmup;
+  const double window = duration - warmup;
+  r.jps = window > 0 ? static_cast<double>(acc.inputs) / window : 0.0;
+  r.dmr_hp = acc.acc[0] ? static_cast<double>(acc.miss[0]) / acc.acc[0] : 0.0;
+  r.dmr_lp = acc.acc[1] ? static_cast<double>(acc.miss[1]) / acc.acc[1] : 0.0;
+  r.response_hp = stats_of(acc.resp[0]);
+  r.response_lp = stats_of(acc.resp[1]);
+  r.released_hp = acc.rel[0];
+  r.released_lp = acc.rel[1];
+  r.accepted_hp = acc.acc[0];
+  r.accepted_lp = acc.acc[1];
+  r.rejected_hp = acc.rej[0];
+  r.rejected_lp = acc.rej[1];
+  r.completed_hp = acc.cmp[0];
+  r.completed_lp = acc.cmp[1];
+  r.missed_hp = acc.miss[0];
+  r.missed_lp = acc.miss[1];
+  if (report) *report = r;
+  if (stats) *stats = st;
+  return DARIS_OK;
+}
+
+int daris_exec_busy_calibrate(daris_exec* ex, const int32_t* task_stage_counts, int32_t n_tasks,
+                              const int32_t* slot_tasks, double seconds, double* out_mean_job_time) {
+  using clock = std::chrono::steady_clock;
+  const daris_exec_config& c = ex->cfg;
+  const int n_slots = c.n_contexts * c.n_streams;
+  struct Loop {
+    int task, stage, ctx, stream, slot;
+    double job_start;
+  };
+  std::vector<Loop> loops(n_slots);
+  const auto t0 = clock::now();
+  auto now = [&]() { return std::chrono::duration<double>(clock::now() - t0).count(); };
+  for (int s = 0; s < n_slots; ++s) {
+    const int task = slot_tasks[s];
+    if (task < 1 || task > n_tasks) return fail(ex, "bad calibration task");
+    loops[s] = Loop{task, 0, s / c.n_streams + 1, s % c.n_streams, s % c.slots_per_task, 0.0};
+  }
+  auto go = [&](Loop& l) -> int {
+    Partition& p = ex->parts[l.ctx - 1];
+    cudaGraphExec_t g = ex->graphs[ex->gidx(l.task, l.stage, l.ctx, l.slot)];
+    if (!g) return fail(ex, "calibration needs graphs for every task in every context");
+    CUDA_TRY(ex, cudaGraphLaunch(g, p.streams[l.stream]));
+    CUDA_TRY(ex, cudaEventRecord(p.done[l.stream], p.streams[l.stream]));
+    return DARIS_OK;
+  };
+  for (auto& l : loops) {
+    l.job_start = now();
+    int rc = go(l);
+    if (rc) return rc;
+  }
+  double sum = 0;
+  long long jobs = 0;
+  while (now() < seconds || jobs == 0) {
+    for (int s = 0; s < n_slots; ++s) {
+      Loop& l = loops[s];
+      cudaError_t q = cudaEventQuery(ex->parts[l.ctx - 1].done[l.stream]);
+      if (q == cudaErrorNotReady) continue;
+      if (q != cudaSuccess) return fail(ex, cudaGetErrorString(q), DARIS_E_INTERNAL);
+      l.stage += 1;
+      if (l.stage == task_stage_counts[l.task - 1]) {
+        const double t = now();
+        if (s == 0) {
+          sum += t - l.job_start;
+          jobs++;
+        }
+        l.stage = 0;
+        l.job_start = t;
+      }
+      int rc = go(l);
+      if (rc) return rc;
+    }
+    if (now() > seconds * 20 + 5) break;  // safety
+  }
+  cudaDeviceSynchronize();
+  *out_mean_job_time = jobs ? sum / jobs : 0.0;
+  return DARIS_OK;
+}
+
+}  // extern "C"

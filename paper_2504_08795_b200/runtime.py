@@ -1,0 +1,414 @@
+"""Real-GPU DARIS runtime: partitions + stage graphs + the native executor.
+
+This is the B200 replacement of the reference's device model (gpu.py) and
+event loop (engine.py): tasks are real DNNs (nets.py) whose stages run as
+CUDA graphs of sm_100a kernels inside green-context SM partitions, scheduled
+by the native dispatcher (libdaris_core) from the native wall-clock executor
+(libdaris_gpu, include/daris_exec.h).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import random
+import time
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _core, nets
+from . import kernels as K
+from .engine import ResponseStats, report_from_native
+from .gpu import GpuConfig, Policy, sm_per_context
+from .model import Priority, StageProfile, TaskSpec, spec_to_dict
+from .scheduler import AblationFlags, SchedulerMode
+
+QUANTUM = 1.0 / 1048576.0
+
+
+def quantize(x: float) -> float:
+    return math.floor(x / QUANTUM + 0.5) * QUANTUM
+
+
+class ExecConfigC(C.Structure):
+    _fields_ = [("device", C.c_int32), ("n_contexts", C.c_int32), ("n_streams", C.c_int32),
+                ("sm_per_context", C.c_int32), ("partition_mode", C.c_int32), ("slots_per_task", C.c_int32),
+                ("max_tasks", C.c_int32), ("max_stages", C.c_int32)]
+
+
+class PartitionC(C.Structure):
+    _fields_ = [("context", C.c_int32), ("sm_count", C.c_int32), ("first_group", C.c_int32),
+                ("n_groups", C.c_int32), ("green", C.c_int32)]
+
+
+class StageTraceC(C.Structure):
+    _fields_ = [("task", C.c_int32), ("job", C.c_int32), ("stage", C.c_int32), ("context", C.c_int32),
+                ("stream", C.c_int32), ("slot", C.c_int32), ("start", C.c_double), ("end", C.c_double)]
+
+
+class ExecStatsC(C.Structure):
+    _fields_ = [("graph_launches", C.c_int64), ("copies_h2d", C.c_int64), ("copies_d2h", C.c_int64),
+                ("copies_d2d", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+                ("slot_waits", C.c_int64), ("polls", C.c_int64), ("wall_seconds", C.c_double),
+                ("release_lag_max", C.c_double)]
+
+
+_exec_lib = None
+
+
+def exec_lib() -> C.CDLL:
+    global _exec_lib
+    if _exec_lib is None:
+        _core.lib()  # load the dispatcher first (libdaris_gpu links against it)
+        L = K.lib()
+        vp, i32, i64, f64, P = C.c_void_p, C.c_int32, C.c_int64, C.c_double, C.POINTER
+        sig = {
+            "daris_exec_create": [P(ExecConfigC), P(vp), C.c_char_p, C.c_size_t],
+            "daris_exec_partition_info": [vp, i32, P(PartitionC)],
+            "daris_exec_stream": [vp, i32, i32, P(vp)],
+            "daris_exec_capture_begin": [vp, i32, P(vp)],
+            "daris_exec_capture_end": [vp, i32, i32, i32, i32],
+            "daris_exec_graph_count": [vp, P(i64)],
+            "daris_exec_set_io": [vp, i32, i32, vp, vp],
+            "daris_exec_set_pool": [vp, i32, vp, i32, i32, i64, vp, i64],
+            "daris_exec_run": [vp, vp, f64, f64, P(f64), i32, P(_core.ReportC), P(ExecStatsC)],
+            "daris_exec_busy_calibrate": [vp, P(i32), i32, P(i32), f64, P(f64)],
+        }
+        for name, args in sig.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        L.daris_exec_destroy.argtypes = [vp]
+        L.daris_exec_destroy.restype = None
+        L.daris_exec_last_error.argtypes = [vp]
+        L.daris_exec_last_error.restype = C.c_char_p
+        L.daris_exec_trace_count.argtypes = [vp]
+        L.daris_exec_trace_count.restype = C.c_int64
+        L.daris_exec_trace_copy.argtypes = [vp, P(StageTraceC), i64]
+        L.daris_exec_trace_copy.restype = C.c_int64
+        L.daris_exec_quantum.argtypes = []
+        L.daris_exec_quantum.restype = C.c_double
+        _exec_lib = L
+    return _exec_lib
+
+
+class ExecutorError(RuntimeError):
+    pass
+
+
+class Executor:
+    """Thin owner of one native daris_exec (partitions, streams, graphs)."""
+
+    def __init__(self, n_contexts: int, n_streams: int, sm_per_ctx: int, *, partition: str = "green",
+                 slots: int = 3, max_tasks: int = 64, max_stages: int = 8, device: int = 0):
+        L = exec_lib()
+        cfg = ExecConfigC(device, n_contexts, n_streams, sm_per_ctx, 0 if partition == "green" else 1, slots,
+                          max_tasks, max_stages)
+        err = C.create_string_buffer(512)
+        h = C.c_void_p()
+        rc = L.daris_exec_create(C.byref(cfg), C.byref(h), err, 512)
+        if rc != 0:
+            raise ExecutorError(f"daris_exec_create failed ({rc}): {err.value.decode()}")
+        self._h = h
+        self.n_contexts, self.n_streams, self.slots = n_contexts, n_streams, slots
+        self.partitions = []
+        for k in range(1, n_contexts + 1):
+            p = PartitionC()
+            L.daris_exec_partition_info(h, k, C.byref(p))
+            self.partitions.append({"context": p.context, "sm_count": p.sm_count, "first_group": p.first_group,
+                                    "n_groups": p.n_groups, "green": bool(p.green)})
+
+    def _c(self, rc: int, what: str) -> None:
+        if rc != 0:
+            raise ExecutorError(f"{what} failed ({rc}): {exec_lib().daris_exec_last_error(self._h).decode()}")
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            exec_lib().daris_exec_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def stream(self, context: int, stream: int) -> int:
+        out = C.c_void_p()
+        self._c(exec_lib().daris_exec_stream(self._h, context, stream, C.byref(out)), "daris_exec_stream")
+        return out.value
+
+    def capture(self, task: int, stage: int, context: int, slot: int, body) -> None:
+        s = C.c_void_p()
+        self._c(exec_lib().daris_exec_capture_begin(self._h, context, C.byref(s)), "capture_begin")
+        try:
+            body(s.value)
+        except Exception:
+            exec_lib().daris_exec_capture_end(self._h, 1, 0, context, 0)
+            raise
+        self._c(exec_lib().daris_exec_capture_end(self._h, task, stage, context, slot), "capture_end")
+
+    def graph_count(self) -> int:
+        out = C.c_int64()
+        exec_lib().daris_exec_graph_count(self._h, C.byref(out))
+        return out.value
+
+    def set_io(self, task: int, slot: int, dev_input: int, dev_output: int) -> None:
+        self._c(exec_lib().daris_exec_set_io(self._h, task, slot, dev_input, dev_output), "set_io")
+
+    def set_pool(self, task: int, pool_ptr: int, on_host: bool, n_inputs: int, in_bytes: int,
+                 host_out_ptr: int | None, out_bytes: int) -> None:
+        self._c(exec_lib().daris_exec_set_pool(self._h, task, pool_ptr, int(on_host), n_inputs, in_bytes,
+                                               host_out_ptr, out_bytes), "set_pool")
+
+    def run(self, handle: _core.Handle, duration: float, warmup: float, phases: Sequence[float]):
+        rep = _core.ReportC()
+        st = ExecStatsC()
+        ph = (C.c_double * max(1, len(phases)))(*phases)
+        rc = exec_lib().daris_exec_run(self._h, handle._h, duration, warmup, ph, 1, C.byref(rep), C.byref(st))
+        self._c(rc, "daris_exec_run")
+        return rep, st
+
+    def trace(self) -> list[tuple]:
+        L = exec_lib()
+        n = L.daris_exec_trace_count(self._h)
+        arr = (StageTraceC * max(1, n))()
+        L.daris_exec_trace_copy(self._h, arr, n)
+        return [(a.task, a.job, a.stage, a.context, a.stream, a.slot, a.start, a.end) for a in list(arr)[:n]]
+
+    def busy_calibrate(self, stage_counts: Sequence[int], slot_tasks: Sequence[int], seconds: float) -> float:
+        sc = (C.c_int32 * len(stage_counts))(*stage_counts)
+        st = (C.c_int32 * len(slot_tasks))(*slot_tasks)
+        out = C.c_double()
+        self._c(exec_lib().daris_exec_busy_calibrate(self._h, sc, len(stage_counts), st, seconds, C.byref(out)),
+                "busy_calibrate")
+        return out.value
+
+
+# ----------------------------------------------------------------------------
+# workload description
+# ----------------------------------------------------------------------------
+
+@dataclass
+class TaskDef:
+    """A periodic DNN inference task on the real GPU."""
+    id: int
+    model: str
+    priority: Priority
+    rate: float                  # jobs per second (period = 1/rate, quantised)
+    n_stages: int | None = None
+
+    @property
+    def period(self) -> float:
+        return quantize(1.0 / self.rate)
+
+
+@dataclass
+class RunResult:
+    report: object
+    stats: dict
+    trace: list
+    records: list
+    admissions: list
+    full_load: dict
+    phases: list
+    tasks: list
+    periods: dict
+    stage_nominal: dict
+    partitions: list
+
+
+class DarisRuntime:
+    """Owns networks, per-task buffers, stage graphs, a dispatcher and the executor."""
+
+    def __init__(self, tasks: Sequence[TaskDef], gpu: GpuConfig, *, slots: int = 3, partition: str = "green",
+                 window_size: int = 5, flags: AblationFlags = AblationFlags(), hpa: bool = False,
+                 stage_migration: bool = False, seed: int = 0, e2e: bool = False, pool_size: int = 64,
+                 device: int = 0):
+        if not torch.cuda.is_available():
+            raise RuntimeError("DarisRuntime needs a CUDA device (there is no CPU fallback)")
+        self.tasks = sorted(tasks, key=lambda t: t.id)
+        self.gpu = gpu
+        self.seed = seed
+        self.flags, self.hpa, self.window_size = flags, hpa, window_size
+        self.stage_migration = stage_migration
+        self.e2e = e2e
+        self.device = torch.device("cuda", device)
+        self.sm_per_ctx = sm_per_context(gpu)
+        max_stages = 8
+        self.exec = Executor(gpu.n_contexts, gpu.n_streams, self.sm_per_ctx, partition=partition, slots=slots,
+                             max_tasks=max(t.id for t in self.tasks), max_stages=max_stages, device=device)
+        self.sm_budget = min(p["sm_count"] for p in self.exec.partitions)
+        # one weight copy per model, shared by all tasks running it
+        self.nets: dict[tuple, nets.Network] = {}
+        for t in self.tasks:
+            key = (t.model, t.n_stages)
+            if key not in self.nets:
+                self.nets[key] = nets.build_network(t.model, batch=1, n_stages=t.n_stages, seed=seed,
+                                                    device=self.device)
+        self.buffers: dict[tuple[int, int], nets.TaskBuffers] = {}
+        for t in self.tasks:
+            net = self.net_of(t)
+            for s in range(slots):
+                self.buffers[(t.id, s)] = nets.allocate_buffers(net, self.sm_budget)
+        self.pool_size = pool_size
+        self._pool_cache: dict = {}
+        self._make_pools(pool_size)
+        torch.cuda.synchronize()
+        self.stage_nominal = self._measure_isolated()
+        self.handle = None
+        self.afet: dict[int, float] | None = None
+
+    def net_of(self, t: TaskDef) -> nets.Network:
+        return self.nets[(t.model, t.n_stages)]
+
+    # -- inputs ------------------------------------------------------------
+    def _make_pools(self, pool_size: int) -> None:
+        """Synthetic images x ~ N(0,1), one pool per task; device
+        resident (resident mode) or pinned host memory (end-to-end mode)."""
+        self.pools = {}
+        self.host_out = {}
+        for t in self.tasks:
+            key = (t.id, self.e2e)
+            if key not in self._pool_cache:
+                g = torch.Generator().manual_seed(self.seed * 1000 + t.id)
+                imgs = torch.randn((pool_size, 3, 224, 224), generator=g)
+                if self.e2e:
+                    self._pool_cache[key] = (imgs.pin_memory(),
+                                             torch.zeros(self.net_of(t).output_shape,
+                                                         dtype=torch.float32).pin_memory())
+                else:
+                    self._pool_cache[key] = (imgs.to(self.device), None)
+            pool, out = self._pool_cache[key]
+            self.pools[t.id] = pool
+            self.host_out[t.id] = out
+            in_bytes = 3 * 224 * 224 * 4
+            self.exec.set_pool(t.id, pool.data_ptr(), self.e2e, pool_size, in_bytes,
+                               out.data_ptr() if out is not None else None,
+                               out.numel() * 4 if out is not None else 0)
+            for s in range(self.exec.slots):
+                tb = self.buffers[(t.id, s)]
+                self.exec.set_io(t.id, s, tb.input.data_ptr(), tb.output.data_ptr())
+
+    # -- graphs ------------------------------------------------------------
+    def capture_all(self, homes: dict[int, int] | None = None) -> int:
+        """Capture one graph per (task, stage, context, slot); HP tasks only in
+        their home context when `homes` is given."""
+        n = 0
+        for t in self.tasks:
+            net = self.net_of(t)
+            ctxs = range(1, self.gpu.n_contexts + 1)
+            if homes is not None and t.priority is Priority.HP:
+                ctxs = [homes[t.id]]
+            for k in ctxs:
+                for s in range(self.exec.slots):
+                    tb = self.buffers[(t.id, s)]
+                    for st in range(net.n_stages):
+                        self.exec.capture(t.id, st, k, s,
+                                          lambda stream, st=st, tb=tb, net=net: nets.run_stage(
+                                              net, st, tb, stream, self.sm_budget))
+                        n += 1
+        return n
+
+    def _measure_isolated(self, reps: int = 20) -> dict[str, list[float]]:
+        """Isolated per-stage time of each model in one partition (nominal_time)."""
+        out = {}
+        stream = torch.cuda.Stream(device=self.device)
+        for (model, _), net in self.nets.items():
+            tb = self.buffers[(next(t.id for t in self.tasks if t.model == model), 0)]
+            times = []
+            with torch.cuda.stream(stream):
+                for st in range(net.n_stages):
+                    for _ in range(3):
+                        nets.run_stage(net, st, tb, stream.cuda_stream, self.sm_budget)
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    for _ in range(reps):
+                        nets.run_stage(net, st, tb, stream.cuda_stream, self.sm_budget)
+                    e1.record(stream)
+                    e1.synchronize()
+                    times.append(max(e0.elapsed_time(e1) / 1e3 / reps, 2 * QUANTUM))
+            out[model] = times
+        return out
+
+    # -- dispatcher ----------------------------------------------------------
+    def specs(self) -> list[TaskSpec]:
+        out = []
+        for t in self.tasks:
+            nom = self.stage_nominal[t.model]
+            stages = tuple(StageProfile(float(x), self.sm_per_ctx) for x in nom)
+            out.append(TaskSpec.periodic(t.id, t.period, t.priority, stages))
+        return out
+
+    def open_dispatcher(self, full_load: dict[int, float]) -> _core.Handle:
+        dicts = [spec_to_dict(s) for s in self.specs()]
+        opts = _core.options_struct(window_size=self.window_size, no_last=self.flags.no_last,
+                                    no_prior=self.flags.no_prior, no_fixed=self.flags.no_fixed, hpa=self.hpa,
+                                    stage_migration=self.stage_migration)
+        h = _core.Handle(self.gpu.native(), dicts, opts)
+        h.set_full_load([full_load[i] for i in h.task_ids])
+        h.populate()
+        return h
+
+    def calibrate_full_load(self, seconds: float = 0.2) -> dict[int, float]:
+        """AFET on the GPU (timing.py:147-218 made real): each distinct model is
+        timed on ctx 1 / stream 0 while every other slot loops random tasks."""
+        if self.exec.graph_count() == 0:
+            self.capture_all()
+        rng = random.Random(self.seed * 7919)
+        n_slots = self.gpu.n_contexts * self.gpu.n_streams
+        ids = [t.id for t in self.tasks]
+        counts = [self.net_of(t).n_stages for t in self.tasks]
+        by_model: dict[str, float] = {}
+        out = {}
+        for t in self.tasks:
+            if t.model not in by_model:
+                slot_tasks = [t.id] + [rng.choice(ids) for _ in range(n_slots - 1)]
+                by_model[t.model] = quantize(max(self.exec.busy_calibrate(counts, slot_tasks, seconds),
+                                                 2 * QUANTUM))
+            out[t.id] = by_model[t.model]
+        self.afet = out
+        return out
+
+    def phases(self) -> list[float]:
+        rng = random.Random(self.seed)
+        return [quantize(rng.random() * t.period) for t in self.tasks]
+
+    def set_rate(self, rate: float) -> None:
+        """Same per-task release rate for every task (periods are quantised)."""
+        for t in self.tasks:
+            t.rate = rate
+
+    def use_host_io(self, on: bool) -> None:
+        """Switch between device-resident input pools and pinned-host pools with
+        H2D input / D2H logits copies every job (end-to-end mode)."""
+        if on != self.e2e:
+            self.e2e = on
+            self._make_pools(self.pool_size)
+            torch.cuda.synchronize()
+
+    def run(self, duration: float, warmup: float, *, full_load: dict[int, float] | None = None) -> RunResult:
+        if self.exec.graph_count() == 0:
+            self.capture_all()
+        if full_load is None:
+            full_load = self.afet if self.afet is not None else self.calibrate_full_load()
+        h = self.open_dispatcher(full_load)
+        torch.cuda.synchronize()
+        phases = self.phases()
+        rep, st = self.exec.run(h, quantize(duration), quantize(warmup), phases)
+        self.handle = h
+        report = report_from_native(rep, label=f"{self.gpu.n_contexts}x{self.gpu.n_streams}_"
+                                                f"{self.gpu.oversubscription:g}", config=self.gpu,
+                                    seed=self.seed)
+        stats = {f: getattr(st, f) for f, _ in ExecStatsC._fields_}
+        records = _core.records_from_array(h.log_array())
+        from .scheduler import AdmissionDecision
+        admissions = [AdmissionDecision.from_native(a) for a in h.audits()]
+        return RunResult(report, stats, self.exec.trace(), records, admissions, full_load, phases,
+                         self.specs(), {t.id: t.period for t in self.tasks}, self.stage_nominal,
+                         self.exec.partitions)
+
+    def close(self) -> None:
+        self.exec.close()
