@@ -17,6 +17,8 @@ static inline int grid_for(long long work, int block) {
 // one thread per (output pixel, 8-wide K chunk)
 __global__ void stem_im2col_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out, int n, int c, int h,
                                    int w, int kh, int kw, int stride, int pad, int ho, int wo, int kpad) {
+  pdl_wait();
+  pdl_trigger();
   const int chunks = kpad / 8;
   const long long total = static_cast<long long>(n) * ho * wo * chunks;
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -51,6 +53,8 @@ __global__ void stem_im2col_kernel(const float* __restrict__ x, __nv_bfloat16* _
 
 __global__ void pack_nhwc_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out, int n, int c, int h,
                                  int w, int cpad) {
+  pdl_wait();
+  pdl_trigger();
   const int chunks = cpad / 8;
   const long long total = static_cast<long long>(n) * h * w * chunks;
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -76,6 +80,8 @@ __global__ void pack_nhwc_kernel(const float* __restrict__ x, __nv_bfloat16* __r
 // one thread per (output pixel, 8 channels)
 __global__ void maxpool_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y, int n, int h,
                                int w, int c, int k, int stride, int pad, int ho, int wo) {
+  pdl_wait();
+  pdl_trigger();
   const int chunks = c / 8;
   const long long total = static_cast<long long>(n) * ho * wo * chunks;
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -114,6 +120,8 @@ __global__ void maxpool_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat1
 
 // one thread per (image, 8 channels); hw is small (49) so a serial loop is fine
 __global__ void avgpool_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ y, int n, int hw, int c) {
+  pdl_wait();
+  pdl_trigger();
   const int chunks = c / 8;
   const int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= n * chunks) return;
@@ -165,6 +173,8 @@ __device__ __forceinline__ void load_x8(const void* x, int x_bf16, size_t off, f
 __global__ void linear_kernel(const void* __restrict__ x, int x_bf16, const __nv_bfloat16* __restrict__ w,
                               const float* __restrict__ bias, void* __restrict__ y, int y_bf16, int batch, int k,
                               int o, int relu) {
+  pdl_wait();
+  pdl_trigger();
   const int warps_per_block = blockDim.x >> 5;
   const int out_idx = blockIdx.x * warps_per_block + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -215,6 +225,8 @@ __global__ void dwconv_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16
                               const __nv_bfloat16* __restrict__ wt, const float* __restrict__ scale,
                               const float* __restrict__ bias, int n, int h, int w, int c, int k, int stride, int pad,
                               int ho, int wo, int relu) {
+  pdl_wait();
+  pdl_trigger();
   const int chunks = c / 8;
   const long long total = static_cast<long long>(n) * ho * wo * chunks;
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -268,9 +280,9 @@ extern "C" int daris_stem_im2col(const float* x, void* out, int32_t n, int32_t c
   if (!x || !out) return DARIS_K_BAD_ARG;
   if (kpad % 64 != 0 || kpad < c * kh * kw) return DARIS_K_BAD_SHAPE;
   const long long work = static_cast<long long>(n) * ho * wo * (kpad / 8);
-  stem_im2col_kernel<<<grid_for(work, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  cudaError_t return_code = launch_pdl(stem_im2col_kernel, dim3(grid_for(work, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream),
       x, static_cast<__nv_bfloat16*>(out), n, c, h, w, kh, kw, stride, pad, ho, wo, kpad);
-  return static_cast<int>(cudaGetLastError());
+  return static_cast<int>(return_code);
 }
 
 extern "C" int daris_pack_nhwc(const float* x, void* out, int32_t n, int32_t c, int32_t h, int32_t w, int32_t cpad,
@@ -278,9 +290,9 @@ extern "C" int daris_pack_nhwc(const float* x, void* out, int32_t n, int32_t c, 
   if (!x || !out) return DARIS_K_BAD_ARG;
   if (cpad % 8 != 0 || cpad < c) return DARIS_K_BAD_SHAPE;
   const long long work = static_cast<long long>(n) * h * w * (cpad / 8);
-  pack_nhwc_kernel<<<grid_for(work, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  cudaError_t return_code = launch_pdl(pack_nhwc_kernel, dim3(grid_for(work, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream),
       x, static_cast<__nv_bfloat16*>(out), n, c, h, w, cpad);
-  return static_cast<int>(cudaGetLastError());
+  return static_cast<int>(return_code);
 }
 
 extern "C" int daris_maxpool(const void* x, void* y, int32_t n, int32_t h, int32_t w, int32_t c, int32_t k,
@@ -288,18 +300,18 @@ extern "C" int daris_maxpool(const void* x, void* y, int32_t n, int32_t h, int32
   if (!x || !y) return DARIS_K_BAD_ARG;
   if (c % 8 != 0) return DARIS_K_BAD_SHAPE;
   const long long work = static_cast<long long>(n) * ho * wo * (c / 8);
-  maxpool_kernel<<<grid_for(work, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  cudaError_t return_code = launch_pdl(maxpool_kernel, dim3(grid_for(work, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream),
       static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), n, h, w, c, k, stride, pad, ho, wo);
-  return static_cast<int>(cudaGetLastError());
+  return static_cast<int>(return_code);
 }
 
 extern "C" int daris_avgpool(const void* x, float* y, int32_t n, int32_t hw, int32_t c, void* stream) {
   if (!x || !y) return DARIS_K_BAD_ARG;
   if (c % 8 != 0) return DARIS_K_BAD_SHAPE;
   const int work = n * (c / 8);
-  avgpool_kernel<<<grid_for(work, 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+  cudaError_t return_code = launch_pdl(avgpool_kernel, dim3(grid_for(work, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream),
       static_cast<const __nv_bfloat16*>(x), y, n, hw, c);
-  return static_cast<int>(cudaGetLastError());
+  return static_cast<int>(return_code);
 }
 
 extern "C" int daris_linear(const void* x, int32_t x_bf16, const void* w, const float* bias, void* y, int32_t y_bf16,
@@ -307,9 +319,9 @@ extern "C" int daris_linear(const void* x, int32_t x_bf16, const void* w, const 
   if (!x || !w || !y) return DARIS_K_BAD_ARG;
   if (k % 8 != 0 || batch < 1 || o < 1) return DARIS_K_BAD_SHAPE;
   const int warps = 8;
-  linear_kernel<<<(o + warps - 1) / warps, warps * 32, 0, static_cast<cudaStream_t>(stream)>>>(
+  cudaError_t return_code = launch_pdl(linear_kernel, dim3((o + warps - 1) / warps), dim3(warps * 32), 0, static_cast<cudaStream_t>(stream), 
       x, x_bf16, static_cast<const __nv_bfloat16*>(w), bias, y, y_bf16, batch, k, o, relu);
-  return static_cast<int>(cudaGetLastError());
+  return static_cast<int>(return_code);
 }
 
 extern "C" int daris_dwconv(const void* x, void* y, const void* weight, const float* scale, const float* bias,
@@ -318,8 +330,8 @@ extern "C" int daris_dwconv(const void* x, void* y, const void* weight, const fl
   if (!x || !y || !weight || !scale || !bias) return DARIS_K_BAD_ARG;
   if (c % 8 != 0) return DARIS_K_BAD_SHAPE;
   const long long work = static_cast<long long>(n) * ho * wo * (c / 8);
-  dwconv_kernel<<<grid_for(work, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  cudaError_t return_code = launch_pdl(dwconv_kernel, dim3(grid_for(work, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream),
       static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y),
       static_cast<const __nv_bfloat16*>(weight), scale, bias, n, h, w, c, k, stride, pad, ho, wo, relu);
-  return static_cast<int>(cudaGetLastError());
+  return static_cast<int>(return_code);
 }

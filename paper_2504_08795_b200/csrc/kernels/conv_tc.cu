@@ -12,9 +12,15 @@
 //   warp 4     weight producer: one TMA 2D box {64, BN} per K block; owns TMEM.
 //   warp 5     MMA issuer: one thread, 4 x tcgen05.mma (K=16) per K block.
 //
-// Split-K (small-M layers at batch 1): each split writes fp32 partials to a
-// workspace; the last CTA of a tile (atomic ticket) reduces them in split
-// order (deterministic) and runs the epilogue, then re-arms the ticket.
+// Split-K (small-M layers at batch 1): every split reduces its fp32 partial
+// tile into a zeroed per-tile accumulator with red.global.add.v4.f32 (at L2);
+// the last CTA of a tile (atomic ticket) reads the sum once, runs the epilogue
+// and re-zeroes the accumulator and the ticket for the next launch.
+//
+// Programmatic dependent launch: weights do not depend on the previous layer,
+// so the TMA warp starts streaming them before griddepcontrol.wait; the
+// activation producers wait, and every CTA triggers its dependents as soon as
+// its mainloop is done so the next layer's prologue overlaps this epilogue.
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <cstdio>
@@ -160,6 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         iw0[p] = -1 << 20;
       }
     }
+    pdl_wait();  // activations come from the previous layer
     const uint32_t sA_u32 = smem_u32(sA);
     for (int i = 0; i < nkb; ++i) {
       const int s = i % kStages;
@@ -194,6 +201,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
     mbar_wait(tmem_full, 0);
     tc_fence_after();
+    if (threadIdx.x == 0) pdl_trigger();  // mainloop done: let the next layer start its prologue
     const int row = warp * 32 + lane;
     const int m = m0 + row;
     const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
@@ -206,16 +214,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     } else {
       const int tile = tile_m * gridDim.y + tile_n;
-      float* part = a.ws + (static_cast<size_t>(tile) * a.splits + split) * (kBM * BN) + static_cast<size_t>(row) * BN;
+      float* acc_row = a.ws + static_cast<size_t>(tile) * (kBM * BN) + static_cast<size_t>(row) * BN;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(t_row + c0, r);
-        float4* dst = reinterpret_cast<float4*>(part + c0);
+        if (m < a.M) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                               __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+          for (int q = 0; q < 8; ++q)
+            red_add_v4(acc_row + c0 + 4 * q, __uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                       __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+        }
       }
       __threadfence();
       asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -226,31 +235,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (*last_flag) {
         __threadfence();
-        const float* base = a.ws + static_cast<size_t>(tile) * a.splits * (kBM * BN) + static_cast<size_t>(row) * BN;
+        if (m < a.M) {
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          float acc[32];
-#pragma unroll
-          for (int j = 0; j < 32; ++j) acc[j] = 0.f;
-          for (int sp = 0; sp < a.splits; ++sp) {
-            const float4* src = reinterpret_cast<const float4*>(base + static_cast<size_t>(sp) * (kBM * BN) + c0);
+          for (int c0 = 0; c0 < BN; c0 += 32) {
+            float acc[32];
+            float4* src = reinterpret_cast<float4*>(acc_row + c0);
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
               float4 f = __ldcg(src + q);
-              acc[4 * q] += f.x;
-              acc[4 * q + 1] += f.y;
-              acc[4 * q + 2] += f.z;
-              acc[4 * q + 3] += f.w;
+              acc[4 * q] = f.x;
+              acc[4 * q + 1] = f.y;
+              acc[4 * q + 2] = f.z;
+              acc[4 * q + 3] = f.w;
+              __stcg(src + q, make_float4(0.f, 0.f, 0.f, 0.f));  // re-arm for the next launch
             }
+            finalize_row32(a, m, n0 + c0, acc);
           }
-          finalize_row32(a, m, n0 + c0, acc);
         }
-        if (threadIdx.x == 0) a.counters[tile] = 0;  // re-arm for the next launch
+        if (threadIdx.x == 0) a.counters[tile] = 0;
       }
     }
   } else if (warp == 4) {
     // ---------------- weight producer (TMA) ----------------
     if (lane == 0) {
+      // weights are constant: stream them before waiting on the previous layer
       for (int i = 0; i < nkb; ++i) {
         const int s = i % kStages;
         if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
@@ -341,9 +349,17 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   a.num_kb = d->kh * d->kw * a.cin_blocks;
   a.kb_per_split = pl.kb_per_split;
   a.splits = pl.splits;
-  dim3 grid(pl.tiles_m, pl.tiles_n, pl.splits);
-  conv_igemm_tc_kernel<BN><<<grid, kThreads, L::kTotal, st>>>(map, a);
-  return static_cast<int>(cudaGetLastError());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pl.tiles_m, pl.tiles_n, pl.splits);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = L::kTotal;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN>, map, a));
 }
 
 }  // namespace daris
@@ -398,7 +414,7 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
   out->kb_per_split = kbps;
   out->tiles_m = tiles_m;
   out->tiles_n = tiles_n;
-  out->workspace_floats = splits > 1 ? static_cast<int64_t>(tiles) * splits * kBM * bn : 0;
+  out->workspace_floats = splits > 1 ? static_cast<int64_t>(tiles) * kBM * bn : 0;  // zero-initialised
   out->counters = splits > 1 ? tiles : 0;
   out->ctas = tiles * splits;
   return DARIS_K_OK;

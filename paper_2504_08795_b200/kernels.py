@@ -109,7 +109,7 @@ def conv2d(x: torch.Tensor, weight: torch.Tensor, scale: torch.Tensor, bias: tor
         out = torch.empty((d.n, d.ho, d.wo, cout), dtype=torch.bfloat16, device=x.device)
     if p.splits > 1:
         if workspace is None or workspace.numel() < p.workspace_floats:
-            workspace = torch.empty(p.workspace_floats, dtype=torch.float32, device=x.device)
+            workspace = torch.zeros(p.workspace_floats, dtype=torch.float32, device=x.device)
         if counters is None or counters.numel() < p.counters:
             counters = torch.zeros(p.counters, dtype=torch.int32, device=x.device)
     d.x, d.y, d.residual, d.weight = _ptr(x), _ptr(out), _ptr(residual), _ptr(weight)

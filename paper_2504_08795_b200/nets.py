@@ -478,7 +478,7 @@ def allocate_buffers(net: Network, sm_budget: int = 0) -> TaskBuffers:
             p = K.conv_plan(d)
             ws = max(ws, p.workspace_floats)
             ctr = max(ctr, p.counters)
-    return TaskBuffers(bufs, torch.empty(ws, dtype=torch.float32, device=net.device),
+    return TaskBuffers(bufs, torch.zeros(ws, dtype=torch.float32, device=net.device),
                        torch.zeros(ctr, dtype=torch.int32, device=net.device))
 
 

@@ -103,13 +103,15 @@ def test_conv_split_k_repeat_resets_counters():
     d = K.conv_desc((1, 7, 7, 512), 512, 3, 3, 1, 1, sm_budget=148)
     p = K.conv_plan(d)
     assert p.splits > 1
-    ws = torch.empty(p.workspace_floats, device=dev)
+    ws = torch.zeros(p.workspace_floats, device=dev)
     ctr = torch.zeros(p.counters, dtype=torch.int32, device=dev)
-    outs = [K.conv2d(x, wt, s, b, pad=1, workspace=ws, counters=ctr, sm_budget=148) for _ in range(3)]
+    outs = [K.conv2d(x, wt, s, b, pad=1, workspace=ws, counters=ctr, sm_budget=148).clone() for _ in range(3)]
     torch.cuda.synchronize()
-    assert int(ctr.abs().sum()) == 0
+    assert int(ctr.abs().sum()) == 0          # tickets re-armed
+    assert float(ws.abs().sum()) == 0.0       # accumulators re-zeroed
+    # fp32 atomics reorder the split sums: equal up to bf16 output rounding
     for o in outs[1:]:
-        assert torch.equal(o, outs[0])
+        assert (o.float() - outs[0].float()).abs().max().item() <= 2e-2 * outs[0].float().abs().max().item()
 
 
 def test_stem_im2col_gemm_matches_conv7x7():
