@@ -142,42 +142,89 @@ def feasible(rep) -> bool:
 
 
 def conv_roofline(rt, peaks) -> dict:
-    """Dominant kernel (conv_igemm_tc_kernel): algorithmic FLOPs / CUDA-event time
-    per launch, measured on a partition stream of the live executor."""
+    """Dominant kernel (conv_igemm_tc_kernel): algorithmic FLOPs per launch ÷ the
+    launch's CUDA-event time on a live partition stream (each op captured 10x in
+    a graph so host launch cost is excluded)."""
     import torch
     from paper_2504_08795_b200 import nets
     net = next(iter(rt.nets.values()))
     tb = rt.buffers[(rt.tasks[0].id, 0)]
-    stream_ptr = rt.exec.stream(1, 0)
-    s = torch.cuda.ExternalStream(stream_ptr)
-    convs = [op for op in net.ops if op.kind == "conv"]
-    total_flops = sum(op.flops for op in convs)
-    times = []
-    other = []
+    sp = rt.exec.stream(1, 0)
+    s = torch.cuda.ExternalStream(sp)
+    reps = 10
+    per_op = []
     with torch.cuda.stream(s):
-        for rep in range(6):
-            ev = []
-            for op in net.ops:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(s)
-                nets.run_op(op, tb, stream_ptr, rt.sm_budget)
-                e1.record(s)
-                ev.append((op, e0, e1))
-            s.synchronize()
-            if rep >= 2:
-                times.append(sum(e0.elapsed_time(e1) for op, e0, e1 in ev if op.kind == "conv") / 1e3)
-                other.append(sum(e0.elapsed_time(e1) for op, e0, e1 in ev if op.kind != "conv") / 1e3)
-    t_conv = statistics.median(times)
-    t_other = statistics.median(other)
-    achieved = total_flops / t_conv / 1e12
-    per_launch_us = t_conv / len(convs) * 1e6
+        for op in net.ops:
+            g = torch.cuda.CUDAGraph()
+            g.capture_begin()
+            for _ in range(reps):
+                nets.run_op(op, tb, sp, rt.sm_budget)
+            g.capture_end()
+            g.replay()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(3):
+                g.replay()
+            e1.record(s)
+            e1.synchronize()
+            per_op.append((op, e0.elapsed_time(e1) / 1e3 / (3 * reps)))
+    conv = [(op, t) for op, t in per_op if op.kind == "conv"]
+    t_conv = sum(t for _, t in conv)
+    t_all = sum(t for _, t in per_op)
+    flops = sum(op.flops for op, _ in conv)
+    achieved = flops / t_conv / 1e12
     return {"kernel": "conv_igemm_tc_kernel", "bound": "tensor", "achieved": round(achieved, 3),
             "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_tflops"], 5),
-            "traffic": None, "launches_per_inference": len(convs),
-            "flops_per_launch_avg": total_flops // len(convs), "avg_launch_us": round(per_launch_us, 3),
-            "share_of_inference": round(t_conv / (t_conv + t_other), 4),
+            "traffic": 1173248, "traffic_note": "dram bytes (read+write) of one layer3 split-K conv launch, "
+                                                "ncu --set full (profiles/r01_conv_ncu_full_raw.csv)",
+            "launches_per_inference": len(conv), "flops_per_launch_avg": flops // len(conv),
+            "avg_launch_us": round(t_conv / len(conv) * 1e6, 3), "share_of_inference": round(t_conv / t_all, 4),
             "partition_sms": rt.sm_budget, "peak_kind": f"bf16 dense burst ({peaks['source']})"}
+
+
+def batching_baseline(batches=(1, 2, 4, 8, 16, 32), reps: int = 20) -> dict:
+    """Single-tenant batched inference of the same model with the same kernels on
+    the whole GPU (one 148-SM green partition, one stream, one CUDA graph per
+    forward incl. the D2D copy of B distinct inputs): inferences/s per batch."""
+    import torch
+    from paper_2504_08795_b200 import nets
+    from paper_2504_08795_b200.runtime import Executor
+    ex = Executor(1, 1, 148, slots=1, max_tasks=1, max_stages=8)
+    sm = ex.partitions[0]["sm_count"]
+    sp = ex.stream(1, 0)
+    s = torch.cuda.ExternalStream(sp)
+    model = nets.make_torch_model("resnet50", 0)
+    pool = torch.randn((64, 3, 224, 224), generator=torch.Generator().manual_seed(5)).cuda()
+    out = {}
+    for b in batches:
+        net = nets.build_network("resnet50", batch=b, n_stages=1, model=model)
+        tb = nets.allocate_buffers(net, sm_budget=sm)
+        src = pool[:b] if b <= 64 else pool.repeat((b + 63) // 64, 1, 1, 1)[:b]
+        with torch.cuda.stream(s):
+            tb.input.copy_(src)
+            nets.run_stage(net, 0, tb, sp, sm)
+            g = torch.cuda.CUDAGraph()
+            g.capture_begin()
+            tb.input.copy_(src)
+            nets.run_stage(net, 0, tb, sp, sm)
+            g.capture_end()
+            for _ in range(3):
+                g.replay()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(reps):
+                g.replay()
+            e1.record(s)
+        e1.synchronize()
+        lat = e0.elapsed_time(e1) / 1e3 / reps
+        out[str(b)] = {"inf_per_s": round(b / lat, 1), "latency_ms": round(lat * 1e3, 3)}
+        del net, tb, g
+    ex.close()
+    best = max(out.items(), key=lambda kv: kv[1]["inf_per_s"])
+    return {"per_batch": out, "best_batch": int(best[0]), "best_inf_per_s": best[1]["inf_per_s"],
+            "setup": "resnet50, one 148-SM green partition, one stream, CUDA graph per forward, same kernels"}
 
 
 def knee_search(rt, build_rate: float, probe_s: float, log) -> float:
@@ -290,6 +337,8 @@ def ours(args) -> dict | None:
     rt.use_host_io(False)
 
     roof = conv_roofline(rt, peaks) if rank == 0 else None
+    rt.close()
+    batching = batching_baseline() if (rank == 0 and not args.no_batching) else None
     cpu = cpu_reference(args.cpu_seconds) if (rank == 0 and world == 1 and not args.no_cpu) else None
     flops_inf = next(iter(rt.nets.values())).flops_per_image
     out = None
@@ -309,6 +358,8 @@ def ours(args) -> dict | None:
                        "timing": "host steady clock over the periodic schedule, barrier + synchronize both "
                                  "sides, max over ranks; stage completions via CUDA events"},
             "hp_miss": int(tot[1]), "dmr_lp": (tot[2] / tot[4]) if tot[4] else 0.0,
+            "executor_stats": {k: res.stats[k] for k in ("graph_launches", "slot_waits", "polls",
+                                                          "release_lag_max", "loop_gap_max", "wall_seconds")},
             "p99_hp_response_ms": round(p99 * 1e3, 3), "p95_hp_response_ms": round(rep.response_hp.p95 * 1e3, 3),
             "mean_hp_response_ms": round(rep.response_hp.mean * 1e3, 3), "rejected_lp": int(tot[6]),
             "e2e": e2e, "gpu_launches": int(tot[5]), "clocks": clocks, "roofline": roof,
@@ -317,8 +368,10 @@ def ours(args) -> dict | None:
                                "frac": round(value * flops_inf / 1e12 / (peaks["bf16_tflops_sustained"] * world), 5),
                                "flops_per_inference": flops_inf},
             "cpu_baseline": cpu,
+            "batching_baseline": batching,
+            "vs_single_tenant_batching": (round(value / world / batching["best_inf_per_s"], 4)
+                                          if batching else None),
         }
-    rt.close()
     return out
 
 
@@ -402,9 +455,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--step-seconds", type=float, default=0.25)
-    ap.add_argument("--probe-seconds", type=float, default=0.6)
+    ap.add_argument("--probe-seconds", type=float, default=1.0)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-batching", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -59,6 +59,7 @@ typedef struct daris_exec_stats {
   int64_t polls;
   double wall_seconds;      /* host wall time of the run incl. drain */
   double release_lag_max;   /* worst delay between a nominal release and its processing */
+  double loop_gap_max;      /* longest host gap between two polling passes (host stalls) */
 } daris_exec_stats;
 
 typedef struct daris_exec daris_exec;

@@ -34,7 +34,8 @@ enum daris_kstatus {
 /* Implicit-GEMM convolution on tcgen05 (TMEM accumulators, TMA-fed weights,
  * cp.async-gathered activations) with a fused epilogue:
  *   y = act(conv(x, w) * scale + bias [+ residual])
- * Requirements: cin % 64 == 0, cout % 64 == 0.
+ * Requirements: cin % 64 == 0 (or cin == 8: stem mode, NHWC8 input, K = kh*kw*8
+ * zero-padded by TMA to a multiple of 64), cout % 64 == 0.
  * Split-K is used when the output tile count is small against `sm_budget`
  * (the SM count of the partition the stage runs in). */
 typedef struct daris_conv_desc {
@@ -51,6 +52,8 @@ typedef struct daris_conv_desc {
   int32_t block_n;        /* 0 = auto, else 64/128/256 */
   int32_t splits;         /* 0 = auto, else forced split-K factor */
   int32_t sm_budget;      /* SMs available to this launch (0 = whole device) */
+  int32_t _pad;
+  void* timestamps;       /* optional: 8 uint64 globaltimer stamps per CTA (profiling), or NULL */
 } daris_conv_desc;
 
 typedef struct daris_conv_plan_t {

@@ -60,7 +60,8 @@ Driver& driver() {
 struct Partition {
   int sm_count = 0, first_group = 0, n_groups = 0;
   CUgreenCtx green = nullptr;
-  std::vector<cudaStream_t> streams;
+  std::vector<cudaStream_t> streams;     // low (default) priority: LP stages
+  std::vector<cudaStream_t> streams_hi;  // highest priority: HP stages (CTA scheduling preference)
   std::vector<cudaEvent_t> done;
   cudaStream_t capture = nullptr;
 };
@@ -166,18 +167,22 @@ int build_partitions(daris_exec* ex) {
         return fail(ex, "green context creation failed", DARIS_E_INTERNAL);
       }
     }
-    const int n_streams = c.n_streams + 1;  // + capture stream
+    int prio_low = 0, prio_high = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
+    const int n_streams = 2 * c.n_streams + 1;  // low + high priority per slot, + capture stream
     for (int s = 0; s < n_streams; ++s) {
+      const int prio = (s >= c.n_streams && s < 2 * c.n_streams) ? prio_high : prio_low;
       cudaStream_t st;
       if (p.green) {
         CUstream cs;
-        if (d.greenStream(&cs, p.green, CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS)
+        if (d.greenStream(&cs, p.green, CU_STREAM_NON_BLOCKING, prio) != CUDA_SUCCESS)
           return fail(ex, "green stream creation failed", DARIS_E_INTERNAL);
         st = reinterpret_cast<cudaStream_t>(cs);
       } else {
-        CUDA_TRY(ex, cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        CUDA_TRY(ex, cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, prio));
       }
       if (s < c.n_streams) p.streams.push_back(st);
+      else if (s < 2 * c.n_streams) p.streams_hi.push_back(st);
       else p.capture = st;
     }
     for (int s = 0; s < c.n_streams; ++s) {
@@ -278,6 +283,7 @@ void daris_exec_destroy(daris_exec* ex) {
   for (auto& p : ex->parts) {
     for (auto e : p.done) cudaEventDestroy(e);
     for (auto s : p.streams) cudaStreamDestroy(s);
+    for (auto s : p.streams_hi) cudaStreamDestroy(s);
     if (p.capture) cudaStreamDestroy(p.capture);
     if (p.green && driver().greenDestroy) driver().greenDestroy(p.green);
   }
@@ -416,10 +422,10 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
 
   auto launch = [&](const daris_stage_ref& r) -> int {
     Partition& p = ex->parts[r.context - 1];
-    cudaStream_t s = p.streams[r.stream];
+    const TaskInfo& t = info[r.task];
+    cudaStream_t s = (t.prio == DARIS_HP ? p.streams_hi : p.streams)[r.stream];
     const int slot = job_slot[r.job];
     const size_t si = ex->sidx(r.task, slot);
-    const TaskInfo& t = info[r.task];
     if (r.stage == 0) {
       const int owner = ex->slot_owner[si];
       if (owner != 0 && owner != r.job) {
@@ -490,8 +496,12 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
     int ctx, stream, job, stage;
   };
   std::vector<Done> done;
+  double last_pass = 0.0;
   for (;;) {
-    const double now = quant(elapsed());
+    const double raw_now = elapsed();
+    if (raw_now - last_pass > st.loop_gap_max) st.loop_gap_max = raw_now - last_pass;
+    last_pass = raw_now;
+    const double now = quant(raw_now);
     bool progressed = false;
     // 1) due releases, in (time, task) order, each at its nominal instant
     while (!heap.empty() && heap.top().first <= now) {

@@ -2,7 +2,9 @@
 //
 // GEMM view: M = n*ho*wo output pixels, N = cout, K = kh*kw*cin with K ordered
 // (kh, kw, cin) so one 64-wide K block is 64 contiguous NHWC channels of one
-// input pixel (128 B). Per CTA: a 128 x BN output tile, fp32 accumulator in
+// input pixel (128 B). Stems (cin = 8 after padding 3 -> 8 channels) use
+// "pixel chunks": each 16-B chunk of a K block is one kernel position's 8
+// channels, so a 7x7 stem is 7 K blocks gathered straight from NHWC8. Per CTA: a 128 x BN output tile, fp32 accumulator in
 // TMEM (BN columns), a STAGES-deep smem ring.
 //
 //   warps 0-3  activation producers: cp.async gather of 128 rows x 128 B per
@@ -24,6 +26,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include "sm100.cuh"
 #include "../../../include/daris_kernels.h"
@@ -32,9 +35,13 @@ namespace daris {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;            // bf16 elements per K block = 128 B rows
-constexpr int kStages = 4;
-constexpr int kLag = 2;            // cp.async groups kept in flight per producer thread
 constexpr int kThreads = 192;
+// Pipeline depth per tile width: shallow rings keep smem per CTA small so three
+// CTAs (of different tenants' kernels) fit on one SM — at batch 1 the layers
+// are latency-bound and co-residency, not pipeline depth, sets throughput.
+template <int BN> struct Depth { static constexpr int kStages = 3; };
+template <> struct Depth<128> { static constexpr int kStages = 2; };
+template <> struct Depth<256> { static constexpr int kStages = 2; };
 
 struct ConvArgs {
   const __nv_bfloat16* x;
@@ -46,10 +53,19 @@ struct ConvArgs {
   int* counters;
   int n, h, w, cin, cout, kh, kw, stride, pad, ho, wo;
   int M, relu, num_kb, kb_per_split, splits, cin_blocks;
+  unsigned long long* ts;  // optional per-CTA phase timestamps (globaltimer ns), 8 per CTA
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <int BN>
 struct SmemLayout {
+  static constexpr int kStages = Depth<BN>::kStages;
+  static constexpr int kLag = kStages - 1;  // cp.async groups kept in flight per producer thread
   static constexpr int kABytes = kBM * 128;
   static constexpr int kBBytes = BN * 128;
   static constexpr int kAOff = 0;
@@ -106,9 +122,11 @@ __device__ __forceinline__ void finalize_row32(const ConvArgs& a, int m, int col
 }
 
 template <int BN>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 3)
     conv_igemm_tc_kernel(const __grid_constant__ CUtensorMap wmap, const ConvArgs a) {
   using L = SmemLayout<BN>;
+  constexpr int kStages = L::kStages;
+  constexpr int kLag = L::kLag;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem + L::kAOff;
@@ -122,6 +140,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int tile_m = blockIdx.x, tile_n = blockIdx.y, split = blockIdx.z;
+  unsigned long long* ts = a.ts ? a.ts + 8ull * (blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) : nullptr;
+  if (ts && threadIdx.x == 0) ts[0] = gtimer();
   const int m0 = tile_m * kBM, n0 = tile_n * BN;
   const int kb_begin = split * a.kb_per_split;
   const int kb_end = min(a.num_kb, kb_begin + a.kb_per_split);
@@ -143,6 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (ts && threadIdx.x == 0) ts[1] = gtimer();
 
   if (warp < 4) {
     // ---------------- activation producer ----------------
@@ -167,22 +188,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     pdl_wait();  // activations come from the previous layer
+    if (ts && threadIdx.x == 0) ts[2] = gtimer();
     const uint32_t sA_u32 = smem_u32(sA);
     for (int i = 0; i < nkb; ++i) {
       const int s = i % kStages;
       if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
       const int kb = kb_begin + i;
-      const int kpos = kb / a.cin_blocks;
-      const int cb = kb - kpos * a.cin_blocks;
+      // K block -> (kernel position, channel offset) of this thread's 16-B chunk.
+      // Normal layers: one position per K block, 64 channels. Stem layers
+      // (cin == 8, "pixel chunks"): every chunk is one position's 8 channels.
+      int kpos, coff;
+      if (a.cin == 8) {
+        kpos = kb * 8 + chunk;
+        coff = 0;
+      } else {
+        kpos = kb / a.cin_blocks;
+        coff = (kb - kpos * a.cin_blocks) * kBK + chunk * 8;
+      }
+      const bool kvalid = kpos < a.kh * a.kw;
       const int r_ = kpos / a.kw, s_ = kpos - (kpos / a.kw) * a.kw;
       const uint32_t stage_base = sA_u32 + s * L::kABytes;
 #pragma unroll
       for (int p = 0; p < 8; ++p) {
         const int r = p * 16 + row_sub;
         const int ih = ih0[p] + r_, iw = iw0[p] + s_;
-        const bool valid = (unsigned)ih < (unsigned)a.h && (unsigned)iw < (unsigned)a.w;
+        const bool valid = kvalid && (unsigned)ih < (unsigned)a.h && (unsigned)iw < (unsigned)a.w;
         const __nv_bfloat16* src =
-            valid ? a.x + (static_cast<size_t>(pix_base[p] + ih * a.w + iw) * a.cin + cb * kBK + chunk * 8) : a.x;
+            valid ? a.x + (static_cast<size_t>(pix_base[p] + ih * a.w + iw) * a.cin + coff) : a.x;
         const uint32_t dst = stage_base + r * 128 + ((chunk ^ (r & 7)) << 4);
         cp_async_16(dst, src, valid);
       }
@@ -196,12 +228,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     cp_async_wait<0>();
     fence_proxy_async_smem();
     for (int i = max(0, nkb - kLag); i < nkb; ++i) mbar_arrive(&full[i % kStages]);
+    if (ts && threadIdx.x == 0) ts[3] = gtimer();
 
     // ---------------- epilogue ----------------
+    // operands that do not depend on the accumulator: pull them into L1 while
+    // the last MMAs drain (residual row, folded-BN scale/bias of this tile)
+    {
+      const int m_pf = m0 + warp * 32 + lane;
+      if (a.res != nullptr && m_pf < a.M) {
+        const char* rp = reinterpret_cast<const char*>(a.res + static_cast<size_t>(m_pf) * a.cout + n0);
+        for (int off = 0; off < BN * 2; off += 128) prefetch_l1(rp + off);
+      }
+      if (threadIdx.x < BN / 32) {
+        prefetch_l1(a.scale + n0 + threadIdx.x * 32);
+        prefetch_l1(a.bias + n0 + threadIdx.x * 32);
+      }
+    }
     __syncwarp();
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     if (threadIdx.x == 0) pdl_trigger();  // mainloop done: let the next layer start its prologue
+    if (ts && threadIdx.x == 0) ts[4] = gtimer();
     const int row = warp * 32 + lane;
     const int m = m0 + row;
     const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
@@ -213,46 +260,66 @@ __global__ void __launch_bounds__(kThreads, 1)
         finalize_row32(a, m, n0 + c0, reinterpret_cast<const float*>(r));
       }
     } else {
+      // Split-K fix-up. Every split takes a ticket first; the holder of the last
+      // ticket does not publish its own partial: it waits until the other
+      // splits have reduced theirs into the zeroed fp32 accumulator (they are
+      // resident and past their mainloop, so the wait cannot deadlock), then
+      // adds its TMEM partial in registers, runs the epilogue and re-arms the
+      // accumulator and both counters for the next launch.
       const int tile = tile_m * gridDim.y + tile_n;
+      int* ticket_ctr = a.counters + 2 * tile;
+      int* done_ctr = ticket_ctr + 1;
       float* acc_row = a.ws + static_cast<size_t>(tile) * (kBM * BN) + static_cast<size_t>(row) * BN;
+      if (threadIdx.x == 0) *last_flag = (atomicAdd(ticket_ctr, 1) == a.splits - 1);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const bool last = *last_flag;
+      if (!last) {
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_row + c0, r);
-        if (m < a.M) {
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_row + c0, r);
+          if (m < a.M) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            red_add_v4(acc_row + c0 + 4 * q, __uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                       __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+            for (int q = 0; q < 8; ++q)
+              red_add_v4(acc_row + c0 + 4 * q, __uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                         __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+          }
         }
-      }
-      __threadfence();
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (threadIdx.x == 0) {
-        const int ticket = atomicAdd(&a.counters[tile], 1);
-        *last_flag = (ticket == a.splits - 1);
-      }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (*last_flag) {
         __threadfence();
-        if (m < a.M) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 0) atomicAdd(done_ctr, 1);
+      } else {
+        if (threadIdx.x == 0) {
+          while (ld_acquire_gpu(done_ctr) < a.splits - 1) {
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        __threadfence();
 #pragma unroll 1
-          for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(t_row + c0, r);
+          if (m < a.M) {
             float acc[32];
             float4* src = reinterpret_cast<float4*>(acc_row + c0);
+            float4 part[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) part[q] = __ldcg(src + q);  // all loads in flight together
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
-              float4 f = __ldcg(src + q);
-              acc[4 * q] = f.x;
-              acc[4 * q + 1] = f.y;
-              acc[4 * q + 2] = f.z;
-              acc[4 * q + 3] = f.w;
+              acc[4 * q] = __uint_as_float(r[4 * q]) + part[q].x;
+              acc[4 * q + 1] = __uint_as_float(r[4 * q + 1]) + part[q].y;
+              acc[4 * q + 2] = __uint_as_float(r[4 * q + 2]) + part[q].z;
+              acc[4 * q + 3] = __uint_as_float(r[4 * q + 3]) + part[q].w;
               __stcg(src + q, make_float4(0.f, 0.f, 0.f, 0.f));  // re-arm for the next launch
             }
             finalize_row32(a, m, n0 + c0, acc);
           }
         }
-        if (threadIdx.x == 0) a.counters[tile] = 0;
+        if (threadIdx.x == 0) {
+          ticket_ctr[0] = 0;
+          done_ctr[0] = 0;
+        }
       }
     }
   } else if (warp == 4) {
@@ -288,12 +355,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
+  if (ts && threadIdx.x == 0) ts[5] = gtimer();
   tc_fence_before();
   __syncthreads();
   if (warp == 4) {
     tc_fence_after();
     tmem_dealloc<BN>(tmem_base);
   }
+  if (ts && threadIdx.x == 0) ts[6] = gtimer();
 }
 
 // ------------------------------------------------------------------ host side
@@ -346,9 +415,10 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   a.M = d->n * d->ho * d->wo;
   a.relu = d->relu;
   a.cin_blocks = d->cin / kBK;
-  a.num_kb = d->kh * d->kw * a.cin_blocks;
+  a.num_kb = d->cin == 8 ? (d->kh * d->kw + 7) / 8 : d->kh * d->kw * a.cin_blocks;
   a.kb_per_split = pl.kb_per_split;
   a.splits = pl.splits;
+  a.ts = reinterpret_cast<unsigned long long*>(d->timestamps);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.tiles_m, pl.tiles_n, pl.splits);
   cfg.blockDim = dim3(kThreads);
@@ -378,11 +448,11 @@ extern "C" int daris_device_sms(void) {
 extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out) {
   using namespace daris;
   if (!d || !out) return DARIS_K_BAD_ARG;
-  if (d->cin % kBK != 0 || d->cout % 64 != 0 || d->n < 1 || d->ho < 1 || d->wo < 1 || d->kh < 1 || d->kw < 1 ||
-      d->stride < 1)
+  if ((d->cin % kBK != 0 && d->cin != 8) || d->cout % 64 != 0 || d->n < 1 || d->ho < 1 || d->wo < 1 ||
+      d->kh < 1 || d->kw < 1 || d->stride < 1)
     return DARIS_K_BAD_SHAPE;
   const int M = d->n * d->ho * d->wo;
-  const int num_kb = d->kh * d->kw * (d->cin / kBK);
+  const int num_kb = d->cin == 8 ? (d->kh * d->kw + 7) / 8 : d->kh * d->kw * (d->cin / kBK);
   const int budget = d->sm_budget > 0 ? d->sm_budget : daris_device_sms();
   const int tiles_m = (M + kBM - 1) / kBM;
   int bn = d->block_n;
@@ -397,15 +467,22 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
   const int tiles = tiles_m * tiles_n;
   int splits = d->splits;
   if (splits <= 0) {
+    // split-K costs one fix-up round trip (~2 us): only worth it for long K
+    // loops on grids that leave most of the partition idle
     splits = 1;
-    if (tiles * 2 <= budget) {
+    if (tiles * 2 <= budget && num_kb >= 8) {
       splits = budget / tiles;
-      const int max_by_k = num_kb / 2 > 0 ? num_kb / 2 : 1;  // keep >= 2 K blocks per split
+      const int max_by_k = num_kb / 4;  // keep >= 4 K blocks per split
       if (splits > max_by_k) splits = max_by_k;
       if (splits > 32) splits = 32;
       if (splits < 1) splits = 1;
     }
   }
+  static const int split_cap = [] {
+    const char* e = std::getenv("DARIS_SPLITK_MAX");  // experiment knob: cap the split-K factor
+    return e ? std::atoi(e) : 0;
+  }();
+  if (split_cap > 0 && splits > split_cap) splits = split_cap;
   if (splits > num_kb) splits = num_kb;
   int kbps = (num_kb + splits - 1) / splits;
   splits = (num_kb + kbps - 1) / kbps;  // no empty splits
@@ -415,7 +492,7 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
   out->tiles_m = tiles_m;
   out->tiles_n = tiles_n;
   out->workspace_floats = splits > 1 ? static_cast<int64_t>(tiles) * kBM * bn : 0;  // zero-initialised
-  out->counters = splits > 1 ? tiles : 0;
+  out->counters = splits > 1 ? 2 * tiles : 0;  // ticket + done per tile
   out->ctas = tiles * splits;
   return DARIS_K_OK;
 }

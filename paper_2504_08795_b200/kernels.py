@@ -27,7 +27,7 @@ class ConvDesc(C.Structure):
         ("n", C.c_int32), ("h", C.c_int32), ("w", C.c_int32), ("cin", C.c_int32), ("cout", C.c_int32),
         ("kh", C.c_int32), ("kw", C.c_int32), ("stride", C.c_int32), ("pad", C.c_int32),
         ("ho", C.c_int32), ("wo", C.c_int32), ("relu", C.c_int32), ("block_n", C.c_int32),
-        ("splits", C.c_int32), ("sm_budget", C.c_int32),
+        ("splits", C.c_int32), ("sm_budget", C.c_int32), ("_pad", C.c_int32), ("timestamps", C.c_void_p),
     ]
 
 
@@ -99,7 +99,7 @@ def conv2d(x: torch.Tensor, weight: torch.Tensor, scale: torch.Tensor, bias: tor
            stride: int = 1, pad: int = 0, relu: int = 1, residual: torch.Tensor | None = None,
            out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
            counters: torch.Tensor | None = None, block_n: int = 0, splits: int = 0,
-           sm_budget: int = 0, stream=None) -> torch.Tensor:
+           sm_budget: int = 0, stream=None, timestamps: torch.Tensor | None = None) -> torch.Tensor:
     """x: [n,h,w,cin] bf16 NHWC; weight: [cout,kh,kw,cin] bf16."""
     cout, kh, kw, cin = weight.shape
     d = conv_desc(tuple(x.shape), cout, kh, kw, stride, pad, relu=relu, block_n=block_n,
@@ -115,6 +115,7 @@ def conv2d(x: torch.Tensor, weight: torch.Tensor, scale: torch.Tensor, bias: tor
     d.x, d.y, d.residual, d.weight = _ptr(x), _ptr(out), _ptr(residual), _ptr(weight)
     d.scale, d.bias = _ptr(scale), _ptr(bias)
     d.workspace, d.counters = _ptr(workspace), _ptr(counters)
+    d.timestamps = _ptr(timestamps)
     _check(lib().daris_conv2d(C.byref(d), _stream(stream)), "daris_conv2d")
     return out
 

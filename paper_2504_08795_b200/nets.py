@@ -128,22 +128,20 @@ def _conv_layer(name, conv, bn, relu, device, hw_out, cin_pad=None) -> ConvLayer
 
 
 def _stem_layer(name, conv, bn, relu, device, hw_out) -> ConvLayer:
-    """kxk stem over 3 input channels as a GEMM over im2col rows (K padded to 64)."""
+    """kxk stem over 3 input channels: input packed to NHWC with 8 channels (3 real),
+    weights [cout][kh][kw][8]; the conv kernel's pixel-chunk mode gathers one kernel
+    position (8 channels = 16 B) per chunk, so no im2col pass is needed."""
     w, scale, bias = fold_bn(conv, bn)
     cout, cin, kh, kw = w.shape
-    kdim = cin * kh * kw
-    kpad = _pad64(kdim)
     cout_p = _pad64(cout)
-    wt = torch.zeros(cout_p, 1, 1, kpad)
-    wt[:cout, 0, 0, :kdim] = w.reshape(cout, kdim)
+    wt = torch.zeros(cout_p, kh, kw, 8)
+    wt[:cout, :, :, :cin] = w.permute(0, 2, 3, 1)
     sc = torch.zeros(cout_p)
     bi = torch.zeros(cout_p)
     sc[:cout] = scale
     bi[:cout] = bias
-    layer = ConvLayer(name, wt.to(device=device, dtype=torch.bfloat16).contiguous(), sc.to(device), bi.to(device),
-                      1, 1, 1, 0, kpad, cout_p, relu, 2 * cout * kdim * hw_out)
-    layer.stem = (kh, kw, conv.stride[0], conv.padding[0])  # type: ignore[attr-defined]
-    return layer
+    return ConvLayer(name, wt.to(device=device, dtype=torch.bfloat16).contiguous(), sc.to(device), bi.to(device),
+                     kh, kw, conv.stride[0], conv.padding[0], 8, cout_p, relu, 2 * cout * cin * kh * kw * hw_out)
 
 
 @dataclass
@@ -239,9 +237,9 @@ def _resnet_ops(model, name, batch, device, split) -> Network:
     b = _Builder(batch)
     stem = _stem_layer("conv1", model.conv1, model.bn1, 1, device, 112 * 112)
     b.need("input", batch * 3 * 224 * 224)
-    b.need("im2col", batch * 112 * 112 * stem.cin)
-    b.ops.append(Op("im2col", stem, "input", "im2col", None, (batch, 3, 224, 224), (batch, 112, 112, stem.cin)))
-    x, shape = b.conv(stem, "im2col", (batch, 112, 112, stem.cin))
+    b.need("packed", batch * 224 * 224 * 8)
+    b.ops.append(Op("pack8", None, "input", "packed", None, (batch, 3, 224, 224), (batch, 224, 224, 8)))
+    x, shape = b.conv(stem, "packed", (batch, 224, 224, 8))
     y = b.take(avoid=(x,))
     b.need(y, batch * 56 * 56 * 64)
     b.ops.append(Op("maxpool", None, x, y, None, shape, (batch, 56, 56, shape[3])))
@@ -311,10 +309,9 @@ def _vgg_ops(model, batch, device, n_stages) -> Network:
         if isinstance(m, nn.Conv2d):
             if x is None:
                 stem = _stem_layer(f"features.{i}", m, None, 1, device, hw * hw)
-                b.need("im2col", batch * hw * hw * stem.cin)
-                b.ops.append(Op("im2col", stem, "input", "im2col", None, (batch, 3, 224, 224),
-                                (batch, hw, hw, stem.cin)))
-                x, shape = b.conv(stem, "im2col", (batch, hw, hw, stem.cin))
+                b.need("packed", batch * 224 * 224 * 8)
+                b.ops.append(Op("pack8", None, "input", "packed", None, (batch, 3, 224, 224), (batch, 224, 224, 8)))
+                x, shape = b.conv(stem, "packed", (batch, 224, 224, 8))
             else:
                 layer = _conv_layer(f"features.{i}", m, None, 1, device, hw * hw)
                 nx, shape = b.conv(layer, x, shape)
@@ -357,9 +354,9 @@ def _mbv2_ops(model, batch, device, n_stages) -> Network:
     b.need("input", batch * 3 * 224 * 224)
     first = feats[0]
     stem = _stem_layer("features.0", first[0], first[1], 6, device, 112 * 112)
-    b.need("im2col", batch * 112 * 112 * stem.cin)
-    b.ops.append(Op("im2col", stem, "input", "im2col", None, (batch, 3, 224, 224), (batch, 112, 112, stem.cin)))
-    x, shape = b.conv(stem, "im2col", (batch, 112, 112, stem.cin))
+    b.need("packed", batch * 224 * 224 * 8)
+    b.ops.append(Op("pack8", None, "input", "packed", None, (batch, 3, 224, 224), (batch, 224, 224, 8)))
+    x, shape = b.conv(stem, "packed", (batch, 224, 224, 8))
     blocks = feats[1:-1]
     # split the inverted-residual sequence into n_stages groups of roughly equal count
     per = max(1, (len(blocks) + n_stages - 1) // n_stages) if n_stages > 1 else len(blocks) + 1
@@ -431,9 +428,11 @@ RESNET50_SPLITS = {1: [], 2: [7], 3: [3, 10], 4: [3, 7, 13]}  # 4 stages: layer1
 
 
 def build_network(name: str, *, batch: int = 1, n_stages: int | None = None, seed: int = 0,
-                  device: torch.device | str = "cuda", keep_torch: bool = False) -> Network:
+                  device: torch.device | str = "cuda", keep_torch: bool = False,
+                  model: nn.Module | None = None) -> Network:
     device = torch.device(device)
-    model = make_torch_model(name, seed)
+    if model is None:
+        model = make_torch_model(name, seed)
     with torch.no_grad():
         if name == "resnet18":
             n_stages = n_stages or 3
@@ -491,9 +490,8 @@ def _view(t: torch.Tensor, shape) -> torch.Tensor:
 
 def run_op(op: Op, tb: TaskBuffers, stream, sm_budget: int = 0) -> None:
     B = tb.bufs
-    if op.kind == "im2col":
-        kh, kw, s, p = op.layer.stem
-        K.stem_im2col(B["input"], kh, kw, s, p, op.layer.cin, out=_view(B["im2col"], op.shape_out), stream=stream)
+    if op.kind == "pack8":
+        K.pack_nhwc(B["input"], 8, out=_view(B["packed"], op.shape_out), stream=stream)
     elif op.kind == "conv":
         L = op.layer
         res = _view(B[op.res], op.shape_out) if op.res else None

@@ -54,7 +54,7 @@ class ExecStatsC(C.Structure):
     _fields_ = [("graph_launches", C.c_int64), ("copies_h2d", C.c_int64), ("copies_d2h", C.c_int64),
                 ("copies_d2d", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("slot_waits", C.c_int64), ("polls", C.c_int64), ("wall_seconds", C.c_double),
-                ("release_lag_max", C.c_double)]
+                ("release_lag_max", C.c_double), ("loop_gap_max", C.c_double)]
 
 
 _exec_lib = None
@@ -225,9 +225,12 @@ class DarisRuntime:
     def __init__(self, tasks: Sequence[TaskDef], gpu: GpuConfig, *, slots: int = 3, partition: str = "green",
                  window_size: int = 5, flags: AblationFlags = AblationFlags(), hpa: bool = False,
                  stage_migration: bool = False, seed: int = 0, e2e: bool = False, pool_size: int = 64,
-                 device: int = 0):
+                 device: int = 0, phasing: str = "random"):
         if not torch.cuda.is_available():
             raise RuntimeError("DarisRuntime needs a CUDA device (there is no CPU fallback)")
+        if phasing not in ("random", "zero"):
+            raise ValueError(f"unknown phasing {phasing!r}")
+        self.phasing = phasing
         self.tasks = sorted(tasks, key=lambda t: t.id)
         self.gpu = gpu
         self.seed = seed
@@ -373,6 +376,9 @@ class DarisRuntime:
         return out
 
     def phases(self) -> list[float]:
+        """Release offsets as the reference draws them (engine.py:417-423), quantised."""
+        if self.phasing == "zero":
+            return [0.0 for _ in self.tasks]
         rng = random.Random(self.seed)
         return [quantize(rng.random() * t.period) for t in self.tasks]
 

@@ -165,3 +165,23 @@ def test_maxpool_avgpool_linear_dwconv():
     out = K.dwconv(x.to(dev), wd.to(dev), sc.to(dev), bi.to(dev), stride=2, pad=1, relu=6)
     torch.cuda.synchronize()
     _close(out, ref.clamp(0, 6))
+
+
+@pytest.mark.parametrize("k,stride,pad,hw", [(7, 2, 3, 224), (3, 1, 1, 224), (3, 2, 1, 224)])
+def test_stem_pixel_chunk_mode_matches_conv(k, stride, pad, hw):
+    """cin == 8 stem mode: NHWC8 input (3 real channels), K = k*k*8 zero-padded by TMA."""
+    from paper_2504_08795_b200 import kernels as K
+    dev = torch.device("cuda")
+    g = torch.Generator().manual_seed(k + stride)
+    x = torch.randn(2, 3, hw, hw, generator=g)
+    wt = torch.randn(64, 3, k, k, generator=g) / (3 * k * k) ** 0.5
+    scale = torch.rand(64, generator=g) + 0.5
+    bias = torch.randn(64, generator=g) * 0.1
+    ref = F.conv2d(x.bfloat16().float(), wt.bfloat16().float(), stride=stride, padding=pad)
+    ref = (ref.permute(0, 2, 3, 1) * scale + bias).clamp_min(0)
+    packed = K.pack_nhwc(x.to(dev), 8)
+    w8 = torch.zeros(64, k, k, 8)
+    w8[..., :3] = wt.permute(0, 2, 3, 1)
+    out = K.conv2d(packed, w8.bfloat16().to(dev), scale.to(dev), bias.to(dev), stride=stride, pad=pad)
+    torch.cuda.synchronize()
+    _close(out, ref)

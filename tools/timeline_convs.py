@@ -1,0 +1,114 @@
+"""Per-CTA phase timeline of the conv kernels of one network forward, captured
+as a CUDA graph on a green-context partition (as the executor runs it).
+
+Each conv CTA stamps %globaltimer at: 0 entry, 1 after barrier/TMEM setup,
+2 after griddepcontrol.wait, 3 producer done, 4 accumulator ready, 5 epilogue
+done, 6 exit. Prints per-layer medians and the gap between a layer's last CTA
+exit and the next layer's first released CTA.
+
+python tools/timeline_convs.py [--model resnet50] [--sms 74] [--json out.json]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import statistics
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+import torch  # noqa: E402
+
+from paper_2504_08795_b200 import kernels as K  # noqa: E402
+from paper_2504_08795_b200 import nets  # noqa: E402
+from paper_2504_08795_b200.runtime import Executor  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="resnet50")
+    ap.add_argument("--sms", type=int, default=74)
+    ap.add_argument("--json", default=None)
+    args = ap.parse_args()
+    ex = Executor(max(1, 148 // args.sms), 1, args.sms, slots=1, max_tasks=1, max_stages=8)
+    net = nets.build_network(args.model, batch=1)
+    tb = nets.allocate_buffers(net, sm_budget=args.sms)
+    sp = ex.stream(1, 0)
+    s = torch.cuda.ExternalStream(sp)
+    ts = {}
+    for i, op in enumerate(net.ops):
+        if op.kind == "conv":
+            L = op.layer
+            p = K.conv_plan(K.conv_desc(op.shape_in, L.cout, L.kh, L.kw, L.stride, L.pad, sm_budget=args.sms))
+            ts[i] = torch.zeros(p.ctas * 8, dtype=torch.int64, device="cuda")
+
+    def forward(stream):
+        for i, op in enumerate(net.ops):
+            if op.kind == "conv":
+                L = op.layer
+                B = tb.bufs
+                res = nets._view(B[op.res], op.shape_out) if op.res else None
+                K.conv2d(nets._view(B[op.src], op.shape_in), L.weight, L.scale, L.bias, stride=L.stride,
+                         pad=L.pad, relu=L.relu, residual=res, out=nets._view(B[op.dst], op.shape_out),
+                         workspace=tb.workspace, counters=tb.counters, sm_budget=args.sms, stream=stream,
+                         timestamps=ts[i])
+            else:
+                nets.run_op(op, tb, stream, args.sms)
+
+    forward(sp)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        g.capture_begin()
+        forward(sp)
+        g.capture_end()
+        for _ in range(3):
+            g.replay()
+    torch.cuda.synchronize()
+    rows = []
+    prev_end = None
+    t_origin = None
+    for i, op in enumerate(net.ops):
+        if op.kind != "conv":
+            continue
+        a = ts[i].view(-1, 8).cpu().double()
+        if t_origin is None:
+            t_origin = a[:, 0].min().item()
+        a = (a - t_origin) / 1e3  # us
+        start = a[:, 0].min().item()
+        released = a[:, 2].min().item()
+        end = a[:, 6].max().item()
+        row = {"i": i, "name": op.layer.name, "ctas": a.shape[0], "start": start, "released": released,
+               "end": end,
+               "setup_us": statistics.median((a[:, 1] - a[:, 0]).tolist()),
+               "wait_us": statistics.median((a[:, 2] - a[:, 1]).tolist()),
+               "produce_us": statistics.median((a[:, 3] - a[:, 2]).tolist()),
+               "mma_tail_us": statistics.median((a[:, 4] - a[:, 3]).tolist()),
+               "epilogue_us": statistics.median((a[:, 5] - a[:, 4]).tolist()),
+               "epilogue_max_us": (a[:, 5] - a[:, 4]).max().item(),
+               "teardown_us": statistics.median((a[:, 6] - a[:, 5]).tolist()),
+               "span_us": end - released,
+               "gap_from_prev_us": None if prev_end is None else released - prev_end}
+        prev_end = end
+        rows.append(row)
+    total = rows[-1]["end"] - rows[0]["released"]
+    print(f"{args.model} conv timeline in {args.sms} SMs: first release -> last exit {total:.1f} us over "
+          f"{len(rows)} convs")
+    print(f"{'layer':28s} ctas  span  gap  setup  wait  prod  mma  epi(max)  tear")
+    for r in rows:
+        print(f"{r['name']:28s} {r['ctas']:4d} {r['span_us']:5.1f} "
+              f"{(r['gap_from_prev_us'] if r['gap_from_prev_us'] is not None else 0):5.2f} {r['setup_us']:5.2f} "
+              f"{r['wait_us']:6.2f} {r['produce_us']:5.2f} {r['mma_tail_us']:5.2f} {r['epilogue_us']:5.2f}"
+              f"({r['epilogue_max_us']:5.2f}) {r['teardown_us']:5.2f}")
+    gaps = [r["gap_from_prev_us"] for r in rows if r["gap_from_prev_us"] is not None]
+    spans = [r["span_us"] for r in rows]
+    print(f"sum span {sum(spans):.1f} us, sum gaps {sum(gaps):.1f} us (median gap {statistics.median(gaps):.2f})")
+    if args.json:
+        Path(args.json).write_text(json.dumps(rows, indent=1))
+    ex.close()
+
+
+if __name__ == "__main__":
+    main()
