@@ -196,6 +196,9 @@ int64_t daris_audit_copy(const daris_handle* h, daris_audit* buf, int64_t cap);
 void daris_log_clear(daris_handle* h);
 /* append one record (used by the GPU executor so real runs log like the sim) */
 void daris_log_push(daris_handle* h, const daris_log_record* rec);
+/* pre-size (and pre-fault) the log and audit buffers so a real-time run never
+   reallocates them mid-flight (a multi-MB realloc stalls the dispatch loop) */
+void daris_log_reserve(daris_handle* h, int64_t records, int64_t audits);
 /* pending admitted work: ready stages summed over contexts */
 int daris_ready_total(const daris_handle* h, int32_t* out);
 

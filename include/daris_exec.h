@@ -49,6 +49,8 @@ typedef struct daris_exec_partition {
 typedef struct daris_stage_trace {
   int32_t task, job, stage, context, stream, slot;
   double start, end;        /* quantised executor time (s) */
+  double gpu_start, gpu_end; /* device time (s) of the stage's first / last work on its stream, from
+                                timing events (only when DARIS_GPU_TIMING is set; NaN otherwise) */
 } daris_stage_trace;
 
 typedef struct daris_exec_stats {
@@ -60,6 +62,9 @@ typedef struct daris_exec_stats {
   double wall_seconds;      /* host wall time of the run incl. drain */
   double release_lag_max;   /* worst delay between a nominal release and its processing */
   double loop_gap_max;      /* longest host gap between two polling passes (host stalls) */
+  double progress_gap_max;  /* longest time with stages in flight and no completion observed */
+  int64_t stalls;           /* GPU-wide stalls: progress gaps above the stall threshold */
+  double first_stall_at;    /* executor time of the first stall (-1 if none) */
 } daris_exec_stats;
 
 typedef struct daris_exec daris_exec;
@@ -90,6 +95,12 @@ int daris_exec_set_pool(daris_exec* ex, int32_t task, const void* pool, int32_t 
  * released in [warmup, duration); in-flight jobs are drained and counted. */
 int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warmup, const double* phases,
                    int32_t collect_log, daris_report* report, daris_exec_stats* stats);
+
+/* A progress gap (stages in flight, no completion) longer than `seconds`
+ * counts as a GPU-wide stall in daris_exec_stats (default 1 ms). An idle B200
+ * shows ~1.7 ms whole-GPU pauses every few seconds (tools/freeze_probe.cu), so
+ * runs can tell an environmental pause from a scheduling failure. */
+int daris_exec_set_stall_threshold(daris_exec* ex, double seconds);
 
 int64_t daris_exec_trace_count(const daris_exec* ex);
 int64_t daris_exec_trace_copy(const daris_exec* ex, daris_stage_trace* buf, int64_t cap);

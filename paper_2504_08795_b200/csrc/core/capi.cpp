@@ -254,6 +254,21 @@ void daris_log_push(daris_handle* h, const daris_log_record* r) {
   if (h->d->collect_log) h->d->log.push_back({r->time, r->kind, r->task, r->job, r->stage, r->context, r->stream, r->rate});
 }
 
+void daris_log_reserve(daris_handle* h, int64_t records, int64_t audits) {
+  auto& L = h->d->log;
+  auto& A = h->d->audits;
+  if (records > 0 && static_cast<size_t>(records) > L.capacity()) {
+    const size_t keep = L.size();
+    L.resize(static_cast<size_t>(records));  // touch every page now, not inside the timed loop
+    L.resize(keep);
+  }
+  if (audits > 0 && static_cast<size_t>(audits) > A.capacity()) {
+    const size_t keep = A.size();
+    A.resize(static_cast<size_t>(audits));
+    A.resize(keep);
+  }
+}
+
 int daris_ready_total(const daris_handle* h, int32_t* out) {
   int n = 0;
   for (int c = 1; c <= h->d->gpu().n_contexts; ++c) n += h->d->ready_count(c);

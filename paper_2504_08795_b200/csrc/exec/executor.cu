@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <queue>
@@ -70,6 +71,7 @@ struct Running {
   bool busy = false;
   int task = 0, job = 0, stage = 0, slot = 0;
   double start = 0;
+  int ev = -1;  // index of the stage's timing-event pair (DARIS_GPU_TIMING)
 };
 
 struct TaskInfo {
@@ -101,6 +103,7 @@ struct daris_exec {
   std::vector<daris_stage_trace> trace;
   std::string err;
   int64_t graph_count = 0;
+  double stall_threshold = 1e-3;
 
   size_t gidx(int task, int stage, int ctx, int slot) const {
     return ((static_cast<size_t>(task - 1) * cfg.max_stages + stage) * cfg.n_contexts + (ctx - 1)) *
@@ -169,6 +172,7 @@ int build_partitions(daris_exec* ex) {
     }
     int prio_low = 0, prio_high = 0;
     cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
+    if (std::getenv("DARIS_NO_HIPRIO")) prio_high = prio_low;  // experiment knob
     const int n_streams = 2 * c.n_streams + 1;  // low + high priority per slot, + capture stream
     for (int s = 0; s < n_streams; ++s) {
       const int prio = (s >= c.n_streams && s < 2 * c.n_streams) ? prio_high : prio_low;
@@ -359,6 +363,12 @@ int daris_exec_set_pool(daris_exec* ex, int32_t task, const void* pool, int32_t 
   return DARIS_OK;
 }
 
+int daris_exec_set_stall_threshold(daris_exec* ex, double seconds) {
+  if (!(seconds > 0)) return fail(ex, "stall threshold must be positive");
+  ex->stall_threshold = seconds;
+  return DARIS_OK;
+}
+
 int64_t daris_exec_trace_count(const daris_exec* ex) { return static_cast<int64_t>(ex->trace.size()); }
 
 int64_t daris_exec_trace_copy(const daris_exec* ex, daris_stage_trace* buf, int64_t cap) {
@@ -413,9 +423,43 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
     period[id] = info[id].period;  // Python quantises periods before creating the handle
     if (phase[id] < duration) heap.push({phase[id], id});
   }
+  // Size every growing buffer for the whole run up front (and fault its pages
+  // in now): a multi-MB vector reallocation inside the loop stalls dispatch
+  // for ~1 ms and shows up as a burst of deadline misses.
+  long long expect_jobs = 0;
+  int max_st = 1;
+  for (int i = 0; i < n_tasks; ++i) {
+    const TaskInfo& t = info[ids[i]];
+    if (t.period > 0) expect_jobs += static_cast<long long>(std::ceil(duration / t.period)) + 1;
+    max_st = std::max(max_st, t.n_stages);
+  }
+  expect_jobs = expect_jobs + expect_jobs / 4 + 64;
+  daris_log_reserve(h, expect_jobs * (3 + 2 * max_st) + 16, expect_jobs * (c.n_contexts + 1));
+  {
+    const size_t keep = ex->trace.size();
+    ex->trace.resize(static_cast<size_t>(expect_jobs * max_st));
+    ex->trace.resize(keep);
+  }
+  for (int k = 0; k < 2; ++k) {
+    acc.resp[k].resize(static_cast<size_t>(expect_jobs));
+    acc.resp[k].clear();
+  }
+  // optional device-side stage timing: a (begin, end) timing-event pair per launch
+  const bool gpu_timing = std::getenv("DARIS_GPU_TIMING") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  cudaEvent_t tref = nullptr;
+  int tev_next = 0;
+  if (gpu_timing) {
+    tev.resize(static_cast<size_t>(2 * expect_jobs * max_st));
+    for (auto& e : tev) CUDA_TRY(ex, cudaEventCreate(&e));
+    CUDA_TRY(ex, cudaEventCreate(&tref));
+  }
   std::unordered_map<int, int> job_slot;     // job -> buffer slot
   std::unordered_map<int, double> job_rel;   // job -> release time
   std::unordered_map<int, int> job_seq;      // job -> per-task sequence number
+  job_slot.reserve(1024);
+  job_rel.reserve(1024);
+  job_seq.reserve(1024);
   std::vector<std::vector<Running>> run(c.n_contexts, std::vector<Running>(c.n_streams));
   int job_counter = 0;
   int in_flight = 0;
@@ -448,7 +492,14 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
     }
     cudaGraphExec_t g = ex->graphs[ex->gidx(r.task, r.stage, r.context, slot)];
     if (!g) return fail(ex, "no graph for dispatched stage", DARIS_E_INTERNAL);
+    int ev = -1;
+    if (gpu_timing && tev_next + 2 <= static_cast<int>(tev.size())) {
+      ev = tev_next;
+      tev_next += 2;
+      CUDA_TRY(ex, cudaEventRecord(tev[ev], s));
+    }
     CUDA_TRY(ex, cudaGraphLaunch(g, s));
+    if (ev >= 0) CUDA_TRY(ex, cudaEventRecord(tev[ev + 1], s));
     st.graph_launches++;
     if (r.stage == t.n_stages - 1) {
       const auto& pool = ex->pools[r.task - 1];
@@ -468,6 +519,7 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
     rr.stage = r.stage;
     rr.slot = slot;
     rr.start = r.started_at;
+    rr.ev = ev;
     in_flight++;
     return DARIS_OK;
   };
@@ -491,16 +543,32 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
   };
 
   const auto t0 = clock::now();
+  if (gpu_timing) CUDA_TRY(ex, cudaEventRecord(tref, ex->parts[0].streams[0]));
   auto elapsed = [&]() { return std::chrono::duration<double>(clock::now() - t0).count(); };
   struct Done {
     int ctx, stream, job, stage;
   };
   std::vector<Done> done;
   double last_pass = 0.0;
+  double last_progress = 0.0;  // last completion observed, or last moment nothing was in flight
+  bool in_stall = false;
+  st.first_stall_at = -1.0;
   for (;;) {
     const double raw_now = elapsed();
     if (raw_now - last_pass > st.loop_gap_max) st.loop_gap_max = raw_now - last_pass;
     last_pass = raw_now;
+    if (in_flight == 0) {
+      last_progress = raw_now;
+      in_stall = false;
+    } else {
+      const double gap = raw_now - last_progress;
+      if (gap > st.progress_gap_max) st.progress_gap_max = gap;
+      if (gap > ex->stall_threshold && !in_stall) {
+        in_stall = true;
+        st.stalls++;
+        if (st.first_stall_at < 0) st.first_stall_at = raw_now - gap;
+      }
+    }
     const double now = quant(raw_now);
     bool progressed = false;
     // 1) due releases, in (time, task) order, each at its nominal instant
@@ -549,7 +617,11 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
         if (!rr.busy) continue;
         st.polls++;
         cudaError_t q = cudaEventQuery(ex->parts[k].done[s]);
-        if (q == cudaSuccess) done.push_back({k + 1, s, rr.job, rr.stage});
+        if (q == cudaSuccess) {
+          done.push_back({k + 1, s, rr.job, rr.stage});
+          last_progress = raw_now;
+          in_stall = false;
+        }
         else if (q != cudaErrorNotReady) {
           status = fail(ex, std::string("stage failed on the GPU: ") + cudaGetErrorString(q), DARIS_E_INTERNAL);
           break;
@@ -569,7 +641,8 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
         status = fail(ex, std::string("complete: ") + daris_last_error(h), rc);
         break;
       }
-      ex->trace.push_back(daris_stage_trace{rr.task, rr.job, rr.stage, d.ctx, d.stream, rr.slot, rr.start, t});
+      ex->trace.push_back(daris_stage_trace{rr.task, rr.job, rr.stage, d.ctx, d.stream, rr.slot, rr.start, t,
+                                            static_cast<double>(rr.ev), NAN});
       push_log(h, t, DARIS_LOG_STAGE_COMPLETE, rr.task, rr.job, rr.stage, d.ctx, d.stream, 1.0);
       rr.busy = false;
       in_flight--;
@@ -607,6 +680,20 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
     return status;
   }
   cudaDeviceSynchronize();
+  for (auto& tr : ex->trace) {
+    const int ev = std::isnan(tr.gpu_start) ? -1 : static_cast<int>(tr.gpu_start);
+    tr.gpu_start = tr.gpu_end = NAN;
+    if (gpu_timing && ev >= 0) {
+      float a = 0, b = 0;
+      if (cudaEventElapsedTime(&a, tref, tev[ev]) == cudaSuccess &&
+          cudaEventElapsedTime(&b, tref, tev[ev + 1]) == cudaSuccess) {
+        tr.gpu_start = a * 1e-3;
+        tr.gpu_end = b * 1e-3;
+      }
+    }
+  }
+  for (auto e : tev) cudaEventDestroy(e);
+  if (tref) cudaEventDestroy(tref);
   push_log(h, duration, DARIS_LOG_SIM_END);
   st.wall_seconds = elapsed();
 

@@ -47,14 +47,16 @@ class PartitionC(C.Structure):
 
 class StageTraceC(C.Structure):
     _fields_ = [("task", C.c_int32), ("job", C.c_int32), ("stage", C.c_int32), ("context", C.c_int32),
-                ("stream", C.c_int32), ("slot", C.c_int32), ("start", C.c_double), ("end", C.c_double)]
+                ("stream", C.c_int32), ("slot", C.c_int32), ("start", C.c_double), ("end", C.c_double),
+                ("gpu_start", C.c_double), ("gpu_end", C.c_double)]
 
 
 class ExecStatsC(C.Structure):
     _fields_ = [("graph_launches", C.c_int64), ("copies_h2d", C.c_int64), ("copies_d2h", C.c_int64),
                 ("copies_d2d", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("slot_waits", C.c_int64), ("polls", C.c_int64), ("wall_seconds", C.c_double),
-                ("release_lag_max", C.c_double), ("loop_gap_max", C.c_double)]
+                ("release_lag_max", C.c_double), ("loop_gap_max", C.c_double),
+                ("progress_gap_max", C.c_double), ("stalls", C.c_int64), ("first_stall_at", C.c_double)]
 
 
 _exec_lib = None
@@ -77,6 +79,7 @@ def exec_lib() -> C.CDLL:
             "daris_exec_set_pool": [vp, i32, vp, i32, i32, i64, vp, i64],
             "daris_exec_run": [vp, vp, f64, f64, P(f64), i32, P(_core.ReportC), P(ExecStatsC)],
             "daris_exec_busy_calibrate": [vp, P(i32), i32, P(i32), f64, P(f64)],
+            "daris_exec_set_stall_threshold": [vp, f64],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -170,12 +173,21 @@ class Executor:
         self._c(rc, "daris_exec_run")
         return rep, st
 
+    def set_stall_threshold(self, seconds: float) -> None:
+        self._c(exec_lib().daris_exec_set_stall_threshold(self._h, seconds), "set_stall_threshold")
+
     def trace(self) -> list[tuple]:
         L = exec_lib()
         n = L.daris_exec_trace_count(self._h)
         arr = (StageTraceC * max(1, n))()
         L.daris_exec_trace_copy(self._h, arr, n)
+        self._gpu_times = [(a.gpu_start, a.gpu_end) for a in list(arr)[:n]]
         return [(a.task, a.job, a.stage, a.context, a.stream, a.slot, a.start, a.end) for a in list(arr)[:n]]
+
+    def trace_gpu(self) -> list[tuple[float, float]]:
+        """Device-side (start, end) of each traced stage, aligned with trace()
+        (NaN unless the run had DARIS_GPU_TIMING set)."""
+        return getattr(self, "_gpu_times", [])
 
     def busy_calibrate(self, stage_counts: Sequence[int], slot_tasks: Sequence[int], seconds: float) -> float:
         sc = (C.c_int32 * len(stage_counts))(*stage_counts)
@@ -403,6 +415,9 @@ class DarisRuntime:
         h = self.open_dispatcher(full_load)
         torch.cuda.synchronize()
         phases = self.phases()
+        # a progress gap this long with stages in flight is a GPU-wide stall, not scheduling
+        longest = max(max(v) for v in self.stage_nominal.values())
+        self.exec.set_stall_threshold(max(1e-3, 3.0 * longest))
         rep, st = self.exec.run(h, quantize(duration), quantize(warmup), phases)
         self.handle = h
         report = report_from_native(rep, label=f"{self.gpu.n_contexts}x{self.gpu.n_streams}_"
