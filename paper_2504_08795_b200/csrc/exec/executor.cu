@@ -733,10 +733,17 @@ int daris_exec_busy_calibrate(daris_exec* ex, const int32_t* task_stage_counts, 
   std::vector<Loop> loops(n_slots);
   const auto t0 = clock::now();
   auto now = [&]() { return std::chrono::duration<double>(clock::now() - t0).count(); };
+  // every concurrently looping copy of a task needs its own buffer set: the
+  // k-th stream running task t uses buffer slot k (stage programs and split-K
+  // scratch belong to a buffer set and must never run twice at once)
+  std::vector<int> uses(static_cast<size_t>(n_tasks) + 1, 0);
   for (int s = 0; s < n_slots; ++s) {
     const int task = slot_tasks[s];
     if (task < 1 || task > n_tasks) return fail(ex, "bad calibration task");
-    loops[s] = Loop{task, 0, s / c.n_streams + 1, s % c.n_streams, s % c.slots_per_task, 0.0};
+    const int slot = uses[task]++;
+    if (slot >= c.slots_per_task)
+      return fail(ex, "calibration runs task " + std::to_string(task) + " on more streams than it has buffer slots");
+    loops[s] = Loop{task, 0, s / c.n_streams + 1, s % c.n_streams, slot, 0.0};
   }
   auto go = [&](Loop& l) -> int {
     Partition& p = ex->parts[l.ctx - 1];

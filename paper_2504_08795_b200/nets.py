@@ -185,6 +185,7 @@ class TaskBuffers:
     bufs: dict[str, torch.Tensor]
     workspace: torch.Tensor
     counters: torch.Tensor
+    programs: dict = field(default_factory=dict)   # (net id, stage, grid) -> K.StageProgram
 
     @property
     def input(self) -> torch.Tensor:
@@ -520,16 +521,95 @@ def run_op(op: Op, tb: TaskBuffers, stream, sm_budget: int = 0) -> None:
         raise ValueError(op.kind)
 
 
-def run_stage(net: Network, stage: int, tb: TaskBuffers, stream, sm_budget: int = 0) -> int:
+# stage execution mode: "persistent" = one stage-kernel launch per stage
+# (csrc/kernels/stage_tc.cu), "layers" = one launch per op (conv_tc.cu + aux.cu)
+import os as _os
+
+STAGE_MODE = _os.environ.get("DARIS_STAGE_MODE", "layers")
+# persistent mode: CTAs per stage kernel (0 = the partition's SM count)
+STAGE_GRID = int(_os.environ.get("DARIS_STAGE_GRID", "0"))
+
+
+def stage_ops(net: Network, stage: int, tb: TaskBuffers) -> list:
+    """The stage's ops as a persistent-kernel op table bound to this buffer set."""
+    B = tb.bufs
+    out = []
+    a, b = net.stage_bounds[stage], net.stage_bounds[stage + 1]
+    for op in net.ops[a:b]:
+        if op.kind == "pack8":
+            n, c, h, w = op.shape_in
+            out.append(K.stage_op(K.OP_PACK8, B["input"], B["packed"], n=n, c=c, h=h, w=w))
+        elif op.kind == "conv":
+            L = op.layer
+            n, h, w, c = op.shape_in
+            _, ho, wo, cout = op.shape_out
+            out.append(K.stage_op(K.OP_CONV, B[op.src], B[op.dst], residual=B[op.res] if op.res else None,
+                                  weight=L.weight, scale=L.scale, bias=L.bias, n=n, h=h, w=w, c=c, cout=cout,
+                                  kh=L.kh, kw=L.kw, stride=L.stride, pad=L.pad, ho=ho, wo=wo, relu=L.relu))
+        elif op.kind in ("maxpool", "maxpool2"):
+            n, h, w, c = op.shape_in
+            _, ho, wo, _ = op.shape_out
+            k, st, pd = (3, 2, 1) if op.kind == "maxpool" else (2, 2, 0)
+            out.append(K.stage_op(K.OP_MAXPOOL, B[op.src], B[op.dst], n=n, h=h, w=w, c=c, kh=k, kw=k, stride=st,
+                                  pad=pd, ho=ho, wo=wo))
+        elif op.kind == "avgpool":
+            n, h, w, c = op.shape_in
+            out.append(K.stage_op(K.OP_AVGPOOL, B[op.src], B[op.dst], n=n, h=h, w=w, c=c))
+        elif op.kind == "linear":
+            L = op.layer
+            src, dst = B[op.src], B[op.dst]
+            n, k = op.shape_in[0], 1
+            for d in op.shape_in[1:]:
+                k *= d
+            flags = (1 if src.dtype == torch.bfloat16 else 0) | (2 if L.out_bf16 else 0)
+            out.append(K.stage_op(K.OP_LINEAR, src, dst, weight=L.weight, bias=L.bias, n=n, c=k,
+                                  cout=op.shape_out[1], relu=L.relu, flags=flags))
+        elif op.kind == "dwconv":
+            L = op.layer
+            n, h, w, c = op.shape_in
+            _, ho, wo, _ = op.shape_out
+            out.append(K.stage_op(K.OP_DWCONV, B[op.src], B[op.dst], weight=L.weight, scale=L.scale, bias=L.bias,
+                                  n=n, h=h, w=w, c=c, kh=L.k, kw=L.k, stride=L.stride, pad=L.pad, ho=ho, wo=wo,
+                                  relu=L.relu))
+        else:
+            raise ValueError(f"op {op.kind!r} has no persistent-kernel form")
+    return out
+
+
+def stage_launches(net: Network, stage: int, mode: str | None = None) -> int:
+    """Kernel launches one execution of the stage issues."""
+    if (mode or STAGE_MODE) == "persistent":
+        return 1
+    return net.stage_bounds[stage + 1] - net.stage_bounds[stage]
+
+
+def stage_program(net: Network, stage: int, tb: TaskBuffers, grid: int) -> "K.StageProgram":
+    key = (id(net), stage, grid)
+    prog = tb.programs.get(key)
+    if prog is None:
+        a, b = net.stage_bounds[stage], net.stage_bounds[stage + 1]
+        prog = K.StageProgram(stage_ops(net, stage, tb), grid, keep=[op.layer for op in net.ops[a:b]])
+        tb.programs[key] = prog
+    return prog
+
+
+def run_stage(net: Network, stage: int, tb: TaskBuffers, stream, sm_budget: int = 0, mode: str | None = None) -> int:
+    """Launch one stage; returns the number of kernel launches issued."""
+    mode = mode or STAGE_MODE
+    if mode == "persistent":
+        grid = STAGE_GRID or (sm_budget if sm_budget > 0 else K.device_sms())
+        stage_program(net, stage, tb, grid).launch(stream)
+        return 1
     a, b = net.stage_bounds[stage], net.stage_bounds[stage + 1]
     for op in net.ops[a:b]:
         run_op(op, tb, stream, sm_budget)
     return b - a
 
 
-def forward(net: Network, tb: TaskBuffers, x: torch.Tensor | None = None, stream=None, sm_budget: int = 0):
+def forward(net: Network, tb: TaskBuffers, x: torch.Tensor | None = None, stream=None, sm_budget: int = 0,
+            mode: str | None = None):
     if x is not None:
         tb.input.copy_(x)
     for s in range(net.n_stages):
-        run_stage(net, s, tb, stream, sm_budget)
+        run_stage(net, s, tb, stream, sm_budget, mode)
     return _view(tb.output, net.output_shape)

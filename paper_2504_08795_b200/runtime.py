@@ -316,6 +316,10 @@ class DarisRuntime:
             ctxs = range(1, self.gpu.n_contexts + 1)
             if homes is not None and t.priority is Priority.HP:
                 ctxs = [homes[t.id]]
+            for s in range(self.exec.slots):  # stage programs allocate: build them outside capture
+                for st in range(net.n_stages):
+                    if nets.STAGE_MODE == "persistent":
+                        nets.stage_program(net, st, self.buffers[(t.id, s)], nets.STAGE_GRID or self.sm_budget)
             for k in ctxs:
                 for s in range(self.exec.slots):
                     tb = self.buffers[(t.id, s)]
@@ -380,7 +384,15 @@ class DarisRuntime:
         out = {}
         for t in self.tasks:
             if t.model not in by_model:
-                slot_tasks = [t.id] + [rng.choice(ids) for _ in range(n_slots - 1)]
+                # random co-runners, each task at most `slots` times (one buffer set per concurrent copy)
+                if len(ids) * self.exec.slots < n_slots:
+                    raise ValueError(f"AFET calibration needs {n_slots} concurrent jobs but {len(ids)} tasks x "
+                                     f"{self.exec.slots} buffer slots cannot supply them")
+                slot_tasks = [t.id]
+                while len(slot_tasks) < n_slots:
+                    c = rng.choice(ids)
+                    if slot_tasks.count(c) < self.exec.slots:
+                        slot_tasks.append(c)
                 by_model[t.model] = quantize(max(self.exec.busy_calibrate(counts, slot_tasks, seconds),
                                                  2 * QUANTUM))
             out[t.id] = by_model[t.model]
