@@ -43,6 +43,26 @@ template <int BN> struct Depth { static constexpr int kStages = 3; };
 template <> struct Depth<128> { static constexpr int kStages = 2; };
 template <> struct Depth<256> { static constexpr int kStages = 2; };
 
+// Division by a launch-invariant divisor as multiply-high + shift (n < 2^31):
+// a runtime integer division is a ~20-instruction dependent chain and the
+// activation gather needs a dozen of them before its first load.
+struct FDiv {
+  uint32_t mul, shr;  // mul == 0: divisor 1
+};
+static inline FDiv make_fdiv(int d) {
+  FDiv f{0, 0};
+  if (d <= 1) return f;
+  int l = 0;
+  while ((1u << l) < static_cast<uint32_t>(d)) ++l;  // ceil(log2 d)
+  const uint64_t p = 31 + l;
+  f.mul = static_cast<uint32_t>(((1ull << p) + d - 1) / d);
+  f.shr = static_cast<uint32_t>(p - 32);
+  return f;
+}
+__device__ __forceinline__ int fdiv(int n, FDiv d) {
+  return d.mul ? static_cast<int>(__umulhi(static_cast<uint32_t>(n), d.mul) >> d.shr) : n;
+}
+
 struct ConvArgs {
   const __nv_bfloat16* x;
   __nv_bfloat16* y;
@@ -54,6 +74,7 @@ struct ConvArgs {
   int n, h, w, cin, cout, kh, kw, stride, pad, ho, wo;
   int M, relu, num_kb, kb_per_split, splits, cin_blocks;
   unsigned long long* ts;  // optional per-CTA phase timestamps (globaltimer ns), 8 per CTA
+  FDiv d_howo, d_wo, d_kw, d_cinb;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -71,7 +92,8 @@ struct SmemLayout {
   static constexpr int kAOff = 0;
   static constexpr int kBOff = kStages * kABytes;
   static constexpr int kBarOff = kBOff + kStages * kBBytes;
-  static constexpr int kTotal = kBarOff + 256 + 1024;  // + barriers + alignment slack
+  static constexpr int kEpiOff = kBarOff + 256;         // folded-BN scale[BN], bias[BN] of this tile
+  static constexpr int kTotal = kEpiOff + 2 * BN * 4 + 1024;  // + alignment slack
 };
 
 __device__ __forceinline__ float act_apply(float v, int relu) {
@@ -80,36 +102,28 @@ __device__ __forceinline__ float act_apply(float v, int relu) {
   return v;
 }
 
-// 32 accumulator columns of one output row -> scale/bias/residual/act -> bf16.
-__device__ __forceinline__ void finalize_row32(const ConvArgs& a, int m, int col0, const float* v) {
-  if (m >= a.M) return;
-  const float4* sc = reinterpret_cast<const float4*>(a.scale + col0);
-  const float4* bi = reinterpret_cast<const float4*>(a.bias + col0);
+__device__ __forceinline__ uint4 ldg_nc16(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
+
+// 32 accumulator columns of one output row -> scale/bias (smem) + residual
+// (already in registers) -> act -> bf16 NHWC.
+__device__ __forceinline__ void finalize_row32(const ConvArgs& a, int m, int col0, int c_local, const float* v,
+                                               const float* s_scale, const float* s_bias, const uint4* res4) {
   float o[32];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    float4 s = __ldg(sc + q), b = __ldg(bi + q);
-    o[4 * q + 0] = v[4 * q + 0] * s.x + b.x;
-    o[4 * q + 1] = v[4 * q + 1] * s.y + b.y;
-    o[4 * q + 2] = v[4 * q + 2] * s.z + b.z;
-    o[4 * q + 3] = v[4 * q + 3] * s.w + b.w;
-  }
-  const size_t off = static_cast<size_t>(m) * a.cout + col0;
-  if (a.res != nullptr) {
-    const uint4* rp = reinterpret_cast<const uint4*>(a.res + off);
+  for (int j = 0; j < 32; ++j) o[j] = v[j] * s_scale[c_local + j] + s_bias[c_local + j];
+  if (res4 != nullptr) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      uint4 r = __ldg(rp + q);
-      uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+      const uint32_t rr[4] = {res4[q].x, res4[q].y, res4[q].z, res4[q].w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        float2 f = unpack_bf16x2(rr[e]);
+        const float2 f = unpack_bf16x2(rr[e]);
         o[8 * q + 2 * e] += f.x;
         o[8 * q + 2 * e + 1] += f.y;
       }
     }
   }
-  uint4* yp = reinterpret_cast<uint4*>(a.y + off);
+  uint4* yp = reinterpret_cast<uint4*>(a.y + static_cast<size_t>(m) * a.cout + col0);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     uint4 pk;
@@ -122,7 +136,7 @@ __device__ __forceinline__ void finalize_row32(const ConvArgs& a, int m, int col
 }
 
 template <int BN>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __maxnreg__(112)
     conv_igemm_tc_kernel(const __grid_constant__ CUtensorMap wmap, const ConvArgs a) {
   using L = SmemLayout<BN>;
   constexpr int kStages = L::kStages;
@@ -169,24 +183,29 @@ __global__ void __launch_bounds__(kThreads, 3)
     // ---------------- activation producer ----------------
     const int t = threadIdx.x;
     const int row_sub = t >> 3, chunk = t & 7;
+    float* s_scale = reinterpret_cast<float*>(smem + L::kEpiOff);
+    float* s_bias = s_scale + BN;
     int pix_base[8], ih0[8], iw0[8];
     const int howo = a.ho * a.wo;
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
       const int m = m0 + p * 16 + row_sub;
-      if (m < a.M) {
-        const int img = m / howo;
-        const int rem = m - img * howo;
-        const int oh = rem / a.wo, ow = rem - (rem / a.wo) * a.wo;
-        pix_base[p] = img * a.h * a.w;
-        ih0[p] = oh * a.stride - a.pad;
-        iw0[p] = ow * a.stride - a.pad;
-      } else {
-        pix_base[p] = 0;
-        ih0[p] = -1 << 20;  // forces the bounds test to fail
-        iw0[p] = -1 << 20;
-      }
+      const int img = fdiv(m, a.d_howo);
+      const int rem = m - img * howo;
+      const int oh = fdiv(rem, a.d_wo);
+      const int ow = rem - oh * a.wo;
+      const bool in = m < a.M;
+      pix_base[p] = in ? img * a.h * a.w : 0;
+      ih0[p] = in ? oh * a.stride - a.pad : -(1 << 20);  // out-of-range rows fail the bounds test
+      iw0[p] = in ? ow * a.stride - a.pad : -(1 << 20);
     }
+    // folded-BN scale/bias of this tile -> smem (constant: loaded before the dependency wait)
+    for (int c = t; c < BN; c += 128) {
+      s_scale[c] = __ldg(a.scale + n0 + c);
+      s_bias[c] = __ldg(a.bias + n0 + c);
+    }
+    const bool stem = a.cin == 8;
+    const int ksize = a.kh * a.kw;
     pdl_wait();  // activations come from the previous layer
     if (ts && threadIdx.x == 0) ts[2] = gtimer();
     const uint32_t sA_u32 = smem_u32(sA);
@@ -198,15 +217,15 @@ __global__ void __launch_bounds__(kThreads, 3)
       // Normal layers: one position per K block, 64 channels. Stem layers
       // (cin == 8, "pixel chunks"): every chunk is one position's 8 channels.
       int kpos, coff;
-      if (a.cin == 8) {
+      if (stem) {
         kpos = kb * 8 + chunk;
         coff = 0;
       } else {
-        kpos = kb / a.cin_blocks;
+        kpos = fdiv(kb, a.d_cinb);
         coff = (kb - kpos * a.cin_blocks) * kBK + chunk * 8;
       }
-      const bool kvalid = kpos < a.kh * a.kw;
-      const int r_ = kpos / a.kw, s_ = kpos - (kpos / a.kw) * a.kw;
+      const bool kvalid = kpos < ksize;
+      const int r_ = fdiv(kpos, a.d_kw), s_ = kpos - r_ * a.kw;
       const uint32_t stage_base = sA_u32 + s * L::kABytes;
 #pragma unroll
       for (int p = 0; p < 8; ++p) {
@@ -225,101 +244,92 @@ __global__ void __launch_bounds__(kThreads, 3)
         mbar_arrive(&full[(i - kLag) % kStages]);
       }
     }
+    // this thread's first residual chunk: in flight while the last loads land
+    const int row = warp * 32 + lane;
+    const int m = m0 + row;
+    const bool row_ok = m < a.M;
+    const bool has_res = a.res != nullptr && row_ok;
+    const __nv_bfloat16* res_row = has_res ? a.res + static_cast<size_t>(m) * a.cout + n0 : nullptr;
+    uint4 res_cur[4];
+    if (has_res) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) res_cur[q] = ldg_nc16(res_row + 8 * q);
+    }
     cp_async_wait<0>();
     fence_proxy_async_smem();
     for (int i = max(0, nkb - kLag); i < nkb; ++i) mbar_arrive(&full[i % kStages]);
     if (ts && threadIdx.x == 0) ts[3] = gtimer();
 
     // ---------------- epilogue ----------------
-    // operands that do not depend on the accumulator: pull them into L1 while
-    // the last MMAs drain (residual row, folded-BN scale/bias of this tile)
-    {
-      const int m_pf = m0 + warp * 32 + lane;
-      if (a.res != nullptr && m_pf < a.M) {
-        const char* rp = reinterpret_cast<const char*>(a.res + static_cast<size_t>(m_pf) * a.cout + n0);
-        for (int off = 0; off < BN * 2; off += 128) prefetch_l1(rp + off);
-      }
-      if (threadIdx.x < BN / 32) {
-        prefetch_l1(a.scale + n0 + threadIdx.x * 32);
-        prefetch_l1(a.bias + n0 + threadIdx.x * 32);
-      }
-    }
     __syncwarp();
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     if (threadIdx.x == 0) pdl_trigger();  // mainloop done: let the next layer start its prologue
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // scale/bias in smem visible to all producers
     if (ts && threadIdx.x == 0) ts[4] = gtimer();
-    const int row = warp * 32 + lane;
-    const int m = m0 + row;
     const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
     if (a.splits == 1) {
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
+        uint4 res_nxt[4];
+        if (has_res && c0 + 32 < BN) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) res_nxt[q] = ldg_nc16(res_row + c0 + 32 + 8 * q);
+        }
         tmem_ld_32x32b_x32(t_row + c0, r);
-        finalize_row32(a, m, n0 + c0, reinterpret_cast<const float*>(r));
+        if (row_ok)
+          finalize_row32(a, m, n0 + c0, c0, reinterpret_cast<const float*>(r), s_scale, s_bias,
+                         has_res ? res_cur : nullptr);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) res_cur[q] = res_nxt[q];
       }
     } else {
-      // Split-K fix-up. Every split takes a ticket first; the holder of the last
-      // ticket does not publish its own partial: it waits until the other
-      // splits have reduced theirs into the zeroed fp32 accumulator (they are
-      // resident and past their mainloop, so the wait cannot deadlock), then
-      // adds its TMEM partial in registers, runs the epilogue and re-arms the
-      // accumulator and both counters for the next launch.
+      // Split-K: every split reduces its fp32 partial into the zeroed tile
+      // accumulator (red.add at L2), then takes a ticket; the split that
+      // arrives last reads the sum, re-zeroes it, runs the epilogue and
+      // re-arms the ticket for the next launch. Nobody waits for anybody.
       const int tile = tile_m * gridDim.y + tile_n;
       int* ticket_ctr = a.counters + 2 * tile;
-      int* done_ctr = ticket_ctr + 1;
       float* acc_row = a.ws + static_cast<size_t>(tile) * (kBM * BN) + static_cast<size_t>(row) * BN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_row + c0, r);
+        if (row_ok) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            red_add_v4(acc_row + c0 + 4 * q, __uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                       __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+        }
+      }
+      __threadfence();
+      asm volatile("bar.sync 1, 128;" ::: "memory");
       if (threadIdx.x == 0) *last_flag = (atomicAdd(ticket_ctr, 1) == a.splits - 1);
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      const bool last = *last_flag;
-      if (!last) {
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(t_row + c0, r);
-          if (m < a.M) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              red_add_v4(acc_row + c0 + 4 * q, __uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                         __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
-          }
-        }
+      if (*last_flag) {
         __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (threadIdx.x == 0) atomicAdd(done_ctr, 1);
-      } else {
-        if (threadIdx.x == 0) {
-          while (ld_acquire_gpu(done_ctr) < a.splits - 1) {
-          }
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        __threadfence();
+        if (row_ok) {
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(t_row + c0, r);
-          if (m < a.M) {
-            float acc[32];
+          for (int c0 = 0; c0 < BN; c0 += 32) {
             float4* src = reinterpret_cast<float4*>(acc_row + c0);
             float4 part[8];
+            uint4 res_nxt[4];
 #pragma unroll
             for (int q = 0; q < 8; ++q) part[q] = __ldcg(src + q);  // all loads in flight together
+            if (has_res && c0 + 32 < BN) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              acc[4 * q] = __uint_as_float(r[4 * q]) + part[q].x;
-              acc[4 * q + 1] = __uint_as_float(r[4 * q + 1]) + part[q].y;
-              acc[4 * q + 2] = __uint_as_float(r[4 * q + 2]) + part[q].z;
-              acc[4 * q + 3] = __uint_as_float(r[4 * q + 3]) + part[q].w;
-              __stcg(src + q, make_float4(0.f, 0.f, 0.f, 0.f));  // re-arm for the next launch
+              for (int q = 0; q < 4; ++q) res_nxt[q] = ldg_nc16(res_row + c0 + 32 + 8 * q);
             }
-            finalize_row32(a, m, n0 + c0, acc);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) __stcg(src + q, make_float4(0.f, 0.f, 0.f, 0.f));  // re-arm
+            finalize_row32(a, m, n0 + c0, c0, reinterpret_cast<const float*>(part), s_scale, s_bias,
+                           has_res ? res_cur : nullptr);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) res_cur[q] = res_nxt[q];
           }
         }
-        if (threadIdx.x == 0) {
-          ticket_ctr[0] = 0;
-          done_ctr[0] = 0;
-        }
+        if (threadIdx.x == 0) ticket_ctr[0] = 0;
       }
     }
   } else if (warp == 4) {
@@ -415,6 +425,10 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   a.M = d->n * d->ho * d->wo;
   a.relu = d->relu;
   a.cin_blocks = d->cin / kBK;
+  a.d_howo = make_fdiv(d->ho * d->wo);
+  a.d_wo = make_fdiv(d->wo);
+  a.d_kw = make_fdiv(d->kw);
+  a.d_cinb = make_fdiv(a.cin_blocks > 0 ? a.cin_blocks : 1);
   a.num_kb = d->cin == 8 ? (d->kh * d->kw + 7) / 8 : d->kh * d->kw * a.cin_blocks;
   a.kb_per_split = pl.kb_per_split;
   a.splits = pl.splits;
