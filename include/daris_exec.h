@@ -43,6 +43,8 @@ typedef struct daris_exec_partition {
   int32_t sm_count;         /* SMs the partition actually owns */
   int32_t first_group, n_groups;
   int32_t green;            /* 1 if a green context backs it */
+  int32_t group_size;       /* SMs per co-scheduling group: the largest thread-block cluster
+                               a kernel in this partition can launch (8; 2 with DARIS_PART_GROUP=2) */
 } daris_exec_partition;
 
 /* per-stage execution record (one per completed stage) */

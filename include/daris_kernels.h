@@ -52,15 +52,20 @@ typedef struct daris_conv_desc {
   int32_t block_n;        /* 0 = auto, else 64/128/256 */
   int32_t splits;         /* 0 = auto, else forced split-K factor */
   int32_t sm_budget;      /* SMs available to this launch (0 = whole device) */
-  int32_t _pad;
+  int32_t flags;          /* DARIS_CONV_CLUSTER_SPLITK: the launch context can co-schedule
+                             clusters of up to 8 CTAs, so split-K partials are reduced through
+                             distributed shared memory instead of global atomics */
   void* timestamps;       /* optional: 8 uint64 globaltimer stamps per CTA (profiling), or NULL */
 } daris_conv_desc;
+
+enum { DARIS_CONV_CLUSTER_SPLITK = 1 };
 
 typedef struct daris_conv_plan_t {
   int32_t block_n, splits, kb_per_split, tiles_m, tiles_n;
   int64_t workspace_floats; /* needed in desc.workspace */
   int32_t counters;         /* needed in desc.counters */
   int32_t ctas;
+  int32_t cluster;          /* CTAs per cluster (split-K through DSMEM), 1 = none */
 } daris_conv_plan_t;
 
 int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out);

@@ -59,7 +59,7 @@ Driver& driver() {
 }
 
 struct Partition {
-  int sm_count = 0, first_group = 0, n_groups = 0;
+  int sm_count = 0, first_group = 0, n_groups = 0, group_size = 0;
   CUgreenCtx green = nullptr;
   std::vector<cudaStream_t> streams;     // low (default) priority: LP stages
   std::vector<cudaStream_t> streams_hi;  // highest priority: HP stages (CTA scheduling preference)
@@ -142,11 +142,17 @@ int build_partitions(daris_exec* ex) {
     CUdevResource all;
     if (d.getDevResource(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) green = false;
     if (green) {
+      // Co-scheduled 8-SM groups (the hardware granularity on cc >= 9.0): a kernel
+      // in the partition can launch clusters of up to 8 CTAs (split-K through DSMEM).
+      // DARIS_PART_GROUP=2 trades that for 2-SM granularity (IGNORE_SM_COSCHEDULING:
+      // clusters of 2 only; tools/probe_cluster.cu).
+      const char* ge = std::getenv("DARIS_PART_GROUP");
+      const bool fine = ge && std::atoi(ge) == 2;
       unsigned n = static_cast<unsigned>(all.sm.smCount);
       groups.resize(n);
       CUdevResource rem;
-      if (d.split(groups.data(), &n, &all, &rem, CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING, 2) !=
-              CUDA_SUCCESS ||
+      if (d.split(groups.data(), &n, &all, &rem, fine ? CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING : 0,
+                  fine ? 2 : 8) != CUDA_SUCCESS ||
           n == 0)
         green = false;
       groups.resize(n);
@@ -156,8 +162,11 @@ int build_partitions(daris_exec* ex) {
   const int gsize = green ? static_cast<int>(groups[0].sm.smCount) : 2;
   for (int k = 0; k < c.n_contexts; ++k) {
     Partition& p = ex->parts[k];
-    int want = (c.sm_per_context + gsize - 1) / gsize;
+    // nearest whole number of groups (at least one): 74 SMs -> 9 x 8 = 72 or 37 x 2 = 74
+    int want = (c.sm_per_context + gsize / 2) / gsize;
+    if (want < 1) want = 1;
     if (want > G) want = G;
+    p.group_size = green ? gsize : total_sms;
     p.n_groups = want;
     p.first_group = static_cast<int>((static_cast<long long>(k) * G) / c.n_contexts);
     p.sm_count = want * gsize;
@@ -172,7 +181,9 @@ int build_partitions(daris_exec* ex) {
     }
     int prio_low = 0, prio_high = 0;
     cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
-    if (std::getenv("DARIS_NO_HIPRIO")) prio_high = prio_low;  // experiment knob
+    // HP stages on higher-priority streams is opt-in: measured on the C2 knee it
+    // starves LP stages of CTA slots (LP misses bind first) for no HP gain
+    if (!std::getenv("DARIS_HP_STREAM_PRIORITY")) prio_high = prio_low;
     const int n_streams = 2 * c.n_streams + 1;  // low + high priority per slot, + capture stream
     for (int s = 0; s < n_streams; ++s) {
       const int prio = (s >= c.n_streams && s < 2 * c.n_streams) ? prio_high : prio_low;
@@ -299,7 +310,7 @@ const char* daris_exec_last_error(const daris_exec* ex) { return ex ? ex->err.c_
 int daris_exec_partition_info(const daris_exec* ex, int32_t context, daris_exec_partition* out) {
   if (context < 1 || context > ex->cfg.n_contexts) return DARIS_E_VALUE;
   const Partition& p = ex->parts[context - 1];
-  *out = daris_exec_partition{context, p.sm_count, p.first_group, p.n_groups, p.green ? 1 : 0};
+  *out = daris_exec_partition{context, p.sm_count, p.first_group, p.n_groups, p.green ? 1 : 0, p.group_size};
   return DARIS_OK;
 }
 

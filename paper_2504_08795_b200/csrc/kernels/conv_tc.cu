@@ -73,6 +73,7 @@ struct ConvArgs {
   int* counters;
   int n, h, w, cin, cout, kh, kw, stride, pad, ho, wo;
   int M, relu, num_kb, kb_per_split, splits, cin_blocks;
+  int cluster_split;  // 1: the splits of a tile form one cluster and reduce through DSMEM
   unsigned long long* ts;  // optional per-CTA phase timestamps (globaltimer ns), 8 per CTA
   FDiv d_howo, d_wo, d_kw, d_cinb;
 };
@@ -268,7 +269,27 @@ __global__ void __maxnreg__(112)
     asm volatile("bar.sync 1, 128;" ::: "memory");  // scale/bias in smem visible to all producers
     if (ts && threadIdx.x == 0) ts[4] = gtimer();
     const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
-    if (a.splits == 1) {
+    if (BN == 64 && a.cluster_split) {
+      // Split-K inside one cluster: every split parks its fp32 partial tile in
+      // its own (now idle) A ring, the cluster barrier publishes them, and CTA
+      // r finalises rows [r*128/S, (r+1)*128/S) by summing the S partials
+      // over distributed shared memory. 16-B chunks are XOR-swizzled by row so
+      // the per-row stores do not collide on banks.
+      float4* part = reinterpret_cast<float4*>(sA);  // [128][BN/4], chunk c of row r at c ^ (r & 15)
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_row + c0, r);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          part[row * (BN / 4) + (((c0 / 4) + q) ^ (row & 15))] =
+              make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
+                          __uint_as_float(r[4 * q + 3]));
+      }
+    }
+    if (BN == 64 && a.cluster_split) {
+      // (cluster barrier and reduction below, executed by all 192 threads)
+    } else if (a.splits == 1) {
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
@@ -365,6 +386,57 @@ __global__ void __maxnreg__(112)
     }
   }
 
+  if (BN == 64 && a.cluster_split) {
+    __syncwarp();
+    cluster_sync();  // every split's partial is in its smem
+    if (warp < 4) {
+      const int S = a.splits;
+      const int rank = split;  // cluster dims (1, 1, splits): the rank is the split index
+      const int r_begin = (rank * kBM) / S, r_end = ((rank + 1) * kBM) / S;
+      const int items = (r_end - r_begin) * (BN / 8);  // (row, 8-column group)
+      float* s_scale = reinterpret_cast<float*>(smem + L::kEpiOff);
+      float* s_bias = s_scale + BN;
+      const uint32_t part_u32 = smem_u32(sA);
+      for (int it = threadIdx.x; it < items; it += 128) {
+        const int rr = r_begin + it / (BN / 8), g = it % (BN / 8);
+        const int m = m0 + rr;
+        if (m >= a.M) continue;
+        const uint32_t off0 = static_cast<uint32_t>((rr * (BN / 4) + ((2 * g) ^ (rr & 15))) * 16);
+        const uint32_t off1 = static_cast<uint32_t>((rr * (BN / 4) + ((2 * g + 1) ^ (rr & 15))) * 16);
+        float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int k = 0; k < S; ++k) {
+          const float4 p0 = ld_dsmem_f4(dsmem_map(part_u32 + off0, k));
+          const float4 p1 = ld_dsmem_f4(dsmem_map(part_u32 + off1, k));
+          v[0] += p0.x; v[1] += p0.y; v[2] += p0.z; v[3] += p0.w;
+          v[4] += p1.x; v[5] += p1.y; v[6] += p1.z; v[7] += p1.w;
+        }
+        const int c = g * 8;
+        const size_t off = static_cast<size_t>(m) * a.cout + n0 + c;
+        float rf[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (a.res != nullptr) {
+          const uint4 rv = ldg_nc16(a.res + off);
+          const uint32_t rr4[4] = {rv.x, rv.y, rv.z, rv.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = unpack_bf16x2(rr4[e]);
+            rf[2 * e] = f.x;
+            rf[2 * e + 1] = f.y;
+          }
+        }
+        float o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = act_apply(v[e] * s_scale[c + e] + s_bias[c + e] + rf[e], a.relu);
+        uint4 pk;
+        pk.x = pack_bf16x2(o[0], o[1]);
+        pk.y = pack_bf16x2(o[2], o[3]);
+        pk.z = pack_bf16x2(o[4], o[5]);
+        pk.w = pack_bf16x2(o[6], o[7]);
+        *reinterpret_cast<uint4*>(a.y + off) = pk;
+      }
+    }
+    __syncwarp();
+    cluster_sync();  // peers finished reading this CTA's partial
+  }
   if (ts && threadIdx.x == 0) ts[5] = gtimer();
   tc_fence_before();
   __syncthreads();
@@ -432,17 +504,25 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   a.num_kb = d->cin == 8 ? (d->kh * d->kw + 7) / 8 : d->kh * d->kw * a.cin_blocks;
   a.kb_per_split = pl.kb_per_split;
   a.splits = pl.splits;
+  a.cluster_split = pl.cluster > 1 ? 1 : 0;
   a.ts = reinterpret_cast<unsigned long long*>(d->timestamps);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.tiles_m, pl.tiles_n, pl.splits);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = L::kTotal;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (pl.cluster > 1) {
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 1;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = pl.cluster;
+    cfg.numAttrs = 2;
+  }
   return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN>, map, a));
 }
 
@@ -497,6 +577,8 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
     return e ? std::atoi(e) : 0;
   }();
   if (split_cap > 0 && splits > split_cap) splits = split_cap;
+  // a cluster holds at most 8 CTAs (portable size)
+  if ((d->flags & DARIS_CONV_CLUSTER_SPLITK) && bn == 64 && splits > 8) splits = 8;
   if (splits > num_kb) splits = num_kb;
   int kbps = (num_kb + splits - 1) / splits;
   splits = (num_kb + kbps - 1) / kbps;  // no empty splits
@@ -508,6 +590,11 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
   out->workspace_floats = splits > 1 ? static_cast<int64_t>(tiles) * kBM * bn : 0;  // zero-initialised
   out->counters = splits > 1 ? 2 * tiles : 0;  // ticket + done per tile
   out->ctas = tiles * splits;
+  out->cluster = (splits > 1 && bn == 64 && (d->flags & DARIS_CONV_CLUSTER_SPLITK)) ? splits : 1;
+  if (out->cluster > 1) {  // partials reduce through DSMEM: no global scratch
+    out->workspace_floats = 0;
+    out->counters = 0;
+  }
   return DARIS_K_OK;
 }
 
@@ -517,7 +604,7 @@ extern "C" int daris_conv2d(const daris_conv_desc* d, void* stream) {
   int rc = daris_conv_plan(d, &pl);
   if (rc != DARIS_K_OK) return rc;
   if (!d->x || !d->y || !d->weight || !d->scale || !d->bias) return DARIS_K_BAD_ARG;
-  if (pl.splits > 1 && (!d->workspace || !d->counters)) return DARIS_K_WORKSPACE;
+  if (pl.splits > 1 && pl.cluster == 1 && (!d->workspace || !d->counters)) return DARIS_K_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (pl.block_n) {
     case 64: return launch_bn<64>(d, pl, st);

@@ -27,7 +27,7 @@ class ConvDesc(C.Structure):
         ("n", C.c_int32), ("h", C.c_int32), ("w", C.c_int32), ("cin", C.c_int32), ("cout", C.c_int32),
         ("kh", C.c_int32), ("kw", C.c_int32), ("stride", C.c_int32), ("pad", C.c_int32),
         ("ho", C.c_int32), ("wo", C.c_int32), ("relu", C.c_int32), ("block_n", C.c_int32),
-        ("splits", C.c_int32), ("sm_budget", C.c_int32), ("_pad", C.c_int32), ("timestamps", C.c_void_p),
+        ("splits", C.c_int32), ("sm_budget", C.c_int32), ("flags", C.c_int32), ("timestamps", C.c_void_p),
     ]
 
 
@@ -35,7 +35,7 @@ class ConvPlan(C.Structure):
     _fields_ = [
         ("block_n", C.c_int32), ("splits", C.c_int32), ("kb_per_split", C.c_int32),
         ("tiles_m", C.c_int32), ("tiles_n", C.c_int32), ("workspace_floats", C.c_int64),
-        ("counters", C.c_int32), ("ctas", C.c_int32),
+        ("counters", C.c_int32), ("ctas", C.c_int32), ("cluster", C.c_int32),
     ]
 
 
@@ -109,7 +109,13 @@ def _check(rc: int, what: str) -> None:
         raise KernelError(f"{what} failed with status {rc}")
 
 
-def conv_desc(x_shape, cout, kh, kw, stride, pad, *, relu=1, block_n=0, splits=0, sm_budget=0) -> ConvDesc:
+# split-K through thread-block clusters + DSMEM; needs partitions whose SM
+# groups can co-schedule 8-CTA clusters (the executor's default green contexts)
+CLUSTER_SPLITK = True
+
+
+def conv_desc(x_shape, cout, kh, kw, stride, pad, *, relu=1, block_n=0, splits=0, sm_budget=0,
+              cluster: bool | None = None) -> ConvDesc:
     n, h, w, cin = x_shape
     ho = (h + 2 * pad - kh) // stride + 1
     wo = (w + 2 * pad - kw) // stride + 1
@@ -117,6 +123,7 @@ def conv_desc(x_shape, cout, kh, kw, stride, pad, *, relu=1, block_n=0, splits=0
     d.n, d.h, d.w, d.cin, d.cout = n, h, w, cin, cout
     d.kh, d.kw, d.stride, d.pad, d.ho, d.wo = kh, kw, stride, pad, ho, wo
     d.relu, d.block_n, d.splits, d.sm_budget = relu, block_n, splits, sm_budget
+    d.flags = 1 if (CLUSTER_SPLITK if cluster is None else cluster) else 0
     return d
 
 
@@ -130,11 +137,12 @@ def conv2d(x: torch.Tensor, weight: torch.Tensor, scale: torch.Tensor, bias: tor
            stride: int = 1, pad: int = 0, relu: int = 1, residual: torch.Tensor | None = None,
            out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
            counters: torch.Tensor | None = None, block_n: int = 0, splits: int = 0,
-           sm_budget: int = 0, stream=None, timestamps: torch.Tensor | None = None) -> torch.Tensor:
+           sm_budget: int = 0, stream=None, timestamps: torch.Tensor | None = None,
+           cluster: bool | None = None) -> torch.Tensor:
     """x: [n,h,w,cin] bf16 NHWC; weight: [cout,kh,kw,cin] bf16."""
     cout, kh, kw, cin = weight.shape
     d = conv_desc(tuple(x.shape), cout, kh, kw, stride, pad, relu=relu, block_n=block_n,
-                  splits=splits, sm_budget=sm_budget)
+                  splits=splits, sm_budget=sm_budget, cluster=cluster)
     p = conv_plan(d)
     if out is None:
         out = torch.empty((d.n, d.ho, d.wo, cout), dtype=torch.bfloat16, device=x.device)

@@ -42,7 +42,7 @@ class ExecConfigC(C.Structure):
 
 class PartitionC(C.Structure):
     _fields_ = [("context", C.c_int32), ("sm_count", C.c_int32), ("first_group", C.c_int32),
-                ("n_groups", C.c_int32), ("green", C.c_int32)]
+                ("n_groups", C.c_int32), ("green", C.c_int32), ("group_size", C.c_int32)]
 
 
 class StageTraceC(C.Structure):
@@ -123,7 +123,9 @@ class Executor:
             p = PartitionC()
             L.daris_exec_partition_info(h, k, C.byref(p))
             self.partitions.append({"context": p.context, "sm_count": p.sm_count, "first_group": p.first_group,
-                                    "n_groups": p.n_groups, "green": bool(p.green)})
+                                    "n_groups": p.n_groups, "green": bool(p.green), "group_size": p.group_size})
+        # split-K through 8-CTA clusters only where every partition can co-schedule them
+        K.CLUSTER_SPLITK = min(p["group_size"] for p in self.partitions) >= 8
 
     def _c(self, rc: int, what: str) -> None:
         if rc != 0:

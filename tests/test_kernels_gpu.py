@@ -27,7 +27,7 @@ def _close(out, ref):
 
 
 def _conv_case(n, h, w, cin, cout, k, stride, pad, relu=1, residual=False, block_n=0, splits=0,
-               sm_budget=0, seed=0):
+               sm_budget=0, seed=0, cluster=None):
     from paper_2504_08795_b200 import kernels as K
     g = torch.Generator().manual_seed(seed)
     x = torch.randn(n, h, w, cin, generator=g).bfloat16()
@@ -48,7 +48,7 @@ def _conv_case(n, h, w, cin, cout, k, stride, pad, relu=1, residual=False, block
     dev = torch.device("cuda")
     out = K.conv2d(x.to(dev), wt.to(dev), scale.to(dev), bias.to(dev), stride=stride, pad=pad, relu=relu,
                    residual=None if res is None else res.to(dev), block_n=block_n, splits=splits,
-                   sm_budget=sm_budget)
+                   sm_budget=sm_budget, cluster=cluster)
     torch.cuda.synchronize()
     _close(out, ref)
 
@@ -78,13 +78,23 @@ def test_conv_relu6():
     _conv_case(1, 14, 14, 64, 128, 1, 1, 0, relu=6)
 
 
+@pytest.mark.parametrize("cluster", [True, False])
 @pytest.mark.parametrize("splits", [2, 3, 8])
-def test_conv_split_k_forced(splits):
-    _conv_case(1, 7, 7, 512, 512, 3, 1, 1, splits=splits, residual=True)
+def test_conv_split_k_forced(splits, cluster):
+    # cluster=True: split-K partials reduced through DSMEM inside one cluster;
+    # cluster=False: red.add into a global fp32 tile + last-arriver fix-up
+    _conv_case(1, 7, 7, 512, 512, 3, 1, 1, splits=splits, residual=True, cluster=cluster)
 
 
-def test_conv_split_k_auto_small_m():
-    _conv_case(1, 7, 7, 512, 512, 3, 1, 1, sm_budget=74)
+@pytest.mark.parametrize("cluster", [True, False])
+def test_conv_split_k_auto_small_m(cluster):
+    _conv_case(1, 7, 7, 512, 512, 3, 1, 1, sm_budget=74, cluster=cluster)
+
+
+@pytest.mark.parametrize("cluster", [True, False])
+def test_conv_split_k_tail_rows_and_odd_cluster(cluster):
+    # M = 196 (two M tiles, the second mostly past the end), 5 splits (odd cluster size)
+    _conv_case(1, 14, 14, 256, 256, 3, 1, 1, splits=5, residual=True, cluster=cluster, seed=7)
 
 
 def test_conv_batch_tail_tile():
@@ -100,12 +110,13 @@ def test_conv_split_k_repeat_resets_counters():
     wt = (torch.randn(512, 3, 3, 512, generator=g) / 48).bfloat16().to(dev)
     s = torch.ones(512, device=dev)
     b = torch.zeros(512, device=dev)
-    d = K.conv_desc((1, 7, 7, 512), 512, 3, 3, 1, 1, sm_budget=148)
+    d = K.conv_desc((1, 7, 7, 512), 512, 3, 3, 1, 1, sm_budget=148, cluster=False)
     p = K.conv_plan(d)
-    assert p.splits > 1
+    assert p.splits > 1 and p.cluster == 1
     ws = torch.zeros(p.workspace_floats, device=dev)
     ctr = torch.zeros(p.counters, dtype=torch.int32, device=dev)
-    outs = [K.conv2d(x, wt, s, b, pad=1, workspace=ws, counters=ctr, sm_budget=148).clone() for _ in range(3)]
+    outs = [K.conv2d(x, wt, s, b, pad=1, workspace=ws, counters=ctr, sm_budget=148, cluster=False).clone()
+            for _ in range(3)]
     torch.cuda.synchronize()
     assert int(ctr.abs().sum()) == 0          # tickets re-armed
     assert float(ws.abs().sum()) == 0.0       # accumulators re-zeroed
