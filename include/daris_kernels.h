@@ -55,7 +55,7 @@ typedef struct daris_conv_desc {
   int32_t flags;          /* DARIS_CONV_CLUSTER_SPLITK: the launch context can co-schedule
                              clusters of up to 8 CTAs, so split-K partials are reduced through
                              distributed shared memory instead of global atomics */
-  void* timestamps;       /* optional: 8 uint64 globaltimer stamps per CTA (profiling), or NULL */
+  void* timestamps;       /* optional: 16 uint64 globaltimer stamps per CTA (profiling), or NULL */
 } daris_conv_desc;
 
 enum { DARIS_CONV_CLUSTER_SPLITK = 1 };
@@ -66,6 +66,7 @@ typedef struct daris_conv_plan_t {
   int32_t counters;         /* needed in desc.counters */
   int32_t ctas;
   int32_t cluster;          /* CTAs per cluster (split-K through DSMEM), 1 = none */
+  int32_t tma_rows;         /* > 0: activations arrive by TMA, M tile = tma_rows whole output rows */
 } daris_conv_plan_t;
 
 int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out);

@@ -27,6 +27,8 @@
 #include <cudaTypedefs.h>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <algorithm>
 #include <mutex>
 #include "sm100.cuh"
 #include "../../../include/daris_kernels.h"
@@ -74,8 +76,10 @@ struct ConvArgs {
   int n, h, w, cin, cout, kh, kw, stride, pad, ho, wo;
   int M, relu, num_kb, kb_per_split, splits, cin_blocks;
   int cluster_split;  // 1: the splits of a tile form one cluster and reduce through DSMEM
-  unsigned long long* ts;  // optional per-CTA phase timestamps (globaltimer ns), 8 per CTA
-  FDiv d_howo, d_wo, d_kw, d_cinb;
+  int tma_a;          // 1: activations arrive by TMA (4-D box = th whole output rows of one image)
+  int th, tiles_h;    // TMA mode: output rows per M tile, M tiles per image
+  unsigned long long* ts;  // optional per-CTA phase timestamps (globaltimer ns), 16 per CTA
+  FDiv d_howo, d_wo, d_kw, d_cinb, d_tiles_h;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -138,7 +142,8 @@ __device__ __forceinline__ void finalize_row32(const ConvArgs& a, int m, int col
 
 template <int BN>
 __global__ void __maxnreg__(112)
-    conv_igemm_tc_kernel(const __grid_constant__ CUtensorMap wmap, const ConvArgs a) {
+    conv_igemm_tc_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
+                         const ConvArgs a) {
   using L = SmemLayout<BN>;
   constexpr int kStages = L::kStages;
   constexpr int kLag = L::kLag;
@@ -151,28 +156,46 @@ __global__ void __maxnreg__(112)
   uint64_t* tmem_full = empty + kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  uint64_t* red_bar = tmem_full + 2;  // cluster split-K: this CTA's rows of every split have landed
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int tile_m = blockIdx.x, tile_n = blockIdx.y, split = blockIdx.z;
-  unsigned long long* ts = a.ts ? a.ts + 8ull * (blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) : nullptr;
+  unsigned long long* ts = a.ts ? a.ts + 16ull * (blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) : nullptr;
   if (ts && threadIdx.x == 0) ts[0] = gtimer();
-  const int m0 = tile_m * kBM, n0 = tile_n * BN;
+  // M tile -> first output pixel m0 and number of valid rows. Gather mode: 128
+  // consecutive flattened pixels. TMA mode: th whole output rows of one image
+  // (th * wo <= 128 rows; the rest of the 128-row MMA tile is ignored).
+  int m0, mvalid, img = 0, h0 = 0;
+  if (a.tma_a) {
+    img = fdiv(tile_m, a.d_tiles_h);
+    h0 = (tile_m - img * a.tiles_h) * a.th;
+    m0 = img * (a.ho * a.wo) + h0 * a.wo;
+    mvalid = min(a.th, a.ho - h0) * a.wo;
+  } else {
+    m0 = tile_m * kBM;
+    mvalid = min(kBM, a.M - m0);
+  }
+  const int n0 = tile_n * BN;
   const int kb_begin = split * a.kb_per_split;
   const int kb_end = min(a.num_kb, kb_begin + a.kb_per_split);
   const int nkb = kb_end - kb_begin;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 128 + 1);
+      mbar_init(&full[s], a.tma_a ? 1 : 128 + 1);  // TMA mode: one expect_tx arrival covers A and B
       mbar_init(&empty[s], 1);
     }
     mbar_init(tmem_full, 1);
+    mbar_init(red_bar, 1);
     fence_barrier_init();
   }
   if (warp == 4) {
     tmem_alloc<BN>(tmem_slot);
-    if (lane == 0) tma_prefetch_desc(&wmap);
+    if (lane == 0) {
+      tma_prefetch_desc(&wmap);
+      if (a.tma_a) tma_prefetch_desc(&amap);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -181,29 +204,33 @@ __global__ void __maxnreg__(112)
   if (ts && threadIdx.x == 0) ts[1] = gtimer();
 
   if (warp < 4) {
-    // ---------------- activation producer ----------------
+    // ---------------- activation producer (gather mode) + epilogue ----------------
     const int t = threadIdx.x;
     const int row_sub = t >> 3, chunk = t & 7;
     float* s_scale = reinterpret_cast<float*>(smem + L::kEpiOff);
     float* s_bias = s_scale + BN;
+    // folded-BN scale/bias of this tile -> smem (constant: loaded before the dependency wait)
+    for (int c = t; c < BN; c += 128) {
+      s_scale[c] = __ldg(a.scale + n0 + c);
+      s_bias[c] = __ldg(a.bias + n0 + c);
+    }
+    if (a.tma_a) {
+      pdl_wait();  // the residual below comes from an earlier layer
+      if (ts && threadIdx.x == 0) ts[2] = gtimer();
+    } else {
     int pix_base[8], ih0[8], iw0[8];
     const int howo = a.ho * a.wo;
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
       const int m = m0 + p * 16 + row_sub;
-      const int img = fdiv(m, a.d_howo);
-      const int rem = m - img * howo;
+      const int im = fdiv(m, a.d_howo);
+      const int rem = m - im * howo;
       const int oh = fdiv(rem, a.d_wo);
       const int ow = rem - oh * a.wo;
       const bool in = m < a.M;
-      pix_base[p] = in ? img * a.h * a.w : 0;
+      pix_base[p] = in ? im * a.h * a.w : 0;
       ih0[p] = in ? oh * a.stride - a.pad : -(1 << 20);  // out-of-range rows fail the bounds test
       iw0[p] = in ? ow * a.stride - a.pad : -(1 << 20);
-    }
-    // folded-BN scale/bias of this tile -> smem (constant: loaded before the dependency wait)
-    for (int c = t; c < BN; c += 128) {
-      s_scale[c] = __ldg(a.scale + n0 + c);
-      s_bias[c] = __ldg(a.bias + n0 + c);
     }
     const bool stem = a.cin == 8;
     const int ksize = a.kh * a.kw;
@@ -245,10 +272,14 @@ __global__ void __maxnreg__(112)
         mbar_arrive(&full[(i - kLag) % kStages]);
       }
     }
-    // this thread's first residual chunk: in flight while the last loads land
+    cp_async_wait<0>();
+    fence_proxy_async_smem();
+    for (int i = max(0, nkb - kLag); i < nkb; ++i) mbar_arrive(&full[i % kStages]);
+    }  // gather mode
+    // this thread's first residual chunk: in flight while the last loads land / MMAs drain
     const int row = warp * 32 + lane;
     const int m = m0 + row;
-    const bool row_ok = m < a.M;
+    const bool row_ok = row < mvalid;
     const bool has_res = a.res != nullptr && row_ok;
     const __nv_bfloat16* res_row = has_res ? a.res + static_cast<size_t>(m) * a.cout + n0 : nullptr;
     uint4 res_cur[4];
@@ -256,9 +287,6 @@ __global__ void __maxnreg__(112)
 #pragma unroll
       for (int q = 0; q < 4; ++q) res_cur[q] = ldg_nc16(res_row + 8 * q);
     }
-    cp_async_wait<0>();
-    fence_proxy_async_smem();
-    for (int i = max(0, nkb - kLag); i < nkb; ++i) mbar_arrive(&full[i % kStages]);
     if (ts && threadIdx.x == 0) ts[3] = gtimer();
 
     // ---------------- epilogue ----------------
@@ -269,23 +297,14 @@ __global__ void __maxnreg__(112)
     asm volatile("bar.sync 1, 128;" ::: "memory");  // scale/bias in smem visible to all producers
     if (ts && threadIdx.x == 0) ts[4] = gtimer();
     const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
-    if (BN == 64 && a.cluster_split) {
-      // Split-K inside one cluster: every split parks its fp32 partial tile in
-      // its own (now idle) A ring, the cluster barrier publishes them, and CTA
-      // r finalises rows [r*128/S, (r+1)*128/S) by summing the S partials
-      // over distributed shared memory. 16-B chunks are XOR-swizzled by row so
-      // the per-row stores do not collide on banks.
-      float4* part = reinterpret_cast<float4*>(sA);  // [128][BN/4], chunk c of row r at c ^ (r & 15)
-#pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_row + c0, r);
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          part[row * (BN / 4) + (((c0 / 4) + q) ^ (row & 15))] =
-              make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
-                          __uint_as_float(r[4 * q + 3]));
-      }
+    if (BN == 64 && a.cluster_split && threadIdx.x == 0) {
+      // Split-K inside one cluster: CTA r owns rows [r*128/S, (r+1)*128/S) of
+      // the tile and receives those rows of all S partials (st.async into its
+      // idle A ring); arm its mbarrier for them before the cluster barrier.
+      const int S = a.splits;
+      const int r_begin = (split * kBM) / S, r_end = ((split + 1) * kBM) / S;
+      const int valid = max(0, min(r_end, mvalid) - r_begin);
+      mbar_arrive_expect_tx(red_bar, static_cast<uint32_t>(S * valid * BN * 4));
     }
     if (BN == 64 && a.cluster_split) {
       // (cluster barrier and reduction below, executed by all 192 threads)
@@ -355,13 +374,40 @@ __global__ void __maxnreg__(112)
     }
   } else if (warp == 4) {
     // ---------------- weight producer (TMA) ----------------
-    if (lane == 0) {
+    if (lane == 0 && !a.tma_a) {
       // weights are constant: stream them before waiting on the previous layer
       for (int i = 0; i < nkb; ++i) {
         const int s = i % kStages;
         if (i >= kStages) mbar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
         mbar_arrive_expect_tx(&full[s], L::kBBytes);
         tma_load_2d(&wmap, &full[s], sB + s * L::kBBytes, (kb_begin + i) * kBK, n0);
+      }
+    } else if (lane == 0) {
+      // TMA mode: activations too. K block kb = (kernel position r,s ; 64-channel
+      // block c); its A tile is the 4-D box {64 ch, wo cols, th rows, 1 image}
+      // at input (c, s - pad, h0*stride - pad + r, img), traversed with the conv
+      // stride; padding comes from TMA's zero fill of out-of-bounds elements.
+      const uint32_t a_bytes = static_cast<uint32_t>(a.th * a.wo * 128);
+      auto load_a = [&](int i, int s) {
+        const int kb = kb_begin + i;
+        const int kpos = fdiv(kb, a.d_cinb);
+        const int cb = kb - kpos * a.cin_blocks;
+        const int r_ = fdiv(kpos, a.d_kw), s_ = kpos - r_ * a.kw;
+        tma_load_4d(&amap, &full[s], sA + s * L::kABytes, cb * kBK, s_ - a.pad, h0 * a.stride - a.pad + r_, img);
+      };
+      const int pre = min(nkb, kStages);
+      for (int i = 0; i < pre; ++i) {  // weights first: they do not depend on the previous layer
+        mbar_arrive_expect_tx(&full[i], L::kBBytes + a_bytes);
+        tma_load_2d(&wmap, &full[i], sB + i * L::kBBytes, (kb_begin + i) * kBK, n0);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) load_a(i, i);
+      for (int i = pre; i < nkb; ++i) {
+        const int s = i % kStages;
+        mbar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[s], L::kBBytes + a_bytes);
+        tma_load_2d(&wmap, &full[s], sB + s * L::kBBytes, (kb_begin + i) * kBK, n0);
+        load_a(i, s);
       }
     }
   } else {
@@ -387,34 +433,60 @@ __global__ void __maxnreg__(112)
   }
 
   if (BN == 64 && a.cluster_split) {
+    const int S = a.splits;
+    const int rpc_max = (kBM + S - 1) / S;
+    float* recv = reinterpret_cast<float*>(sA);  // [S][rpc_max][BN] fp32
     __syncwarp();
-    cluster_sync();  // every split's partial is in its smem
+    if (ts && threadIdx.x == 0) ts[8] = gtimer();
+    cluster_sync();  // every split's MMAs are done (rings idle) and every receiver is armed
+    if (ts && threadIdx.x == 0) ts[9] = gtimer();
     if (warp < 4) {
-      const int S = a.splits;
-      const int rank = split;  // cluster dims (1, 1, splits): the rank is the split index
-      const int r_begin = (rank * kBM) / S, r_end = ((rank + 1) * kBM) / S;
-      const int items = (r_end - r_begin) * (BN / 8);  // (row, 8-column group)
+      // push this thread's accumulator row to the CTA that owns it
+      const int row = warp * 32 + lane;
+      const bool push = row < mvalid;
+      const int owner = ((row + 1) * S - 1) / kBM;
+      const int j = row - (owner * kBM) / S;
+      const uint32_t dst = dsmem_map(smem_u32(recv + (static_cast<size_t>(split) * rpc_max + j) * BN), owner);
+      const uint32_t bar = dsmem_map(smem_u32(red_bar), owner);
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_row + c0, r);  // warp-collective (.sync.aligned): every lane loads
+        if (push) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            st_async_v4(dst + (c0 + 4 * q) * 4, __uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                        __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]), bar);
+        }
+      }
+    }
+    __syncwarp();
+    cluster_arrive();  // (released before exit: no CTA leaves while peers may still push to it)
+    if (warp < 4) {
+      const int r_begin = (split * kBM) / S, r_end = ((split + 1) * kBM) / S;
+      const int valid = max(0, min(r_end, mvalid) - r_begin);
+      mbar_wait(red_bar, 0);
+      if (ts && threadIdx.x == 0) ts[10] = gtimer();
       float* s_scale = reinterpret_cast<float*>(smem + L::kEpiOff);
       float* s_bias = s_scale + BN;
-      const uint32_t part_u32 = smem_u32(sA);
+      const int items = valid * (BN / 8);  // (row, 8-column group)
       for (int it = threadIdx.x; it < items; it += 128) {
-        const int rr = r_begin + it / (BN / 8), g = it % (BN / 8);
-        const int m = m0 + rr;
-        if (m >= a.M) continue;
-        const uint32_t off0 = static_cast<uint32_t>((rr * (BN / 4) + ((2 * g) ^ (rr & 15))) * 16);
-        const uint32_t off1 = static_cast<uint32_t>((rr * (BN / 4) + ((2 * g + 1) ^ (rr & 15))) * 16);
+        const int j = it / (BN / 8), g = it % (BN / 8);
+        const int m = m0 + r_begin + j;
+        const int c = g * 8;
+        const size_t off = static_cast<size_t>(m) * a.cout + n0 + c;
+        uint4 rv = make_uint4(0, 0, 0, 0);
+        if (a.res != nullptr) rv = ldg_nc16(a.res + off);
         float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         for (int k = 0; k < S; ++k) {
-          const float4 p0 = ld_dsmem_f4(dsmem_map(part_u32 + off0, k));
-          const float4 p1 = ld_dsmem_f4(dsmem_map(part_u32 + off1, k));
+          const float4* src = reinterpret_cast<const float4*>(recv + (static_cast<size_t>(k) * rpc_max + j) * BN + c);
+          const float4 p0 = src[0], p1 = src[1];
           v[0] += p0.x; v[1] += p0.y; v[2] += p0.z; v[3] += p0.w;
           v[4] += p1.x; v[5] += p1.y; v[6] += p1.z; v[7] += p1.w;
         }
-        const int c = g * 8;
-        const size_t off = static_cast<size_t>(m) * a.cout + n0 + c;
         float rf[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         if (a.res != nullptr) {
-          const uint4 rv = ldg_nc16(a.res + off);
           const uint32_t rr4[4] = {rv.x, rv.y, rv.z, rv.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
@@ -435,7 +507,8 @@ __global__ void __maxnreg__(112)
       }
     }
     __syncwarp();
-    cluster_sync();  // peers finished reading this CTA's partial
+    if (ts && threadIdx.x == 0) ts[11] = gtimer();
+    cluster_wait();
   }
   if (ts && threadIdx.x == 0) ts[5] = gtimer();
   tc_fence_before();
@@ -476,6 +549,24 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return DARIS_K_BAD_ARG;
+  CUtensorMap amap;
+  std::memset(&amap, 0, sizeof(amap));
+  if (pl.tma_rows > 0) {
+    // activations NHWC as a 4-D tensor (c, w, h, n); one box = th output rows x wo
+    // output columns x 64 channels, traversed with the conv stride
+    const int th = pl.tma_rows;
+    cuuint64_t adims[4] = {static_cast<cuuint64_t>(d->cin), static_cast<cuuint64_t>(d->w),
+                           static_cast<cuuint64_t>(d->h), static_cast<cuuint64_t>(d->n)};
+    cuuint64_t astr[3] = {static_cast<cuuint64_t>(d->cin) * 2, static_cast<cuuint64_t>(d->w) * d->cin * 2,
+                          static_cast<cuuint64_t>(d->h) * d->w * d->cin * 2};
+    cuuint32_t abox[4] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(d->wo * d->stride),
+                          static_cast<cuuint32_t>(th * d->stride), 1};
+    cuuint32_t aestr[4] = {1, static_cast<cuuint32_t>(d->stride), static_cast<cuuint32_t>(d->stride), 1};
+    r = encode(&amap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(d->x), adims, astr, abox, aestr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return DARIS_K_BAD_ARG;
+  }
 
   static bool attr_set = false;  // per template instantiation
   if (!attr_set) {
@@ -505,6 +596,10 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   a.kb_per_split = pl.kb_per_split;
   a.splits = pl.splits;
   a.cluster_split = pl.cluster > 1 ? 1 : 0;
+  a.tma_a = pl.tma_rows > 0 ? 1 : 0;
+  a.th = pl.tma_rows > 0 ? pl.tma_rows : 1;
+  a.tiles_h = (d->ho + a.th - 1) / a.th;
+  a.d_tiles_h = make_fdiv(a.tiles_h);
   a.ts = reinterpret_cast<unsigned long long*>(d->timestamps);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.tiles_m, pl.tiles_n, pl.splits);
@@ -523,7 +618,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
     attr[1].val.clusterDim.z = pl.cluster;
     cfg.numAttrs = 2;
   }
-  return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN>, map, a));
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN>, map, amap, a));
 }
 
 }  // namespace daris
@@ -548,7 +643,14 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
   const int M = d->n * d->ho * d->wo;
   const int num_kb = d->cin == 8 ? (d->kh * d->kw + 7) / 8 : d->kh * d->kw * (d->cin / kBK);
   const int budget = d->sm_budget > 0 ? d->sm_budget : daris_device_sms();
-  const int tiles_m = (M + kBM - 1) / kBM;
+  // Activations by TMA (4-D box of th whole output rows) unless the layer is a
+  // stem (8 channels: pixel-chunk gather) or a box side would exceed 256.
+  static const bool tma_off = std::getenv("DARIS_CONV_GATHER") != nullptr;  // experiment knob
+  const int th = std::max(1, std::min(d->ho, kBM / d->wo));
+  const bool tma_a = !tma_off && d->cin % kBK == 0 && d->wo * d->stride <= 256 && th * d->stride <= 256 &&
+                     d->wo <= kBM;
+  const int tiles_h = (d->ho + th - 1) / th;
+  const int tiles_m = tma_a ? d->n * tiles_h : (M + kBM - 1) / kBM;
   int bn = d->block_n;
   if (bn == 0) {
     bn = (d->cout % 128 == 0) ? 128 : 64;
@@ -591,6 +693,7 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
   out->counters = splits > 1 ? 2 * tiles : 0;  // ticket + done per tile
   out->ctas = tiles * splits;
   out->cluster = (splits > 1 && bn == 64 && (d->flags & DARIS_CONV_CLUSTER_SPLITK)) ? splits : 1;
+  out->tma_rows = tma_a ? th : 0;
   if (out->cluster > 1) {  // partials reduce through DSMEM: no global scratch
     out->workspace_floats = 0;
     out->counters = 0;

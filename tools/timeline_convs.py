@@ -37,12 +37,13 @@ def main():
     tb = nets.allocate_buffers(net, sm_budget=args.sms)
     sp = ex.stream(1, 0)
     s = torch.cuda.ExternalStream(sp)
+    args.sms = ex.partitions[0]["sm_count"]  # the partition's actual SM count (whole 8-SM groups)
     ts = {}
     for i, op in enumerate(net.ops):
         if op.kind == "conv":
             L = op.layer
             p = K.conv_plan(K.conv_desc(op.shape_in, L.cout, L.kh, L.kw, L.stride, L.pad, sm_budget=args.sms))
-            ts[i] = torch.zeros(p.ctas * 8, dtype=torch.int64, device="cuda")
+            ts[i] = torch.zeros(p.ctas * 16, dtype=torch.int64, device="cuda")
 
     def forward(stream):
         for i, op in enumerate(net.ops):
@@ -73,7 +74,7 @@ def main():
     for i, op in enumerate(net.ops):
         if op.kind != "conv":
             continue
-        a = ts[i].view(-1, 8).cpu().double()
+        a = ts[i].view(-1, 16).cpu().double()
         if t_origin is None:
             t_origin = a[:, 0].min().item()
         a = (a - t_origin) / 1e3  # us
