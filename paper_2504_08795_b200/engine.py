@@ -295,13 +295,16 @@ class Simulation:
         return self._result(h, rep, effective, full)
 
     def run_trace(self, durations: dict[tuple[int, int, int], float],
-                  full_load: dict[int, float]) -> SimResult:
+                  full_load: dict[int, float], phases: Sequence[float] | None = None) -> SimResult:
         """Trace-replay mode: stage (task, job, stage) runs for
-        durations[...] seconds at rate 1; AFET baselines are given."""
+        durations[...] seconds at rate 1; AFET baselines are given; `phases`
+        (release offsets in task-id order) replace the seeded draw, e.g. the
+        ones a real GPU run used."""
         effective = self._effective()
         h = self._open(effective)
         h.set_full_load([full_load[i] for i in h.task_ids])
         h.populate()
         self.handle = h
-        rep = h.trace_run(self.duration, self.warmup_frac, self.phases(effective), durations, self.collect_log)
+        ph = list(phases) if phases is not None else self.phases(effective)
+        rep = h.trace_run(self.duration, self.warmup_frac, ph, durations, self.collect_log)
         return self._result(h, rep, effective, dict(full_load))

@@ -25,20 +25,24 @@ class DnnProfile:
     width_fraction: float
     batching: BatchingCurve
     default_batch: int
+    model: str | None = None      # the network the gpu backend runs for this profile (None: none exists)
 
 
-def _p(name, jps, fractions, width, ref_b, gain):
-    return DnnProfile(name, 1.0 / jps, fractions, width, BatchingCurve(ref_b, gain), ref_b)
+def _p(name, jps, fractions, width, ref_b, gain, model=None):
+    return DnnProfile(name, 1.0 / jps, fractions, width, BatchingCurve(ref_b, gain), ref_b, model)
 
 
 PROFILES: dict[str, DnnProfile] = {
     # reference profiles (RTX 2080 Ti numbers, Table II)
-    "resnet18": _p("resnet18", 627.0, (0.30, 0.30, 0.25, 0.15), 0.40, 4, 1.63),
+    "resnet18": _p("resnet18", 627.0, (0.30, 0.30, 0.25, 0.15), 0.40, 4, 1.63, "resnet18"),
     "unet": _p("unet", 241.0, (0.30, 0.20, 0.20, 0.30), 0.75, 2, 1.08),
     "inceptionv3": _p("inceptionv3", 142.0, (0.20, 0.30, 0.30, 0.20), 0.20, 8, 3.13),
     # B200 profiles measured with the native kernels (batch 1, 74-SM partition)
-    "resnet50_b200": _p("resnet50_b200", 1.0 / 534e-6, (0.22, 0.20, 0.38, 0.20), 0.50, 32, 6.0),
-    "resnet18_b200": _p("resnet18_b200", 1.0 / 260e-6, (0.33, 0.33, 0.34), 0.50, 32, 6.0),
+    "resnet50_b200": _p("resnet50_b200", 1.0 / 534e-6, (0.22, 0.20, 0.38, 0.20), 0.50, 32, 6.0, "resnet50"),
+    "resnet18_b200": _p("resnet18_b200", 1.0 / 260e-6, (0.33, 0.33, 0.34), 0.50, 32, 6.0, "resnet18"),
+    "vgg16_b200": _p("vgg16_b200", 1.0 / 900e-6, (0.25, 0.25, 0.25, 0.25), 0.50, 32, 6.0, "vgg16"),
+    "mobilenet_v2_b200": _p("mobilenet_v2_b200", 1.0 / 150e-6, (0.34, 0.33, 0.33), 0.50, 32, 6.0,
+                            "mobilenet_v2"),
 }
 
 
@@ -76,6 +80,11 @@ WORKLOADS: dict[str, list[tuple[str, int, int, float]]] = {
     "unet": [("unet", 5, 10, 24.0)],
     "inceptionv3": [("inceptionv3", 9, 18, 24.0)],
     "mixed": [("resnet18", 17, 34, 30.0), ("unet", 5, 10, 24.0), ("inceptionv3", 9, 18, 24.0)],
+    # BASELINE.json configs on one B200 (rates are starting points; bench.py searches the knee)
+    "c1_resnet18_b200": [("resnet18_b200", 1, 1, 30.0)],
+    "c2_resnet50_b200": [("resnet50_b200", 4, 4, 1000.0)],
+    "c3_mixed_b200": [("resnet18_b200", 1, 1, 600.0), ("resnet50_b200", 1, 1, 600.0),
+                      ("vgg16_b200", 1, 1, 300.0), ("mobilenet_v2_b200", 1, 1, 600.0)],
 }
 
 
@@ -86,6 +95,16 @@ def _main(workload: str) -> dict:
 
 
 SCENARIO_PRESETS: dict[str, dict] = {f"{w}_main": _main(w) for w in ("resnet18", "unet", "inceptionv3", "mixed")}
+# BASELINE.json configs[0..2] as scenarios (148 SMs). With "backend": "gpu" they run on the
+# real device; with the default "sim" backend they run through the rate model.
+SCENARIO_PRESETS.update({
+    "c1_b200": {"gpu": {"total_sms": 148, "n_contexts": 2, "n_streams": 2, "oversubscription": 1,
+                        "policy": "mps-str"}, "workload": {"preset": "c1_resnet18_b200"}},
+    "c2_b200": {"gpu": {"total_sms": 148, "n_contexts": 4, "n_streams": 2, "oversubscription": 2,
+                        "policy": "mps-str"}, "workload": {"preset": "c2_resnet50_b200"}},
+    "c3_b200": {"gpu": {"total_sms": 148, "n_contexts": 4, "n_streams": 2, "oversubscription": 2,
+                        "policy": "mps-str"}, "workload": {"preset": "c3_mixed_b200"}, "stage_migration": True},
+})
 
 
 def get_scenario_preset(name: str) -> dict:

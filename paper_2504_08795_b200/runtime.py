@@ -239,7 +239,8 @@ class DarisRuntime:
     def __init__(self, tasks: Sequence[TaskDef], gpu: GpuConfig, *, slots: int = 3, partition: str = "green",
                  window_size: int = 5, flags: AblationFlags = AblationFlags(), hpa: bool = False,
                  stage_migration: bool = False, seed: int = 0, e2e: bool = False, pool_size: int = 64,
-                 device: int = 0, phasing: str = "random"):
+                 device: int = 0, phasing: str = "random", placement_order: str = "descending_util",
+                 edf_on_job_deadline: bool = False):
         if not torch.cuda.is_available():
             raise RuntimeError("DarisRuntime needs a CUDA device (there is no CPU fallback)")
         if phasing not in ("random", "zero"):
@@ -250,6 +251,8 @@ class DarisRuntime:
         self.seed = seed
         self.flags, self.hpa, self.window_size = flags, hpa, window_size
         self.stage_migration = stage_migration
+        self.placement_order = placement_order
+        self.edf_on_job_deadline = edf_on_job_deadline
         self.e2e = e2e
         self.device = torch.device("cuda", device)
         self.sm_per_ctx = sm_per_context(gpu)
@@ -367,6 +370,8 @@ class DarisRuntime:
         dicts = [spec_to_dict(s) for s in self.specs()]
         opts = _core.options_struct(window_size=self.window_size, no_last=self.flags.no_last,
                                     no_prior=self.flags.no_prior, no_fixed=self.flags.no_fixed, hpa=self.hpa,
+                                    placement_order=self.placement_order,
+                                    edf_on_job_deadline=self.edf_on_job_deadline,
                                     stage_migration=self.stage_migration)
         h = _core.Handle(self.gpu.native(), dicts, opts)
         h.set_full_load([full_load[i] for i in h.task_ids])

@@ -1,0 +1,189 @@
+"""BASELINE.json configs beyond the headline on one B200 (bench.py runs C2).
+
+  c1      2 ResNet-18 tasks (1 HP, 1 LP) at 30 JPS, 2 contexts x 2 streams, OS=1, 3 stages
+  c3      mixed ResNet-18/50, VGG-16, MobileNetV2 (1 HP + 1 LP each), 4x2 OS=2, knee of a
+          common rate factor (task rate = factor / isolated latency of its model), stage
+          migration off vs on
+  c4      OS in {1,1.5,2,3} x contexts {2,4,8} x streams {1,2,4} (OS <= contexts) for the C2 task
+          set (8 ResNet-50, 4 HP / 4 LP): knee inferences/s per cell
+  tasks   C5 per GPU: ResNet-50 task count {8,12,16,24} at 4x2 OS=2, knee per count
+
+Every knee uses bench.py's search (HP miss = 0, LP DMR < 2 %) and its GPU-stall
+re-measure rule. One JSON object per cell on stdout.
+
+  python tools/configs_gpu.py c1 c3 c4 tasks [--probe-seconds 0.6] [--c4-cells 2x2_1,4x2_2]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import bench  # noqa: E402
+from paper_2504_08795_b200.gpu import GpuConfig, Policy  # noqa: E402
+from paper_2504_08795_b200.model import Priority  # noqa: E402
+from paper_2504_08795_b200.runtime import DarisRuntime, TaskDef  # noqa: E402
+
+
+def log(m):
+    print(m, file=sys.stderr, flush=True)
+
+
+def emit(d):
+    print(json.dumps(d), flush=True)
+
+
+def summary(rep) -> dict:
+    return {"jps": round(rep.jps, 1), "hp_miss": int(rep.missed_hp), "dmr_lp": round(rep.dmr_lp, 4),
+            "rejected_lp": int(rep.rejected_lp), "p99_hp_ms": round(rep.response_hp.p99 * 1e3, 3),
+            "p99_lp_ms": round(rep.response_lp.p99 * 1e3, 3)}
+
+
+def knee_factor(rt, set_factor, f0: float, probe: float) -> tuple[float, object]:
+    """Largest factor with HP miss 0 / LP DMR < 2 % (grow x1.3, then 5 bisections)."""
+    lo, hi, best = 0.0, None, None
+    f = f0
+    for _ in range(10):
+        set_factor(f)
+        res = bench.run_clean(rt, probe, probe * 0.25, log, f"f={f:.3g}")[0]
+        ok = bench.feasible(res.report)
+        log(f"  probe f={f:.4g} ok={ok} {summary(res.report)}")
+        if ok:
+            lo, best = f, res
+            f *= 1.3
+        else:
+            hi = f
+            break
+    if hi is not None:
+        for _ in range(5):
+            mid = 0.5 * (lo + hi)
+            set_factor(mid)
+            res = bench.run_clean(rt, probe, probe * 0.25, log, f"f={mid:.3g}")[0]
+            ok = bench.feasible(res.report)
+            log(f"  bisect f={mid:.4g} ok={ok} {summary(res.report)}")
+            if ok:
+                lo, best = mid, res
+            else:
+                hi = mid
+    return lo, best
+
+
+def confirm(rt, set_factor, f: float, seconds: float):
+    """Timed confirmation at the knee; step down 5 % while it breaks the constraints."""
+    for _ in range(4):
+        set_factor(f)
+        res = bench.run_clean(rt, seconds, seconds * 0.1, log, f"confirm {f:.3g}")[0]
+        if bench.feasible(res.report):
+            return f, res
+        f *= 0.95
+    return f, res
+
+
+def c1(args):
+    gpu = GpuConfig(148, 2, 2, 1.0, Policy.MPS_STR)
+    tasks = [TaskDef(1, "resnet18", Priority.HP, 30.0, 3), TaskDef(2, "resnet18", Priority.LP, 30.0, 3)]
+    rt = DarisRuntime(tasks, gpu, slots=3, seed=0)
+    rt.capture_all()
+    rt.afet = rt.calibrate_full_load(0.3)
+    res = bench.run_clean(rt, 3.0, 0.3, log, "c1 30jps")[0]
+    out = {"config": "c1", "rate_per_task": 30.0, "partition_sms": [p["sm_count"] for p in rt.exec.partitions],
+           "isolated_ms": round(sum(rt.stage_nominal["resnet18"]) * 1e3, 3), **summary(res.report)}
+    iso = sum(rt.stage_nominal["resnet18"])
+    f, best = knee_factor(rt, rt.set_rate, 0.5 / iso, args.probe_seconds)
+    f, res = confirm(rt, rt.set_rate, f, 2.0)
+    out["knee"] = {"rate_per_task": round(f, 1), **summary(res.report)}
+    emit(out)
+    rt.close()
+
+
+def c3(args):
+    gpu = GpuConfig(148, 4, 2, 2.0, Policy.MPS_STR)
+    models = ["resnet18", "resnet50", "vgg16", "mobilenet_v2"]
+    stages = {"resnet18": 3, "resnet50": 4, "vgg16": 4, "mobilenet_v2": 3}
+    for mig in (False, True):
+        tasks = []
+        for i, m in enumerate(models):
+            tasks.append(TaskDef(2 * i + 1, m, Priority.HP, 100.0, stages[m]))
+            tasks.append(TaskDef(2 * i + 2, m, Priority.LP, 100.0, stages[m]))
+        rt = DarisRuntime(tasks, gpu, slots=3, seed=0, stage_migration=mig)
+        rt.capture_all()
+        rt.afet = rt.calibrate_full_load(0.3)
+        iso = {m: sum(v) for m, v in rt.stage_nominal.items()}
+
+        def set_factor(f, rt=rt, iso=iso):
+            for t in rt.tasks:
+                t.rate = f / iso[t.model]
+
+        f, best = knee_factor(rt, set_factor, 0.05, args.probe_seconds)
+        f, res = confirm(rt, set_factor, f, 2.0)
+        per_model = {}
+        for t in rt.tasks:
+            per_model.setdefault(t.model, 0.0)
+            per_model[t.model] += t.rate
+        flops = {m: rt.nets[(m, stages[m])].flops_per_image for m in models}
+        tflops = sum(per_model[m] * flops[m] for m in models) / 1e12
+        emit({"config": "c3", "stage_migration": mig, "knee_factor": round(f, 4),
+              "isolated_ms": {m: round(v * 1e3, 3) for m, v in iso.items()},
+              "rate_per_task": {m: round(per_model[m] / 2, 1) for m in models},
+              "model_tflops": round(tflops, 2), **summary(res.report)})
+        rt.close()
+
+
+def c4(args):
+    cells = []
+    for os_ in (1.0, 1.5, 2.0, 3.0):
+        for nc in (2, 4, 8):
+            for ns in (1, 2, 4):
+                if os_ <= nc:
+                    cells.append((nc, ns, os_))
+    if args.c4_cells:
+        want = set(args.c4_cells.split(","))
+        cells = [c for c in cells if f"{c[0]}x{c[1]}_{c[2]:g}" in want]
+    for nc, ns, os_ in cells:
+        t0 = time.time()
+        gpu = GpuConfig(148, nc, ns, os_, Policy.MPS_STR)
+        slots = 3 if 8 * 3 >= nc * ns else 4
+        rt = DarisRuntime(bench.c2_tasks(100.0, list(range(8))), gpu, slots=slots, seed=0)
+        rt.capture_all()
+        rt.afet = rt.calibrate_full_load(0.2)
+        iso = sum(rt.stage_nominal["resnet50"])
+        f, best = knee_factor(rt, rt.set_rate, 0.5 * min(8, nc * ns) / iso / 8, args.probe_seconds)
+        f, res = confirm(rt, rt.set_rate, f, 1.0)
+        emit({"config": "c4", "cell": f"{nc}x{ns}_{os_:g}", "contexts": nc, "streams": ns, "oversubscription": os_,
+              "partition_sms": rt.exec.partitions[0]["sm_count"], "isolated_ms": round(iso * 1e3, 3),
+              "knee_rate_per_task": round(f, 1), "seconds": round(time.time() - t0, 1), **summary(res.report)})
+        rt.close()
+
+
+def task_scaling(args):
+    gpu = GpuConfig(148, 4, 2, 2.0, Policy.MPS_STR)
+    for n in (8, 12, 16, 24):
+        rt = DarisRuntime(bench.c2_tasks(100.0, list(range(n))), gpu, slots=3, seed=0)
+        rt.capture_all()
+        rt.afet = rt.calibrate_full_load(0.2)
+        iso = sum(rt.stage_nominal["resnet50"])
+        f, best = knee_factor(rt, rt.set_rate, 0.5 * 8 / iso / n, args.probe_seconds)
+        f, res = confirm(rt, rt.set_rate, f, 1.0)
+        emit({"config": "tasks", "tasks": n, "contexts": 4, "streams": 2, "oversubscription": 2.0,
+              "knee_rate_per_task": round(f, 1), **summary(res.report)})
+        rt.close()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("which", nargs="+", choices=["c1", "c3", "c4", "tasks"])
+    ap.add_argument("--probe-seconds", type=float, default=0.6)
+    ap.add_argument("--c4-cells", default="")
+    args = ap.parse_args()
+    for w in args.which:
+        {"c1": c1, "c3": c3, "c4": c4, "tasks": task_scaling}[w](args)
+
+
+if __name__ == "__main__":
+    main()
