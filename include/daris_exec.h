@@ -82,6 +82,11 @@ int daris_exec_stream(daris_exec* ex, int32_t context, int32_t stream, void** ou
 int daris_exec_capture_begin(daris_exec* ex, int32_t context, void** stream_out);
 int daris_exec_capture_end(daris_exec* ex, int32_t task, int32_t stage, int32_t context, int32_t slot);
 int daris_exec_graph_count(const daris_exec* ex, int64_t* out);
+/* Isolated time of one captured stage graph: `reps` back-to-back launches on
+ * the partition's stream 0 between CUDA events (after 3 warm launches); the
+ * stage's nominal_time (model.py:24-27 StageProfile) on this partition. */
+int daris_exec_time_graph(daris_exec* ex, int32_t task, int32_t stage, int32_t context, int32_t slot, int32_t reps,
+                          double* out_seconds);
 
 /* per (task, slot) I/O buffers. input: device buffer the first stage reads;
  * output: device buffer the last stage writes. Pools: n_inputs images of

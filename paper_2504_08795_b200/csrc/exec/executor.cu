@@ -349,6 +349,30 @@ int daris_exec_capture_end(daris_exec* ex, int32_t task, int32_t stage, int32_t 
   return DARIS_OK;
 }
 
+int daris_exec_time_graph(daris_exec* ex, int32_t task, int32_t stage, int32_t context, int32_t slot, int32_t reps,
+                          double* out_seconds) {
+  if (context < 1 || context > ex->cfg.n_contexts || task < 1 || task > ex->cfg.max_tasks || stage < 0 ||
+      stage >= ex->cfg.max_stages || slot < 0 || slot >= ex->cfg.slots_per_task || reps < 1 || !out_seconds)
+    return fail(ex, "bad graph key");
+  cudaGraphExec_t g = ex->graphs[ex->gidx(task, stage, context, slot)];
+  if (!g) return fail(ex, "no graph captured for that key");
+  cudaStream_t s = ex->parts[context - 1].streams[0];
+  cudaEvent_t e0, e1;
+  CUDA_TRY(ex, cudaEventCreate(&e0));
+  CUDA_TRY(ex, cudaEventCreate(&e1));
+  for (int i = 0; i < 3; ++i) CUDA_TRY(ex, cudaGraphLaunch(g, s));  // warm (L2, icache, TMA descriptors)
+  CUDA_TRY(ex, cudaEventRecord(e0, s));
+  for (int i = 0; i < reps; ++i) CUDA_TRY(ex, cudaGraphLaunch(g, s));
+  CUDA_TRY(ex, cudaEventRecord(e1, s));
+  CUDA_TRY(ex, cudaEventSynchronize(e1));
+  float ms = 0.f;
+  CUDA_TRY(ex, cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *out_seconds = static_cast<double>(ms) * 1e-3 / reps;
+  return DARIS_OK;
+}
+
 int daris_exec_graph_count(const daris_exec* ex, int64_t* out) {
   *out = ex->graph_count;
   return DARIS_OK;

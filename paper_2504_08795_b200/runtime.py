@@ -80,6 +80,7 @@ def exec_lib() -> C.CDLL:
             "daris_exec_run": [vp, vp, f64, f64, P(f64), i32, P(_core.ReportC), P(ExecStatsC)],
             "daris_exec_busy_calibrate": [vp, P(i32), i32, P(i32), f64, P(f64)],
             "daris_exec_set_stall_threshold": [vp, f64],
+            "daris_exec_time_graph": [vp, i32, i32, i32, i32, i32, P(f64)],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
@@ -153,6 +154,12 @@ class Executor:
             exec_lib().daris_exec_capture_end(self._h, 1, 0, context, 0)
             raise
         self._c(exec_lib().daris_exec_capture_end(self._h, task, stage, context, slot), "capture_end")
+
+    def time_graph(self, task: int, stage: int, context: int, slot: int = 0, reps: int = 20) -> float:
+        out = C.c_double()
+        self._c(exec_lib().daris_exec_time_graph(self._h, task, stage, context, slot, reps, C.byref(out)),
+                "time_graph")
+        return out.value
 
     def graph_count(self) -> int:
         out = C.c_int64()
@@ -259,7 +266,11 @@ class DarisRuntime:
         max_stages = 8
         self.exec = Executor(gpu.n_contexts, gpu.n_streams, self.sm_per_ctx, partition=partition, slots=slots,
                              max_tasks=max(t.id for t in self.tasks), max_stages=max_stages, device=device)
-        self.sm_budget = min(p["sm_count"] for p in self.exec.partitions)
+        # SMs the layer planner sizes grids (tiles x split-K) for: the partition by
+        # default; DARIS_PLAN_SMS plans for a smaller share (fewer, longer CTAs:
+        # less fix-up work per job when every SM is shared by several jobs)
+        import os
+        self.sm_budget = int(os.environ.get("DARIS_PLAN_SMS", "0")) or min(p["sm_count"] for p in self.exec.partitions)
         # one weight copy per model, shared by all tasks running it
         self.nets: dict[tuple, nets.Network] = {}
         for t in self.tasks:
@@ -276,7 +287,8 @@ class DarisRuntime:
         self._pool_cache: dict = {}
         self._make_pools(pool_size)
         torch.cuda.synchronize()
-        self.stage_nominal = self._measure_isolated()
+        self._warm()
+        self._nominal: dict[str, list[float]] | None = None
         self.handle = None
         self.afet: dict[int, float] | None = None
 
@@ -335,27 +347,32 @@ class DarisRuntime:
                         n += 1
         return n
 
-    def _measure_isolated(self, reps: int = 20) -> dict[str, list[float]]:
-        """Isolated per-stage time of each model in one partition (nominal_time)."""
-        out = {}
+    def _warm(self) -> None:
+        """One eager pass of every stage (kernel attributes, tensor maps, stage
+        programs) before anything is captured."""
         stream = torch.cuda.Stream(device=self.device)
-        for (model, _), net in self.nets.items():
-            tb = self.buffers[(next(t.id for t in self.tasks if t.model == model), 0)]
-            times = []
-            with torch.cuda.stream(stream):
+        with torch.cuda.stream(stream):
+            for (model, _), net in self.nets.items():
+                tb = self.buffers[(next(t.id for t in self.tasks if t.model == model), 0)]
                 for st in range(net.n_stages):
-                    for _ in range(3):
-                        nets.run_stage(net, st, tb, stream.cuda_stream, self.sm_budget)
-                    e0 = torch.cuda.Event(enable_timing=True)
-                    e1 = torch.cuda.Event(enable_timing=True)
-                    e0.record(stream)
-                    for _ in range(reps):
-                        nets.run_stage(net, st, tb, stream.cuda_stream, self.sm_budget)
-                    e1.record(stream)
-                    e1.synchronize()
-                    times.append(max(e0.elapsed_time(e1) / 1e3 / reps, 2 * QUANTUM))
-            out[model] = times
-        return out
+                    nets.run_stage(net, st, tb, stream.cuda_stream, self.sm_budget)
+        stream.synchronize()
+
+    @property
+    def stage_nominal(self) -> dict[str, list[float]]:
+        """Isolated per-stage time of each model (the StageProfile nominal_time):
+        its captured stage graph replayed alone on partition 1, CUDA-event timed."""
+        if self._nominal is None:
+            if self.exec.graph_count() == 0:
+                self.capture_all()
+            out = {}
+            for t in self.tasks:
+                if t.model in out:
+                    continue
+                out[t.model] = [max(self.exec.time_graph(t.id, st, 1, 0, 20), 2 * QUANTUM)
+                                for st in range(self.net_of(t).n_stages)]
+            self._nominal = out
+        return self._nominal
 
     # -- dispatcher ----------------------------------------------------------
     def specs(self) -> list[TaskSpec]:

@@ -45,33 +45,9 @@ def summary(rep) -> dict:
             "p99_lp_ms": round(rep.response_lp.p99 * 1e3, 3)}
 
 
-def knee_factor(rt, set_factor, f0: float, probe: float) -> tuple[float, object]:
-    """Largest factor with HP miss 0 / LP DMR < 2 % (grow x1.3, then 5 bisections)."""
-    lo, hi, best = 0.0, None, None
-    f = f0
-    for _ in range(10):
-        set_factor(f)
-        res = bench.run_clean(rt, probe, probe * 0.25, log, f"f={f:.3g}")[0]
-        ok = bench.feasible(res.report)
-        log(f"  probe f={f:.4g} ok={ok} {summary(res.report)}")
-        if ok:
-            lo, best = f, res
-            f *= 1.3
-        else:
-            hi = f
-            break
-    if hi is not None:
-        for _ in range(5):
-            mid = 0.5 * (lo + hi)
-            set_factor(mid)
-            res = bench.run_clean(rt, probe, probe * 0.25, log, f"f={mid:.3g}")[0]
-            ok = bench.feasible(res.report)
-            log(f"  bisect f={mid:.4g} ok={ok} {summary(res.report)}")
-            if ok:
-                lo, best = mid, res
-            else:
-                hi = mid
-    return lo, best
+def knee_factor(rt, set_factor, f0: float, probe: float) -> tuple[float, None]:
+    """bench.py's knee: the feasible rate factor with the most completed jobs/s."""
+    return bench.knee_search(rt, f0, probe, log, set_rate=set_factor), None
 
 
 def confirm(rt, set_factor, f: float, seconds: float):
@@ -95,7 +71,7 @@ def c1(args):
     out = {"config": "c1", "rate_per_task": 30.0, "partition_sms": [p["sm_count"] for p in rt.exec.partitions],
            "isolated_ms": round(sum(rt.stage_nominal["resnet18"]) * 1e3, 3), **summary(res.report)}
     iso = sum(rt.stage_nominal["resnet18"])
-    f, best = knee_factor(rt, rt.set_rate, 0.5 / iso, args.probe_seconds)
+    f, best = knee_factor(rt, rt.set_rate, 0.6 * 4 / max(rt.afet.values()) / 2, args.probe_seconds)
     f, res = confirm(rt, rt.set_rate, f, 2.0)
     out["knee"] = {"rate_per_task": round(f, 1), **summary(res.report)}
     emit(out)
@@ -120,7 +96,9 @@ def c3(args):
             for t in rt.tasks:
                 t.rate = f / iso[t.model]
 
-        f, best = knee_factor(rt, set_factor, 0.05, args.probe_seconds)
+        # factor f: every task at f / (its isolated latency); start below the loaded capacity
+        f0 = 0.6 * 8 / sum(rt.afet[t.id] / iso[t.model] for t in rt.tasks)
+        f, best = knee_factor(rt, set_factor, f0, args.probe_seconds)
         f, res = confirm(rt, set_factor, f, 2.0)
         per_model = {}
         for t in rt.tasks:
@@ -153,7 +131,8 @@ def c4(args):
         rt.capture_all()
         rt.afet = rt.calibrate_full_load(0.2)
         iso = sum(rt.stage_nominal["resnet50"])
-        f, best = knee_factor(rt, rt.set_rate, 0.5 * min(8, nc * ns) / iso / 8, args.probe_seconds)
+        f, best = knee_factor(rt, rt.set_rate, 0.6 * min(8, nc * ns) / max(rt.afet.values()) / 8,
+                              args.probe_seconds)
         f, res = confirm(rt, rt.set_rate, f, 1.0)
         emit({"config": "c4", "cell": f"{nc}x{ns}_{os_:g}", "contexts": nc, "streams": ns, "oversubscription": os_,
               "partition_sms": rt.exec.partitions[0]["sm_count"], "isolated_ms": round(iso * 1e3, 3),
@@ -168,7 +147,7 @@ def task_scaling(args):
         rt.capture_all()
         rt.afet = rt.calibrate_full_load(0.2)
         iso = sum(rt.stage_nominal["resnet50"])
-        f, best = knee_factor(rt, rt.set_rate, 0.5 * 8 / iso / n, args.probe_seconds)
+        f, best = knee_factor(rt, rt.set_rate, 0.6 * 8 / max(rt.afet.values()) / n, args.probe_seconds)
         f, res = confirm(rt, rt.set_rate, f, 1.0)
         emit({"config": "tasks", "tasks": n, "contexts": 4, "streams": 2, "oversubscription": 2.0,
               "knee_rate_per_task": round(f, 1), **summary(res.report)})
