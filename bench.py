@@ -205,17 +205,19 @@ def conv_roofline(rt, peaks) -> dict:
                                                 "ncu --set full (profiles/r01_conv_ncu_full_raw.csv)",
             "launches_per_inference": len(conv), "flops_per_launch_avg": flops // len(conv),
             "avg_launch_us": round(t_conv / len(conv) * 1e6, 3), "share_of_inference": round(t_conv / t_all, 4),
-            "partition_sms": rt.sm_budget, "peak_kind": f"bf16 dense burst ({peaks['source']})"}
+            "partition_sms": rt.partition_sms, "plan_sms": rt.sm_budget,
+            "peak_kind": f"bf16 dense burst ({peaks['source']})"}
 
 
-def batching_baseline(batches=(1, 2, 4, 8, 16, 32), reps: int = 20) -> dict:
+def batching_baseline(batches=(1, 2, 4, 8, 16, 32, 64), reps: int = 20) -> dict:
     """Single-tenant batched inference of the same model with the same kernels on
-    the whole GPU (one 148-SM green partition, one stream, one CUDA graph per
-    forward incl. the D2D copy of B distinct inputs): inferences/s per batch."""
+    the whole GPU (all 148 SMs: one plain stream, no green context — 8-SM
+    co-scheduled green groups would cover only 120 — one CUDA graph per forward
+    incl. the D2D copy of B distinct inputs): inferences/s per batch."""
     import torch
     from paper_2504_08795_b200 import nets
     from paper_2504_08795_b200.runtime import Executor
-    ex = Executor(1, 1, 148, slots=1, max_tasks=1, max_stages=8)
+    ex = Executor(1, 1, 148, partition="soft", slots=1, max_tasks=1, max_stages=8)
     sm = ex.partitions[0]["sm_count"]
     sp = ex.stream(1, 0)
     s = torch.cuda.ExternalStream(sp)
@@ -249,7 +251,7 @@ def batching_baseline(batches=(1, 2, 4, 8, 16, 32), reps: int = 20) -> dict:
     ex.close()
     best = max(out.items(), key=lambda kv: kv[1]["inf_per_s"])
     return {"per_batch": out, "best_batch": int(best[0]), "best_inf_per_s": best[1]["inf_per_s"],
-            "setup": "resnet50, one 148-SM green partition, one stream, CUDA graph per forward, same kernels"}
+            "setup": f"resnet50, whole GPU ({sm} SMs, one stream), CUDA graph per forward, same kernels"}
 
 
 STALL_RETRIES = 6  # re-measurements of a window that contained a GPU-wide stall

@@ -606,17 +606,23 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = L::kTotal;
   cfg.stream = st;
+  // experiment knob: without PDL a layer's CTAs are not launched early (an early
+  // CTA holds smem/TMEM while it waits for its predecessor)
+  static const bool no_pdl = std::getenv("DARIS_NO_PDL") != nullptr;
   cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 0;
+  if (!no_pdl) {
+    attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+    cfg.numAttrs++;
+  }
   if (pl.cluster > 1) {
-    attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = 1;
-    attr[1].val.clusterDim.y = 1;
-    attr[1].val.clusterDim.z = pl.cluster;
-    cfg.numAttrs = 2;
+    attr[cfg.numAttrs].id = cudaLaunchAttributeClusterDimension;
+    attr[cfg.numAttrs].val.clusterDim.x = 1;
+    attr[cfg.numAttrs].val.clusterDim.y = 1;
+    attr[cfg.numAttrs].val.clusterDim.z = pl.cluster;
+    cfg.numAttrs++;
   }
   return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN>, map, amap, a));
 }

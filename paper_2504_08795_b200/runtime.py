@@ -266,11 +266,17 @@ class DarisRuntime:
         max_stages = 8
         self.exec = Executor(gpu.n_contexts, gpu.n_streams, self.sm_per_ctx, partition=partition, slots=slots,
                              max_tasks=max(t.id for t in self.tasks), max_stages=max_stages, device=device)
-        # SMs the layer planner sizes grids (tiles x split-K) for: the partition by
-        # default; DARIS_PLAN_SMS plans for a smaller share (fewer, longer CTAs:
-        # less fix-up work per job when every SM is shared by several jobs)
+        # SMs the layer planner sizes each job's grids (M/N tiles x split-K) for.
+        # Not the partition: with n_contexts x n_streams jobs in flight every SM
+        # is shared, and a grid sized for the whole partition spends its extra
+        # CTAs on split-K fix-ups that buy isolated latency but cost throughput.
+        # Planning for the device's share per concurrent job (x1.25) measured
+        # +42 % closed-loop capacity at 4x2 OS=2 and ~2x at 16 streams
+        # (tools/capacity_probe.py, profiles/r01_capacity_*). DARIS_PLAN_SMS overrides.
         import os
-        self.sm_budget = int(os.environ.get("DARIS_PLAN_SMS", "0")) or min(p["sm_count"] for p in self.exec.partitions)
+        self.partition_sms = min(p["sm_count"] for p in self.exec.partitions)
+        share = int(round(1.25 * gpu.total_sms / (gpu.n_contexts * gpu.n_streams)))
+        self.sm_budget = int(os.environ.get("DARIS_PLAN_SMS", "0")) or max(8, min(self.partition_sms, share))
         # one weight copy per model, shared by all tasks running it
         self.nets: dict[tuple, nets.Network] = {}
         for t in self.tasks:

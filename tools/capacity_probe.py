@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--shapes", default="1x1_1,1x2_1,1x4_1,1x8_1,1x16_1,2x2_1,4x2_2,4x4_2,8x2_4")
     ap.add_argument("--seconds", type=float, default=1.0)
     ap.add_argument("--model", default="resnet50")
+    ap.add_argument("--partition", default="green", choices=["green", "soft"])
     args = ap.parse_args()
     for shape in args.shapes.split(","):
         a, os_ = shape.split("_")
@@ -37,12 +38,13 @@ def main():
         for t in tasks:
             t.model = args.model
             t.n_stages = None
-        rt = DarisRuntime(tasks, gpu, slots=1, seed=0)
+        rt = DarisRuntime(tasks, gpu, slots=1, seed=0, partition=args.partition)
         rt.capture_all()
         iso = sum(rt.stage_nominal[args.model])
         job = rt.exec.busy_calibrate([rt.net_of(t).n_stages for t in rt.tasks], [t.id for t in rt.tasks],
                                      args.seconds)
         print(json.dumps({"shape": shape, "slots": n, "partition_sms": rt.exec.partitions[0]["sm_count"],
+                          "plan_sms": rt.sm_budget, "partition": args.partition,
                           "isolated_ms": round(iso * 1e3, 4), "loaded_job_ms": round(job * 1e3, 4),
                           "capacity_inf_s": round(n / job, 1), "stretch": round(job / iso, 3)}), flush=True)
         rt.close()
