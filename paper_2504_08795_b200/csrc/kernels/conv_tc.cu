@@ -78,6 +78,7 @@ struct ConvArgs {
   int cluster_split;  // 1: the splits of a tile form one cluster and reduce through DSMEM
   int tma_a;          // 1: activations arrive by TMA (4-D box = th whole output rows of one image)
   int th, tiles_h;    // TMA mode: output rows per M tile, M tiles per image
+  int tma_c;          // 1: the epilogue stages the bf16 tile in smem and stores it with TMA (splits == 1)
   unsigned long long* ts;  // optional per-CTA phase timestamps (globaltimer ns), 16 per CTA
   FDiv d_howo, d_wo, d_kw, d_cinb, d_tiles_h;
 };
@@ -110,9 +111,9 @@ __device__ __forceinline__ float act_apply(float v, int relu) {
 __device__ __forceinline__ uint4 ldg_nc16(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
 
 // 32 accumulator columns of one output row -> scale/bias (smem) + residual
-// (already in registers) -> act -> bf16 NHWC.
-__device__ __forceinline__ void finalize_row32(const ConvArgs& a, int m, int col0, int c_local, const float* v,
-                                               const float* s_scale, const float* s_bias, const uint4* res4) {
+// (already in registers) -> act -> 4 x 16 B of bf16.
+__device__ __forceinline__ void pack_row32(const ConvArgs& a, int c_local, const float* v, const float* s_scale,
+                                           const float* s_bias, const uint4* res4, uint4 (&pk)[4]) {
   float o[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) o[j] = v[j] * s_scale[c_local + j] + s_bias[c_local + j];
@@ -128,22 +129,29 @@ __device__ __forceinline__ void finalize_row32(const ConvArgs& a, int m, int col
       }
     }
   }
-  uint4* yp = reinterpret_cast<uint4*>(a.y + static_cast<size_t>(m) * a.cout + col0);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    uint4 pk;
-    pk.x = pack_bf16x2(act_apply(o[8 * q + 0], a.relu), act_apply(o[8 * q + 1], a.relu));
-    pk.y = pack_bf16x2(act_apply(o[8 * q + 2], a.relu), act_apply(o[8 * q + 3], a.relu));
-    pk.z = pack_bf16x2(act_apply(o[8 * q + 4], a.relu), act_apply(o[8 * q + 5], a.relu));
-    pk.w = pack_bf16x2(act_apply(o[8 * q + 6], a.relu), act_apply(o[8 * q + 7], a.relu));
-    yp[q] = pk;
+    pk[q].x = pack_bf16x2(act_apply(o[8 * q + 0], a.relu), act_apply(o[8 * q + 1], a.relu));
+    pk[q].y = pack_bf16x2(act_apply(o[8 * q + 2], a.relu), act_apply(o[8 * q + 3], a.relu));
+    pk[q].z = pack_bf16x2(act_apply(o[8 * q + 4], a.relu), act_apply(o[8 * q + 5], a.relu));
+    pk[q].w = pack_bf16x2(act_apply(o[8 * q + 6], a.relu), act_apply(o[8 * q + 7], a.relu));
   }
+}
+
+// ... and straight to this row of the NHWC output (one thread per row).
+__device__ __forceinline__ void finalize_row32(const ConvArgs& a, int m, int col0, int c_local, const float* v,
+                                               const float* s_scale, const float* s_bias, const uint4* res4) {
+  uint4 pk[4];
+  pack_row32(a, c_local, v, s_scale, s_bias, res4, pk);
+  uint4* yp = reinterpret_cast<uint4*>(a.y + static_cast<size_t>(m) * a.cout + col0);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) yp[q] = pk[q];
 }
 
 template <int BN>
 __global__ void __maxnreg__(112)
     conv_igemm_tc_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
-                         const ConvArgs a) {
+                         const __grid_constant__ CUtensorMap ymap, const ConvArgs a) {
   using L = SmemLayout<BN>;
   constexpr int kStages = L::kStages;
   constexpr int kLag = L::kLag;
@@ -195,6 +203,7 @@ __global__ void __maxnreg__(112)
     if (lane == 0) {
       tma_prefetch_desc(&wmap);
       if (a.tma_a) tma_prefetch_desc(&amap);
+      if (a.tma_c) tma_prefetch_desc(&ymap);
     }
   }
   tc_fence_before();
@@ -308,6 +317,41 @@ __global__ void __maxnreg__(112)
     }
     if (BN == 64 && a.cluster_split) {
       // (cluster barrier and reduction below, executed by all 192 threads)
+    } else if (a.splits == 1 && a.tma_c) {
+      // Stage the bf16 tile in the (now idle) A/B ring as 64-column halves of
+      // 128 B rows, 128B-swizzled (conflict-free 16 B writes, one row per
+      // thread), then one TMA store per half: coalesced, asynchronous, and
+      // rows past the image / tensor end are clipped by the tensor map.
+      uint8_t* stage = sA;
+      const uint32_t swz = static_cast<uint32_t>(row & 7);
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        uint4 res_nxt[4];
+        if (has_res && c0 + 32 < BN) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) res_nxt[q] = ldg_nc16(res_row + c0 + 32 + 8 * q);
+        }
+        tmem_ld_32x32b_x32(t_row + c0, r);
+        uint4 pk[4];
+        pack_row32(a, c0, reinterpret_cast<const float*>(r), s_scale, s_bias, has_res ? res_cur : nullptr, pk);
+        uint8_t* rowp = stage + (c0 >> 6) * (kBM * 128) + row * 128;
+        const uint32_t chunk0 = static_cast<uint32_t>((c0 & 63) >> 3);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(rowp + (((chunk0 + q) ^ swz) << 4)) = pk[q];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) res_cur[q] = res_nxt[q];
+      }
+      fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the TMA engine
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (threadIdx.x == 0) {
+        const int c1 = a.tma_a ? h0 * a.wo : m0;
+        const int c2 = a.tma_a ? img : 0;
+#pragma unroll
+        for (int h = 0; h < BN / 64; ++h) tma_store_3d(&ymap, stage + h * (kBM * 128), n0 + h * 64, c1, c2);
+        bulk_commit();
+        bulk_wait_read();
+      }
     } else if (a.splits == 1) {
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -568,6 +612,26 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
     if (r != CUDA_SUCCESS) return DARIS_K_BAD_ARG;
   }
 
+  // epilogue by TMA store (splits == 1): the output as a 3-D tensor {cout, rows, images}
+  // whose box is one M tile (th whole output rows of one image, or 128 flat rows)
+  static const bool no_tma_c = std::getenv("DARIS_NO_TMA_STORE") != nullptr;  // experiment knob
+  const bool tma_c = !no_tma_c && pl.splits == 1;
+  CUtensorMap ymap;
+  std::memset(&ymap, 0, sizeof(ymap));
+  if (tma_c) {
+    const bool per_image = pl.tma_rows > 0;
+    const cuuint64_t rows = per_image ? static_cast<cuuint64_t>(d->ho) * d->wo
+                                      : static_cast<cuuint64_t>(d->n) * d->ho * d->wo;
+    cuuint64_t ydims[3] = {static_cast<cuuint64_t>(d->cout), rows, per_image ? static_cast<cuuint64_t>(d->n) : 1};
+    cuuint64_t ystr[2] = {static_cast<cuuint64_t>(d->cout) * 2, rows * d->cout * 2};
+    cuuint32_t ybox[3] = {64, static_cast<cuuint32_t>(per_image ? pl.tma_rows * d->wo : kBM), 1};
+    cuuint32_t yestr[3] = {1, 1, 1};
+    r = encode(&ymap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, d->y, ydims, ystr, ybox, yestr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return DARIS_K_BAD_ARG;
+  }
+
   static bool attr_set = false;  // per template instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(conv_igemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -597,6 +661,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   a.splits = pl.splits;
   a.cluster_split = pl.cluster > 1 ? 1 : 0;
   a.tma_a = pl.tma_rows > 0 ? 1 : 0;
+  a.tma_c = tma_c ? 1 : 0;
   a.th = pl.tma_rows > 0 ? pl.tma_rows : 1;
   a.tiles_h = (d->ho + a.th - 1) / a.th;
   a.d_tiles_h = make_fdiv(a.tiles_h);
@@ -624,7 +689,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
     attr[cfg.numAttrs].val.clusterDim.z = pl.cluster;
     cfg.numAttrs++;
   }
-  return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN>, map, amap, a));
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN>, map, amap, ymap, a));
 }
 
 }  // namespace daris

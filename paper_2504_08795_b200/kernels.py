@@ -73,6 +73,7 @@ def lib() -> C.CDLL:
         L.daris_maxpool.argtypes = [vp, vp] + [i32] * 9 + [vp]
         L.daris_avgpool.argtypes = [vp, vp, i32, i32, i32, vp]
         L.daris_linear.argtypes = [vp, i32, vp, vp, vp, i32, i32, i32, i32, i32, vp]
+        L.daris_pool_linear.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp]
         L.daris_dwconv.argtypes = [vp, vp, vp, vp, vp] + [i32] * 10 + [vp]
         L.daris_device_sms.argtypes = []
         P = C.POINTER
@@ -86,7 +87,8 @@ def lib() -> C.CDLL:
         L.daris_stage_destroy.argtypes = [vp]
         L.daris_stage_destroy.restype = None
         for name in ("daris_conv_plan", "daris_conv2d", "daris_stem_im2col", "daris_pack_nhwc",
-                     "daris_maxpool", "daris_avgpool", "daris_linear", "daris_dwconv", "daris_device_sms",
+                     "daris_maxpool", "daris_avgpool", "daris_linear", "daris_pool_linear", "daris_dwconv",
+                     "daris_device_sms",
                      "daris_stage_create", "daris_stage_launch", "daris_stage_info", "daris_stage_layer_units",
                      "daris_stage_plan_conv"):
             getattr(L, name).restype = C.c_int
@@ -207,6 +209,18 @@ def linear(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None, *, 
         out = torch.empty((b, o), dtype=torch.bfloat16 if out_bf16 else torch.float32, device=x.device)
     _check(lib().daris_linear(_ptr(x), int(x.dtype == torch.bfloat16), _ptr(weight), _ptr(bias), _ptr(out),
                               int(out.dtype == torch.bfloat16), b, k, o, relu, _stream(stream)), "daris_linear")
+    return out
+
+
+def pool_linear(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None, *,
+                out: torch.Tensor | None = None, grid: int = 0, stream=None) -> torch.Tensor:
+    """mean over the pixels of NHWC bf16 x (batch <= 4), then fp32 x . weight^T + bias."""
+    n, h, w, c = x.shape
+    o = weight.shape[0]
+    if out is None:
+        out = torch.empty((n, o), dtype=torch.float32, device=x.device)
+    _check(lib().daris_pool_linear(_ptr(x), _ptr(weight), _ptr(bias), _ptr(out), n, h * w, c, o, grid,
+                                   _stream(stream)), "daris_pool_linear")
     return out
 
 

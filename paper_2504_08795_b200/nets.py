@@ -234,6 +234,21 @@ class _Builder:
         return dst, out_shape
 
 
+def _pool_classifier(b: "_Builder", lin: LinearLayer, x: str, shape, batch: int) -> None:
+    """Global average pool + the final linear layer: one fused launch for small
+    batches (daris_pool_linear), avgpool then linear otherwise."""
+    feat = shape[3]
+    b.need("pooled", batch * feat)          # the two-launch form (and the persistent stage kernel) use it
+    b.need("logits", batch * lin.weight.shape[0])
+    out_shape = (batch, lin.weight.shape[0])
+    if batch <= 4:
+        b.ops.append(Op("pool_linear", lin, x, "logits", None, shape, out_shape, lin.flops_per_image * batch))
+    else:
+        b.ops.append(Op("avgpool", None, x, "pooled", None, shape, (batch, feat)))
+        b.ops.append(Op("linear", lin, "pooled", "logits", None, (batch, feat), out_shape,
+                        lin.flops_per_image * batch))
+
+
 def _resnet_ops(model, name, batch, device, split) -> Network:
     b = _Builder(batch)
     stem = _stem_layer("conv1", model.conv1, model.bn1, 1, device, 112 * 112)
@@ -283,13 +298,9 @@ def _resnet_ops(model, name, batch, device, split) -> Network:
         x, shape, hw = out, s3, hw_out
     fc = model.fc
     feat = shape[3]
-    b.need("pooled", batch * feat)
-    b.ops.append(Op("avgpool", None, x, "pooled", None, shape, (batch, feat)))
     lin = LinearLayer("fc", fc.weight.detach().to(device=device, dtype=torch.bfloat16).contiguous(),
                       fc.bias.detach().float().to(device), 0, False, 2 * fc.in_features * fc.out_features)
-    b.need("logits", batch * fc.out_features)
-    b.ops.append(Op("linear", lin, "pooled", "logits", None, (batch, feat), (batch, fc.out_features),
-                    lin.flops_per_image * batch))
+    _pool_classifier(b, lin, x, shape, batch)
     b.stage_break()
     flops = sum(op.flops for op in b.ops) // batch
     return Network(name, batch, device, b.ops, b.stage_bounds, b.sizes, (batch, 3, 224, 224),
@@ -409,14 +420,10 @@ def _mbv2_ops(model, batch, device, n_stages) -> Network:
     nx, shape = b.conv(L, x, shape)
     b.give(x)
     x = nx
-    b.need("pooled", batch * shape[3])
-    b.ops.append(Op("avgpool", None, x, "pooled", None, shape, (batch, shape[3])))
     fc = [m for m in model.classifier if isinstance(m, nn.Linear)][0]
     lin = LinearLayer("classifier", fc.weight.detach().to(device=device, dtype=torch.bfloat16).contiguous(),
                       fc.bias.detach().float().to(device), 0, False, 2 * fc.in_features * fc.out_features)
-    b.need("logits", batch * fc.out_features)
-    b.ops.append(Op("linear", lin, "pooled", "logits", None, (batch, shape[3]), (batch, fc.out_features),
-                    lin.flops_per_image * batch))
+    _pool_classifier(b, lin, x, shape, batch)
     b.stage_break()
     flops = sum(op.flops for op in b.ops) // batch
     return Network("mobilenet_v2", batch, device, b.ops, b.stage_bounds, b.sizes, (batch, 3, 224, 224),
@@ -513,6 +520,10 @@ def run_op(op: Op, tb: TaskBuffers, stream, sm_budget: int = 0) -> None:
         if L.out_bf16 and out.dtype != torch.bfloat16:
             raise RuntimeError("bf16 linear output needs a bf16 buffer")
         K.linear(x, L.weight, L.bias, relu=L.relu, out=out, stream=stream)
+    elif op.kind == "pool_linear":
+        L = op.layer
+        K.pool_linear(_view(B[op.src], op.shape_in), L.weight, L.bias, out=_view(B[op.dst], op.shape_out),
+                      grid=sm_budget if sm_budget > 0 else 32, stream=stream)
     elif op.kind == "dwconv":
         L = op.layer
         K.dwconv(_view(B[op.src], op.shape_in), L.weight, L.scale, L.bias, stride=L.stride, pad=L.pad, relu=L.relu,
@@ -564,6 +575,12 @@ def stage_ops(net: Network, stage: int, tb: TaskBuffers) -> list:
             flags = (1 if src.dtype == torch.bfloat16 else 0) | (2 if L.out_bf16 else 0)
             out.append(K.stage_op(K.OP_LINEAR, src, dst, weight=L.weight, bias=L.bias, n=n, c=k,
                                   cout=op.shape_out[1], relu=L.relu, flags=flags))
+        elif op.kind == "pool_linear":  # the stage kernel runs it as avgpool + linear through "pooled"
+            L = op.layer
+            n, h, w, c = op.shape_in
+            out.append(K.stage_op(K.OP_AVGPOOL, B[op.src], B["pooled"], n=n, h=h, w=w, c=c))
+            out.append(K.stage_op(K.OP_LINEAR, B["pooled"], B[op.dst], weight=L.weight, bias=L.bias, n=n, c=c,
+                                  cout=op.shape_out[1], relu=L.relu, flags=0))
         elif op.kind == "dwconv":
             L = op.layer
             n, h, w, c = op.shape_in

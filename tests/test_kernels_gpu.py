@@ -196,3 +196,19 @@ def test_stem_pixel_chunk_mode_matches_conv(k, stride, pad, hw):
     out = K.conv2d(packed, w8.bfloat16().to(dev), scale.to(dev), bias.to(dev), stride=stride, pad=pad)
     torch.cuda.synchronize()
     _close(out, ref)
+
+
+@pytest.mark.parametrize("batch,hw,k,o,grid", [(1, 49, 2048, 1000, 23), (1, 49, 1280, 1000, 0), (4, 49, 2048, 1000, 7),
+                                               (3, 16, 512, 10, 1)])
+def test_pool_linear_fused(batch, hw, k, o, grid):
+    """daris_pool_linear = global average pool + fp32 linear in one launch."""
+    from paper_2504_08795_b200 import kernels as K
+    dev = torch.device("cuda")
+    g = torch.Generator().manual_seed(9)
+    side = int(hw ** 0.5)
+    x = torch.randn(batch, side, side, k, generator=g).bfloat16()
+    w = (torch.randn(o, k, generator=g) / k ** 0.5).bfloat16()
+    bias = torch.randn(o, generator=g)
+    y = K.pool_linear(x.to(dev), w.to(dev), bias.to(dev), grid=grid)
+    torch.cuda.synchronize()
+    _close(y, x.float().mean(dim=(1, 2)) @ w.float().t() + bias)
