@@ -58,7 +58,14 @@ typedef struct daris_conv_desc {
   void* timestamps;       /* optional: 16 uint64 globaltimer stamps per CTA (profiling), or NULL */
 } daris_conv_desc;
 
-enum { DARIS_CONV_CLUSTER_SPLITK = 1 };
+enum {
+  DARIS_CONV_CLUSTER_SPLITK = 1,
+  /* 8-channel stems by TMA: x is stored zero-bordered as [n][h + 2*pad][w + 2*pad + 8][8]
+   * and weight is [cout][kh][8][8] (the kw kernel columns padded to 8 pixel slots with
+   * zeros): one K block = one kernel row, whose A tile is a single TMA box of
+   * overlapping 128-B windows (requires cin == 8, kw <= 8, wo <= 128) */
+  DARIS_CONV_PADDED_INPUT = 2
+};
 
 typedef struct daris_conv_plan_t {
   int32_t block_n, splits, kb_per_split, tiles_m, tiles_n;
@@ -79,6 +86,11 @@ int daris_stem_im2col(const float* x, void* out, int32_t n, int32_t c, int32_t h
                       int32_t kw, int32_t stride, int32_t pad, int32_t ho, int32_t wo, int32_t kpad, void* stream);
 
 /* NCHW fp32 -> NHWC bf16 with channels zero-padded to cpad (multiple of 8). */
+/* NCHW fp32 -> NHWC bf16 (cpad channels) into the interior of a zero-bordered
+ * [n][h + 2*border][w + 2*border + extra][cpad] buffer; the borders are never
+ * written (allocate the buffer zeroed). Feeds DARIS_CONV_PADDED_INPUT stems. */
+int daris_pack_nhwc_bordered(const float* x, void* out, int32_t n, int32_t c, int32_t h, int32_t w, int32_t cpad,
+                             int32_t border, int32_t extra, void* stream);
 int daris_pack_nhwc(const float* x, void* out, int32_t n, int32_t c, int32_t h, int32_t w, int32_t cpad,
                     void* stream);
 

@@ -181,9 +181,12 @@ int build_partitions(daris_exec* ex) {
     }
     int prio_low = 0, prio_high = 0;
     cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
-    // HP stages on higher-priority streams is opt-in: measured on the C2 knee it
-    // starves LP stages of CTA slots (LP misses bind first) for no HP gain
-    if (!std::getenv("DARIS_HP_STREAM_PRIORITY")) prio_high = prio_low;
+    // HP stages run on the highest-priority streams (their CTAs are scheduled first
+    // when SMs free up). With grids planned for the per-job share this lifts the C2
+    // knee (A/B on one box: 12.2k vs 11.5k inf/s, profiles/r01_bench_hpprio*.json);
+    // with partition-sized grids it starved LP stages. DARIS_HP_STREAM_PRIORITY=0: off.
+    const char* hp_env = std::getenv("DARIS_HP_STREAM_PRIORITY");
+    if (hp_env && std::atoi(hp_env) == 0) prio_high = prio_low;
     const int n_streams = 2 * c.n_streams + 1;  // low + high priority per slot, + capture stream
     for (int s = 0; s < n_streams; ++s) {
       const int prio = (s >= c.n_streams && s < 2 * c.n_streams) ? prio_high : prio_low;

@@ -52,7 +52,7 @@ __global__ void stem_im2col_kernel(const float* __restrict__ x, __nv_bfloat16* _
 }
 
 __global__ void pack_nhwc_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ out, int n, int c, int h,
-                                 int w, int cpad) {
+                                 int w, int cpad, int border, int extra) {
   pdl_wait();
   pdl_trigger();
   const int chunks = cpad / 8;
@@ -74,7 +74,14 @@ __global__ void pack_nhwc_kernel(const float* __restrict__ x, __nv_bfloat16* __r
   pk.y = pack_bf16x2(v[2], v[3]);
   pk.z = pack_bf16x2(v[4], v[5]);
   pk.w = pack_bf16x2(v[6], v[7]);
-  reinterpret_cast<uint4*>(out)[idx] = pk;
+  if (border == 0 && extra == 0) {
+    reinterpret_cast<uint4*>(out)[idx] = pk;
+  } else {  // interior of a zero-bordered [n][h + 2b][w + 2b + extra][cpad] buffer (borders stay zero)
+    const int y = static_cast<int>(hw / w), xx = static_cast<int>(hw - static_cast<long long>(y) * w);
+    const long long hp = h + 2 * border, wp = w + 2 * border + extra;
+    const long long o = ((static_cast<long long>(img) * hp + y + border) * wp + xx + border) * chunks + ch;
+    reinterpret_cast<uint4*>(out)[o] = pk;
+  }
 }
 
 // one thread per (output pixel, 8 channels)
@@ -367,8 +374,19 @@ extern "C" int daris_pack_nhwc(const float* x, void* out, int32_t n, int32_t c, 
   if (cpad % 8 != 0 || cpad < c) return DARIS_K_BAD_SHAPE;
   const long long work = static_cast<long long>(n) * h * w * (cpad / 8);
   cudaError_t return_code = launch_pdl(pack_nhwc_kernel, dim3(grid_for(work, 256)), dim3(256), 0, static_cast<cudaStream_t>(stream),
-      x, static_cast<__nv_bfloat16*>(out), n, c, h, w, cpad);
+      x, static_cast<__nv_bfloat16*>(out), n, c, h, w, cpad, 0, 0);
   return static_cast<int>(return_code);
+}
+
+extern "C" int daris_pack_nhwc_bordered(const float* x, void* out, int32_t n, int32_t c, int32_t h, int32_t w,
+                                        int32_t cpad, int32_t border, int32_t extra, void* stream) {
+  if (!x || !out) return DARIS_K_BAD_ARG;
+  if (cpad % 8 != 0 || cpad < c || border < 0 || extra < 0) return DARIS_K_BAD_SHAPE;
+  const long long work = static_cast<long long>(n) * h * w * (cpad / 8);
+  cudaError_t rc = launch_pdl(pack_nhwc_kernel, dim3(grid_for(work, 256)), dim3(256), 0,
+                              static_cast<cudaStream_t>(stream), x, static_cast<__nv_bfloat16*>(out), n, c, h, w,
+                              cpad, border, extra);
+  return static_cast<int>(rc);
 }
 
 extern "C" int daris_maxpool(const void* x, void* y, int32_t n, int32_t h, int32_t w, int32_t c, int32_t k,

@@ -79,6 +79,7 @@ struct ConvArgs {
   int tma_a;          // 1: activations arrive by TMA (4-D box = th whole output rows of one image)
   int th, tiles_h;    // TMA mode: output rows per M tile, M tiles per image
   int tma_c;          // 1: the epilogue stages the bf16 tile in smem and stores it with TMA (splits == 1)
+  int stem_tma;       // 1: 8-channel stem from a zero-bordered input, one TMA window box per kernel row
   unsigned long long* ts;  // optional per-CTA phase timestamps (globaltimer ns), 16 per CTA
   FDiv d_howo, d_wo, d_kw, d_cinb, d_tiles_h;
 };
@@ -434,6 +435,10 @@ __global__ void __maxnreg__(112)
       const uint32_t a_bytes = static_cast<uint32_t>(a.th * a.wo * 128);
       auto load_a = [&](int i, int s) {
         const int kb = kb_begin + i;
+        if (a.stem_tma) {  // K block = kernel row kb: windows of th output rows at padded input row h0*s + kb
+          tma_load_4d(&amap, &full[s], sA + s * L::kABytes, 0, 0, h0 * a.stride + kb, img);
+          return;
+        }
         const int kpos = fdiv(kb, a.d_cinb);
         const int cb = kb - kpos * a.cin_blocks;
         const int r_ = fdiv(kpos, a.d_kw), s_ = kpos - r_ * a.kw;
@@ -583,7 +588,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   using L = SmemLayout<BN>;
   auto encode = get_encode_fn();
   if (!encode) return DARIS_K_NO_DRIVER;
-  const int K = d->kh * d->kw * d->cin;
+  const int K = (d->flags & DARIS_CONV_PADDED_INPUT) ? d->kh * 64 : d->kh * d->kw * d->cin;
   CUtensorMap map;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(d->cout)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(K) * 2};
@@ -595,7 +600,23 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   if (r != CUDA_SUCCESS) return DARIS_K_BAD_ARG;
   CUtensorMap amap;
   std::memset(&amap, 0, sizeof(amap));
-  if (pl.tma_rows > 0) {
+  const bool stem_tma = pl.tma_rows > 0 && d->cin == 8;
+  if (stem_tma) {
+    // zero-bordered NHWC8 input [n][hp][wp][8]: dim0 = the 64-element (128 B) window of
+    // kw pixels x 8 channels starting at padded column ow*stride, dim1 = output column
+    // (windows overlap: global stride stride*16 B), dim2 = padded input row, dim3 = image
+    const int th = pl.tma_rows;
+    const cuuint64_t hp = static_cast<cuuint64_t>(d->h) + 2 * d->pad;
+    const cuuint64_t wp = static_cast<cuuint64_t>(d->w) + 2 * d->pad + 8;
+    cuuint64_t adims[4] = {64, static_cast<cuuint64_t>(d->wo), hp, static_cast<cuuint64_t>(d->n)};
+    cuuint64_t astr[3] = {static_cast<cuuint64_t>(d->stride) * 16, wp * 16, hp * wp * 16};
+    cuuint32_t abox[4] = {64, static_cast<cuuint32_t>(d->wo), static_cast<cuuint32_t>(th * d->stride), 1};
+    cuuint32_t aestr[4] = {1, 1, static_cast<cuuint32_t>(d->stride), 1};
+    r = encode(&amap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(d->x), adims, astr, abox, aestr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return DARIS_K_BAD_ARG;
+  } else if (pl.tma_rows > 0) {
     // activations NHWC as a 4-D tensor (c, w, h, n); one box = th output rows x wo
     // output columns x 64 channels, traversed with the conv stride
     const int th = pl.tma_rows;
@@ -656,12 +677,13 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   a.d_wo = make_fdiv(d->wo);
   a.d_kw = make_fdiv(d->kw);
   a.d_cinb = make_fdiv(a.cin_blocks > 0 ? a.cin_blocks : 1);
-  a.num_kb = d->cin == 8 ? (d->kh * d->kw + 7) / 8 : d->kh * d->kw * a.cin_blocks;
+  a.num_kb = stem_tma ? d->kh : d->cin == 8 ? (d->kh * d->kw + 7) / 8 : d->kh * d->kw * a.cin_blocks;
   a.kb_per_split = pl.kb_per_split;
   a.splits = pl.splits;
   a.cluster_split = pl.cluster > 1 ? 1 : 0;
   a.tma_a = pl.tma_rows > 0 ? 1 : 0;
   a.tma_c = tma_c ? 1 : 0;
+  a.stem_tma = stem_tma ? 1 : 0;
   a.th = pl.tma_rows > 0 ? pl.tma_rows : 1;
   a.tiles_h = (d->ho + a.th - 1) / a.th;
   a.d_tiles_h = make_fdiv(a.tiles_h);
@@ -712,14 +734,16 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
       d->kh < 1 || d->kw < 1 || d->stride < 1)
     return DARIS_K_BAD_SHAPE;
   const int M = d->n * d->ho * d->wo;
-  const int num_kb = d->cin == 8 ? (d->kh * d->kw + 7) / 8 : d->kh * d->kw * (d->cin / kBK);
+  const bool padded = (d->flags & DARIS_CONV_PADDED_INPUT) != 0;
+  if (padded && (d->cin != 8 || d->kw > 8 || d->wo > kBM)) return DARIS_K_BAD_SHAPE;
+  const int num_kb = padded ? d->kh : d->cin == 8 ? (d->kh * d->kw + 7) / 8 : d->kh * d->kw * (d->cin / kBK);
   const int budget = d->sm_budget > 0 ? d->sm_budget : daris_device_sms();
   // Activations by TMA (4-D box of th whole output rows) unless the layer is a
   // stem (8 channels: pixel-chunk gather) or a box side would exceed 256.
   static const bool tma_off = std::getenv("DARIS_CONV_GATHER") != nullptr;  // experiment knob
   const int th = std::max(1, std::min(d->ho, kBM / d->wo));
-  const bool tma_a = !tma_off && d->cin % kBK == 0 && d->wo * d->stride <= 256 && th * d->stride <= 256 &&
-                     d->wo <= kBM;
+  const bool tma_a = padded || (!tma_off && d->cin % kBK == 0 && d->wo * d->stride <= 256 &&
+                                 th * d->stride <= 256 && d->wo <= kBM);
   const int tiles_h = (d->ho + th - 1) / th;
   const int tiles_m = tma_a ? d->n * tiles_h : (M + kBM - 1) / kBM;
   int bn = d->block_n;

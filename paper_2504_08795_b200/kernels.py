@@ -70,6 +70,7 @@ def lib() -> C.CDLL:
         L.daris_conv2d.argtypes = [C.POINTER(ConvDesc), vp]
         L.daris_stem_im2col.argtypes = [vp, vp] + [i32] * 11 + [vp]
         L.daris_pack_nhwc.argtypes = [vp, vp] + [i32] * 5 + [vp]
+        L.daris_pack_nhwc_bordered.argtypes = [vp, vp] + [i32] * 7 + [vp]
         L.daris_maxpool.argtypes = [vp, vp] + [i32] * 9 + [vp]
         L.daris_avgpool.argtypes = [vp, vp, i32, i32, i32, vp]
         L.daris_linear.argtypes = [vp, i32, vp, vp, vp, i32, i32, i32, i32, i32, vp]
@@ -88,6 +89,7 @@ def lib() -> C.CDLL:
         L.daris_stage_destroy.restype = None
         for name in ("daris_conv_plan", "daris_conv2d", "daris_stem_im2col", "daris_pack_nhwc",
                      "daris_maxpool", "daris_avgpool", "daris_linear", "daris_pool_linear", "daris_dwconv",
+                     "daris_pack_nhwc_bordered",
                      "daris_device_sms",
                      "daris_stage_create", "daris_stage_launch", "daris_stage_info", "daris_stage_layer_units",
                      "daris_stage_plan_conv"):
@@ -117,7 +119,7 @@ CLUSTER_SPLITK = True
 
 
 def conv_desc(x_shape, cout, kh, kw, stride, pad, *, relu=1, block_n=0, splits=0, sm_budget=0,
-              cluster: bool | None = None) -> ConvDesc:
+              cluster: bool | None = None, padded_input: bool = False) -> ConvDesc:
     n, h, w, cin = x_shape
     ho = (h + 2 * pad - kh) // stride + 1
     wo = (w + 2 * pad - kw) // stride + 1
@@ -125,7 +127,7 @@ def conv_desc(x_shape, cout, kh, kw, stride, pad, *, relu=1, block_n=0, splits=0
     d.n, d.h, d.w, d.cin, d.cout = n, h, w, cin, cout
     d.kh, d.kw, d.stride, d.pad, d.ho, d.wo = kh, kw, stride, pad, ho, wo
     d.relu, d.block_n, d.splits, d.sm_budget = relu, block_n, splits, sm_budget
-    d.flags = 1 if (CLUSTER_SPLITK if cluster is None else cluster) else 0
+    d.flags = (1 if (CLUSTER_SPLITK if cluster is None else cluster) else 0) | (2 if padded_input else 0)
     return d
 
 
@@ -140,11 +142,15 @@ def conv2d(x: torch.Tensor, weight: torch.Tensor, scale: torch.Tensor, bias: tor
            out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
            counters: torch.Tensor | None = None, block_n: int = 0, splits: int = 0,
            sm_budget: int = 0, stream=None, timestamps: torch.Tensor | None = None,
-           cluster: bool | None = None) -> torch.Tensor:
-    """x: [n,h,w,cin] bf16 NHWC; weight: [cout,kh,kw,cin] bf16."""
-    cout, kh, kw, cin = weight.shape
+           cluster: bool | None = None, padded_input: bool = False, kw: int | None = None) -> torch.Tensor:
+    """x: [n,h,w,cin] bf16 NHWC; weight: [cout,kh,kw,cin] bf16.
+    padded_input (8-channel stems): x's storage is zero-bordered
+    [n][h+2pad][w+2pad+8][8] (pack_nhwc(border=pad, extra=8)), weight is
+    [cout,kh,8,8] and `kw` gives the real kernel width."""
+    cout, kh, kw_w, cin = weight.shape
+    kw = kw if (padded_input and kw is not None) else kw_w
     d = conv_desc(tuple(x.shape), cout, kh, kw, stride, pad, relu=relu, block_n=block_n,
-                  splits=splits, sm_budget=sm_budget, cluster=cluster)
+                  splits=splits, sm_budget=sm_budget, cluster=cluster, padded_input=padded_input)
     p = conv_plan(d)
     if out is None:
         out = torch.empty((d.n, d.ho, d.wo, cout), dtype=torch.bfloat16, device=x.device)
@@ -173,11 +179,18 @@ def stem_im2col(x: torch.Tensor, kh: int, kw: int, stride: int, pad: int, kpad: 
     return out
 
 
-def pack_nhwc(x: torch.Tensor, cpad: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+def pack_nhwc(x: torch.Tensor, cpad: int, out: torch.Tensor | None = None, stream=None, *, border: int = 0,
+              extra: int = 0) -> torch.Tensor:
+    """NCHW fp32 -> NHWC bf16 with cpad channels; with border/extra into the
+    interior of a zero-bordered [n][h+2b][w+2b+extra][cpad] buffer."""
     n, c, h, w = x.shape
     if out is None:
-        out = torch.empty((n, h, w, cpad), dtype=torch.bfloat16, device=x.device)
-    _check(lib().daris_pack_nhwc(_ptr(x), _ptr(out), n, c, h, w, cpad, _stream(stream)), "daris_pack_nhwc")
+        out = torch.zeros((n, h + 2 * border, w + 2 * border + extra, cpad), dtype=torch.bfloat16, device=x.device)
+    if border == 0 and extra == 0:
+        _check(lib().daris_pack_nhwc(_ptr(x), _ptr(out), n, c, h, w, cpad, _stream(stream)), "daris_pack_nhwc")
+    else:
+        _check(lib().daris_pack_nhwc_bordered(_ptr(x), _ptr(out), n, c, h, w, cpad, border, extra,
+                                              _stream(stream)), "daris_pack_nhwc_bordered")
     return out
 
 

@@ -85,6 +85,7 @@ class ConvLayer:
     cout: int                     # padded
     relu: int
     flops_per_image: int          # 2*MAC of the unpadded layer at 224x224 input
+    padded_input: bool = False    # 8-channel stem read by TMA from a zero-bordered input (DARIS_CONV_PADDED_INPUT)
 
 
 @dataclass
@@ -127,21 +128,44 @@ def _conv_layer(name, conv, bn, relu, device, hw_out, cin_pad=None) -> ConvLayer
                      bi.to(device), kh, kw, conv.stride[0], conv.padding[0], cin_p, cout_p, relu, flops)
 
 
-def _stem_layer(name, conv, bn, relu, device, hw_out) -> ConvLayer:
-    """kxk stem over 3 input channels: input packed to NHWC with 8 channels (3 real),
-    weights [cout][kh][kw][8]; the conv kernel's pixel-chunk mode gathers one kernel
-    position (8 channels = 16 B) per chunk, so no im2col pass is needed."""
+def _stem_layer(name, conv, bn, relu, device, hw_out, padded: bool = False) -> ConvLayer:
+    """kxk stem over 3 input channels: input packed to NHWC with 8 channels (3 real).
+    padded=False: weights [cout][kh][kw][8]; the conv kernel's pixel-chunk mode
+    gathers one kernel position (8 channels = 16 B) per chunk.
+    padded=True: the input is packed zero-bordered and weights are [cout][kh][8][8]
+    (kw padded to 8 pixel slots): one K block per kernel row, loaded as one TMA box
+    of overlapping 128-B windows (no gather, no im2col)."""
     w, scale, bias = fold_bn(conv, bn)
     cout, cin, kh, kw = w.shape
     cout_p = _pad64(cout)
-    wt = torch.zeros(cout_p, kh, kw, 8)
-    wt[:cout, :, :, :cin] = w.permute(0, 2, 3, 1)
+    wt = torch.zeros(cout_p, kh, 8 if padded else kw, 8)
+    wt[:cout, :, :kw, :cin] = w.permute(0, 2, 3, 1)
     sc = torch.zeros(cout_p)
     bi = torch.zeros(cout_p)
     sc[:cout] = scale
     bi[:cout] = bias
     return ConvLayer(name, wt.to(device=device, dtype=torch.bfloat16).contiguous(), sc.to(device), bi.to(device),
-                     kh, kw, conv.stride[0], conv.padding[0], 8, cout_p, relu, 2 * cout * cin * kh * kw * hw_out)
+                     kh, kw, conv.stride[0], conv.padding[0], 8, cout_p, relu, 2 * cout * cin * kh * kw * hw_out,
+                     padded)
+
+
+def _stem(b: "_Builder", name, conv, bn, relu, device, batch: int):
+    """pack8 + the stem conv; the TMA-window form when the shape allows it (and
+    the network is not run by the persistent stage kernel, which gathers)."""
+    kh, kw = conv.kernel_size
+    st, pd = conv.stride[0], conv.padding[0]
+    wo = (224 + 2 * pd - kw) // st + 1
+    padded = STAGE_MODE != "persistent" and kw <= 8 and wo <= 128
+    layer = _stem_layer(name, conv, bn, relu, device, wo * wo, padded)
+    b.need("input", batch * 3 * 224 * 224)
+    if padded:
+        hp, wp = 224 + 2 * pd, 224 + 2 * pd + 8
+        b.need("packed", batch * hp * wp * 8)
+        b.ops.append(Op("pack8", (pd, 8), "input", "packed", None, (batch, 3, 224, 224), (batch, hp, wp, 8)))
+    else:
+        b.need("packed", batch * 224 * 224 * 8)
+        b.ops.append(Op("pack8", None, "input", "packed", None, (batch, 3, 224, 224), (batch, 224, 224, 8)))
+    return b.conv(layer, "packed", (batch, 224, 224, 8))
 
 
 @dataclass
@@ -251,11 +275,7 @@ def _pool_classifier(b: "_Builder", lin: LinearLayer, x: str, shape, batch: int)
 
 def _resnet_ops(model, name, batch, device, split) -> Network:
     b = _Builder(batch)
-    stem = _stem_layer("conv1", model.conv1, model.bn1, 1, device, 112 * 112)
-    b.need("input", batch * 3 * 224 * 224)
-    b.need("packed", batch * 224 * 224 * 8)
-    b.ops.append(Op("pack8", None, "input", "packed", None, (batch, 3, 224, 224), (batch, 224, 224, 8)))
-    x, shape = b.conv(stem, "packed", (batch, 224, 224, 8))
+    x, shape = _stem(b, "conv1", model.conv1, model.bn1, 1, device, batch)
     y = b.take(avoid=(x,))
     b.need(y, batch * 56 * 56 * 64)
     b.ops.append(Op("maxpool", None, x, y, None, shape, (batch, 56, 56, shape[3])))
@@ -365,10 +385,7 @@ def _mbv2_ops(model, batch, device, n_stages) -> Network:
     feats = list(model.features)
     b.need("input", batch * 3 * 224 * 224)
     first = feats[0]
-    stem = _stem_layer("features.0", first[0], first[1], 6, device, 112 * 112)
-    b.need("packed", batch * 224 * 224 * 8)
-    b.ops.append(Op("pack8", None, "input", "packed", None, (batch, 3, 224, 224), (batch, 224, 224, 8)))
-    x, shape = b.conv(stem, "packed", (batch, 224, 224, 8))
+    x, shape = _stem(b, "features.0", first[0], first[1], 6, device, batch)
     blocks = feats[1:-1]
     # split the inverted-residual sequence into n_stages groups of roughly equal count
     per = max(1, (len(blocks) + n_stages - 1) // n_stages) if n_stages > 1 else len(blocks) + 1
@@ -481,7 +498,8 @@ def allocate_buffers(net: Network, sm_budget: int = 0) -> TaskBuffers:
     for op in net.ops:
         if op.kind == "conv":
             L = op.layer
-            d = K.conv_desc(op.shape_in, L.cout, L.kh, L.kw, L.stride, L.pad, relu=L.relu, sm_budget=sm_budget)
+            d = K.conv_desc(op.shape_in, L.cout, L.kh, L.kw, L.stride, L.pad, relu=L.relu, sm_budget=sm_budget,
+                            padded_input=L.padded_input)
             p = K.conv_plan(d)
             ws = max(ws, p.workspace_floats)
             ctr = max(ctr, p.counters)
@@ -499,13 +517,16 @@ def _view(t: torch.Tensor, shape) -> torch.Tensor:
 def run_op(op: Op, tb: TaskBuffers, stream, sm_budget: int = 0) -> None:
     B = tb.bufs
     if op.kind == "pack8":
-        K.pack_nhwc(B["input"], 8, out=_view(B["packed"], op.shape_out), stream=stream)
+        border, extra = op.layer if op.layer else (0, 0)
+        K.pack_nhwc(B["input"], 8, out=_view(B["packed"], op.shape_out), border=border, extra=extra,
+                    stream=stream)
     elif op.kind == "conv":
         L = op.layer
         res = _view(B[op.res], op.shape_out) if op.res else None
         K.conv2d(_view(B[op.src], op.shape_in), L.weight, L.scale, L.bias, stride=L.stride, pad=L.pad,
                  relu=L.relu, residual=res, out=_view(B[op.dst], op.shape_out), workspace=tb.workspace,
-                 counters=tb.counters, sm_budget=sm_budget, stream=stream)
+                 counters=tb.counters, sm_budget=sm_budget, stream=stream, padded_input=L.padded_input,
+                 kw=L.kw)
     elif op.kind == "maxpool":
         K.maxpool(_view(B[op.src], op.shape_in), 3, 2, 1, out=_view(B[op.dst], op.shape_out), stream=stream)
     elif op.kind == "maxpool2":

@@ -212,3 +212,30 @@ def test_pool_linear_fused(batch, hw, k, o, grid):
     y = K.pool_linear(x.to(dev), w.to(dev), bias.to(dev), grid=grid)
     torch.cuda.synchronize()
     _close(y, x.float().mean(dim=(1, 2)) @ w.float().t() + bias)
+
+
+@pytest.mark.parametrize("k,stride,pad,hw,batch", [(7, 2, 3, 224, 2), (3, 2, 1, 224, 1), (7, 2, 3, 64, 3)])
+def test_stem_tma_window_mode_matches_conv(k, stride, pad, hw, batch):
+    """DARIS_CONV_PADDED_INPUT stems: zero-bordered NHWC8 input, one TMA box of
+    overlapping 128-B windows per kernel row, weights [cout][k][8][8]."""
+    from paper_2504_08795_b200 import kernels as K
+    dev = torch.device("cuda")
+    g = torch.Generator().manual_seed(100 + k + stride)
+    x = torch.randn(batch, 3, hw, hw, generator=g)
+    wt = torch.randn(64, 3, k, k, generator=g) / (3 * k * k) ** 0.5
+    scale = torch.rand(64, generator=g) + 0.5
+    bias = torch.randn(64, generator=g) * 0.1
+    ref = F.conv2d(x.bfloat16().float(), wt.bfloat16().float(), stride=stride, padding=pad)
+    ref = (ref.permute(0, 2, 3, 1) * scale + bias).clamp_min(0)
+    packed = K.pack_nhwc(x.to(dev), 8, border=pad, extra=8)
+    assert packed.shape == (batch, hw + 2 * pad, hw + 2 * pad + 8, 8)
+    inner = packed[:, pad:pad + hw, pad:pad + hw, :3].float().cpu()
+    assert torch.equal(inner, x.bfloat16().float().permute(0, 2, 3, 1))
+    assert packed[:, :pad].abs().sum().item() == 0 and packed[:, :, :pad].abs().sum().item() == 0
+    w8 = torch.zeros(64, k, 8, 8)
+    w8[:, :, :k, :3] = wt.permute(0, 2, 3, 1)
+    view = packed.view(-1)[: batch * hw * hw * 8].view(batch, hw, hw, 8)  # logical shape, padded storage
+    out = K.conv2d(view, w8.bfloat16().to(dev), scale.to(dev), bias.to(dev), stride=stride, pad=pad,
+                   padded_input=True, kw=k)
+    torch.cuda.synchronize()
+    _close(out, ref)
