@@ -56,6 +56,11 @@ typedef struct daris_conv_desc {
                              clusters of up to 8 CTAs, so split-K partials are reduced through
                              distributed shared memory instead of global atomics */
   void* timestamps;       /* optional: 16 uint64 globaltimer stamps per CTA (profiling), or NULL */
+  /* DARIS_CONV_DUAL: a second 1x1 convolution (a ResNet downsample branch) summed
+   * into the same accumulator as extra K blocks: y = act(conv(x)*scale + x2_s*W2 + bias)
+   * with x2_s = x2 sampled every stride2 pixels; weight is [cout][kh*kw*cin + cin2] */
+  const void* x2;         /* [n][h2][w2][cin2] bf16, or NULL */
+  int32_t h2, w2, cin2, stride2;
 } daris_conv_desc;
 
 enum {
@@ -64,7 +69,10 @@ enum {
    * and weight is [cout][kh][8][8] (the kw kernel columns padded to 8 pixel slots with
    * zeros): one K block = one kernel row, whose A tile is a single TMA box of
    * overlapping 128-B windows (requires cin == 8, kw <= 8, wo <= 128) */
-  DARIS_CONV_PADDED_INPUT = 2
+  DARIS_CONV_PADDED_INPUT = 2,
+  /* see x2 above: the primary conv must take the TMA path (cin % 64 == 0, wo <= 128);
+   * the branch is 1x1, pad 0, (ho-1)*stride2 < h2, cin2 % 64 == 0 */
+  DARIS_CONV_DUAL = 4
 };
 
 typedef struct daris_conv_plan_t {

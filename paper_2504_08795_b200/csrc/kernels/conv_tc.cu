@@ -80,6 +80,8 @@ struct ConvArgs {
   int th, tiles_h;    // TMA mode: output rows per M tile, M tiles per image
   int tma_c;          // 1: the epilogue stages the bf16 tile in smem and stores it with TMA (splits == 1)
   int stem_tma;       // 1: 8-channel stem from a zero-bordered input, one TMA window box per kernel row
+  int kb_seg1;        // K blocks of the primary input; blocks >= kb_seg1 come from x2 (DARIS_CONV_DUAL)
+  int stride2;        // x2 sampling stride
   unsigned long long* ts;  // optional per-CTA phase timestamps (globaltimer ns), 16 per CTA
   FDiv d_howo, d_wo, d_kw, d_cinb, d_tiles_h;
 };
@@ -152,7 +154,8 @@ __device__ __forceinline__ void finalize_row32(const ConvArgs& a, int m, int col
 template <int BN>
 __global__ void __maxnreg__(112)
     conv_igemm_tc_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
-                         const __grid_constant__ CUtensorMap ymap, const ConvArgs a) {
+                         const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap amap2,
+                         const ConvArgs a) {
   using L = SmemLayout<BN>;
   constexpr int kStages = L::kStages;
   constexpr int kLag = L::kLag;
@@ -205,6 +208,7 @@ __global__ void __maxnreg__(112)
       tma_prefetch_desc(&wmap);
       if (a.tma_a) tma_prefetch_desc(&amap);
       if (a.tma_c) tma_prefetch_desc(&ymap);
+      if (a.kb_seg1 < a.num_kb) tma_prefetch_desc(&amap2);
     }
   }
   tc_fence_before();
@@ -439,6 +443,10 @@ __global__ void __maxnreg__(112)
           tma_load_4d(&amap, &full[s], sA + s * L::kABytes, 0, 0, h0 * a.stride + kb, img);
           return;
         }
+        if (kb >= a.kb_seg1) {  // DARIS_CONV_DUAL branch: 1x1 over x2, sampled with stride2
+          tma_load_4d(&amap2, &full[s], sA + s * L::kABytes, (kb - a.kb_seg1) * kBK, 0, h0 * a.stride2, img);
+          return;
+        }
         const int kpos = fdiv(kb, a.d_cinb);
         const int cb = kb - kpos * a.cin_blocks;
         const int r_ = fdiv(kpos, a.d_kw), s_ = kpos - r_ * a.kw;
@@ -588,7 +596,8 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   using L = SmemLayout<BN>;
   auto encode = get_encode_fn();
   if (!encode) return DARIS_K_NO_DRIVER;
-  const int K = (d->flags & DARIS_CONV_PADDED_INPUT) ? d->kh * 64 : d->kh * d->kw * d->cin;
+  const int K = ((d->flags & DARIS_CONV_PADDED_INPUT) ? d->kh * 64 : d->kh * d->kw * d->cin) +
+                ((d->flags & DARIS_CONV_DUAL) ? d->cin2 : 0);
   CUtensorMap map;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(d->cout)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(K) * 2};
@@ -653,6 +662,24 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
     if (r != CUDA_SUCCESS) return DARIS_K_BAD_ARG;
   }
 
+  const bool dual = (d->flags & DARIS_CONV_DUAL) != 0;
+  CUtensorMap amap2;
+  std::memset(&amap2, 0, sizeof(amap2));
+  if (dual) {
+    const int th = pl.tma_rows;
+    cuuint64_t bdims[4] = {static_cast<cuuint64_t>(d->cin2), static_cast<cuuint64_t>(d->w2),
+                           static_cast<cuuint64_t>(d->h2), static_cast<cuuint64_t>(d->n)};
+    cuuint64_t bstr[3] = {static_cast<cuuint64_t>(d->cin2) * 2, static_cast<cuuint64_t>(d->w2) * d->cin2 * 2,
+                          static_cast<cuuint64_t>(d->h2) * d->w2 * d->cin2 * 2};
+    cuuint32_t bbox[4] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(d->wo * d->stride2),
+                          static_cast<cuuint32_t>(th * d->stride2), 1};
+    cuuint32_t bestr[4] = {1, static_cast<cuuint32_t>(d->stride2), static_cast<cuuint32_t>(d->stride2), 1};
+    r = encode(&amap2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(d->x2), bdims, bstr, bbox, bestr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return DARIS_K_BAD_ARG;
+  }
+
   static bool attr_set = false;  // per template instantiation
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(conv_igemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -678,6 +705,9 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   a.d_kw = make_fdiv(d->kw);
   a.d_cinb = make_fdiv(a.cin_blocks > 0 ? a.cin_blocks : 1);
   a.num_kb = stem_tma ? d->kh : d->cin == 8 ? (d->kh * d->kw + 7) / 8 : d->kh * d->kw * a.cin_blocks;
+  a.kb_seg1 = a.num_kb;
+  if (dual) a.num_kb += d->cin2 / kBK;
+  a.stride2 = dual ? d->stride2 : 1;
   a.kb_per_split = pl.kb_per_split;
   a.splits = pl.splits;
   a.cluster_split = pl.cluster > 1 ? 1 : 0;
@@ -711,7 +741,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
     attr[cfg.numAttrs].val.clusterDim.z = pl.cluster;
     cfg.numAttrs++;
   }
-  return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN>, map, amap, ymap, a));
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN>, map, amap, ymap, amap2, a));
 }
 
 }  // namespace daris
@@ -736,14 +766,20 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
   const int M = d->n * d->ho * d->wo;
   const bool padded = (d->flags & DARIS_CONV_PADDED_INPUT) != 0;
   if (padded && (d->cin != 8 || d->kw > 8 || d->wo > kBM)) return DARIS_K_BAD_SHAPE;
-  const int num_kb = padded ? d->kh : d->cin == 8 ? (d->kh * d->kw + 7) / 8 : d->kh * d->kw * (d->cin / kBK);
+  const bool dual = (d->flags & DARIS_CONV_DUAL) != 0;
+  if (dual && (d->cin2 % kBK != 0 || d->cin2 <= 0 || d->stride2 < 1 || (d->ho - 1) * d->stride2 >= d->h2 ||
+               (d->wo - 1) * d->stride2 >= d->w2 || d->cin % kBK != 0 || d->wo > kBM || d->residual))
+    return DARIS_K_BAD_SHAPE;
+  const int num_kb = (padded ? d->kh : d->cin == 8 ? (d->kh * d->kw + 7) / 8 : d->kh * d->kw * (d->cin / kBK)) +
+                     (dual ? d->cin2 / kBK : 0);
   const int budget = d->sm_budget > 0 ? d->sm_budget : daris_device_sms();
   // Activations by TMA (4-D box of th whole output rows) unless the layer is a
   // stem (8 channels: pixel-chunk gather) or a box side would exceed 256.
   static const bool tma_off = std::getenv("DARIS_CONV_GATHER") != nullptr;  // experiment knob
   const int th = std::max(1, std::min(d->ho, kBM / d->wo));
-  const bool tma_a = padded || (!tma_off && d->cin % kBK == 0 && d->wo * d->stride <= 256 &&
-                                 th * d->stride <= 256 && d->wo <= kBM);
+  const bool tma_a = padded || dual ||
+                     (!tma_off && d->cin % kBK == 0 && d->wo * d->stride <= 256 && th * d->stride <= 256 &&
+                      d->wo <= kBM);
   const int tiles_h = (d->ho + th - 1) / th;
   const int tiles_m = tma_a ? d->n * tiles_h : (M + kBM - 1) / kBM;
   int bn = d->block_n;
@@ -802,6 +838,7 @@ extern "C" int daris_conv2d(const daris_conv_desc* d, void* stream) {
   int rc = daris_conv_plan(d, &pl);
   if (rc != DARIS_K_OK) return rc;
   if (!d->x || !d->y || !d->weight || !d->scale || !d->bias) return DARIS_K_BAD_ARG;
+  if ((d->flags & DARIS_CONV_DUAL) && !d->x2) return DARIS_K_BAD_ARG;
   if (pl.splits > 1 && pl.cluster == 1 && (!d->workspace || !d->counters)) return DARIS_K_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (pl.block_n) {

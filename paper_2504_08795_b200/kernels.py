@@ -28,6 +28,7 @@ class ConvDesc(C.Structure):
         ("kh", C.c_int32), ("kw", C.c_int32), ("stride", C.c_int32), ("pad", C.c_int32),
         ("ho", C.c_int32), ("wo", C.c_int32), ("relu", C.c_int32), ("block_n", C.c_int32),
         ("splits", C.c_int32), ("sm_budget", C.c_int32), ("flags", C.c_int32), ("timestamps", C.c_void_p),
+        ("x2", C.c_void_p), ("h2", C.c_int32), ("w2", C.c_int32), ("cin2", C.c_int32), ("stride2", C.c_int32),
     ]
 
 
@@ -119,7 +120,7 @@ CLUSTER_SPLITK = True
 
 
 def conv_desc(x_shape, cout, kh, kw, stride, pad, *, relu=1, block_n=0, splits=0, sm_budget=0,
-              cluster: bool | None = None, padded_input: bool = False) -> ConvDesc:
+              cluster: bool | None = None, padded_input: bool = False, x2_shape=None, stride2: int = 1) -> ConvDesc:
     n, h, w, cin = x_shape
     ho = (h + 2 * pad - kh) // stride + 1
     wo = (w + 2 * pad - kw) // stride + 1
@@ -128,6 +129,10 @@ def conv_desc(x_shape, cout, kh, kw, stride, pad, *, relu=1, block_n=0, splits=0
     d.kh, d.kw, d.stride, d.pad, d.ho, d.wo = kh, kw, stride, pad, ho, wo
     d.relu, d.block_n, d.splits, d.sm_budget = relu, block_n, splits, sm_budget
     d.flags = (1 if (CLUSTER_SPLITK if cluster is None else cluster) else 0) | (2 if padded_input else 0)
+    if x2_shape is not None:  # DARIS_CONV_DUAL: 1x1 branch over x2 as extra K blocks
+        d.flags |= 4
+        _, d.h2, d.w2, d.cin2 = x2_shape
+        d.stride2 = stride2
     return d
 
 
@@ -142,15 +147,24 @@ def conv2d(x: torch.Tensor, weight: torch.Tensor, scale: torch.Tensor, bias: tor
            out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
            counters: torch.Tensor | None = None, block_n: int = 0, splits: int = 0,
            sm_budget: int = 0, stream=None, timestamps: torch.Tensor | None = None,
-           cluster: bool | None = None, padded_input: bool = False, kw: int | None = None) -> torch.Tensor:
+           cluster: bool | None = None, padded_input: bool = False, kw: int | None = None,
+           x2: torch.Tensor | None = None, stride2: int = 1, kh: int | None = None) -> torch.Tensor:
     """x: [n,h,w,cin] bf16 NHWC; weight: [cout,kh,kw,cin] bf16.
     padded_input (8-channel stems): x's storage is zero-bordered
     [n][h+2pad][w+2pad+8][8] (pack_nhwc(border=pad, extra=8)), weight is
-    [cout,kh,8,8] and `kw` gives the real kernel width."""
-    cout, kh, kw_w, cin = weight.shape
-    kw = kw if (padded_input and kw is not None) else kw_w
+    [cout,kh,8,8] and `kw` gives the real kernel width.
+    x2 (DARIS_CONV_DUAL): a 1x1, stride-`stride2` branch over x2 [n,h2,w2,cin2]
+    summed into the same accumulator; weight is 2-D [cout, kh*kw*cin + cin2]
+    and `kh`/`kw` give the primary kernel."""
+    if x2 is not None:
+        cout, cin = weight.shape[0], x.shape[3]
+        kh, kw = kh or 1, kw or 1
+    else:
+        cout, kh, kw_w, cin = weight.shape
+        kw = kw if (padded_input and kw is not None) else kw_w
     d = conv_desc(tuple(x.shape), cout, kh, kw, stride, pad, relu=relu, block_n=block_n,
-                  splits=splits, sm_budget=sm_budget, cluster=cluster, padded_input=padded_input)
+                  splits=splits, sm_budget=sm_budget, cluster=cluster, padded_input=padded_input,
+                  x2_shape=tuple(x2.shape) if x2 is not None else None, stride2=stride2)
     p = conv_plan(d)
     if out is None:
         out = torch.empty((d.n, d.ho, d.wo, cout), dtype=torch.bfloat16, device=x.device)
@@ -163,6 +177,7 @@ def conv2d(x: torch.Tensor, weight: torch.Tensor, scale: torch.Tensor, bias: tor
     d.scale, d.bias = _ptr(scale), _ptr(bias)
     d.workspace, d.counters = _ptr(workspace), _ptr(counters)
     d.timestamps = _ptr(timestamps)
+    d.x2 = _ptr(x2)
     _check(lib().daris_conv2d(C.byref(d), _stream(stream)), "daris_conv2d")
     return out
 

@@ -86,6 +86,8 @@ class ConvLayer:
     relu: int
     flops_per_image: int          # 2*MAC of the unpadded layer at 224x224 input
     padded_input: bool = False    # 8-channel stem read by TMA from a zero-bordered input (DARIS_CONV_PADDED_INPUT)
+    dual_cin: int = 0             # > 0: a fused 1x1 branch over cin2 = dual_cin channels (DARIS_CONV_DUAL);
+    dual_stride: int = 1          #      weight is then 2-D [cout][kh*kw*cin + dual_cin], scale folded in
 
 
 @dataclass
@@ -149,13 +151,35 @@ def _stem_layer(name, conv, bn, relu, device, hw_out, padded: bool = False) -> C
                      padded)
 
 
+def _dual_layer(name, conv, bn, ds_conv, ds_bn, relu, device, hw_out) -> ConvLayer:
+    """A bottleneck's last 1x1 conv with its downsample branch as one GEMM:
+    y = relu(A_x * (W*s) + A_in[::stride] * (W_ds*s_ds) + b + b_ds) — the two
+    BN scales folded into the bf16 weights, K = [cin | cin_ds], no residual read
+    and no separate downsample launch."""
+    w, scale, bias = fold_bn(conv, bn)
+    wd, sd, bd = fold_bn(ds_conv, ds_bn)
+    cout, cin = w.shape[0], w.shape[1]
+    cin_d = wd.shape[1]
+    cin_p, cind_p, cout_p = _pad64(cin), _pad64(cin_d), _pad64(cout)
+    wt = torch.zeros(cout_p, cin_p + cind_p)
+    wt[:cout, :cin] = w[:, :, 0, 0] * scale[:, None]
+    wt[:cout, cin_p:cin_p + cin_d] = wd[:, :, 0, 0] * sd[:, None]
+    sc = torch.zeros(cout_p)
+    bi = torch.zeros(cout_p)
+    sc[:cout] = 1.0
+    bi[:cout] = bias + bd
+    flops = 2 * cout * (cin + cin_d) * hw_out
+    return ConvLayer(name, wt.to(device=device, dtype=torch.bfloat16).contiguous(), sc.to(device), bi.to(device),
+                     1, 1, 1, 0, cin_p, cout_p, relu, flops, False, cind_p, ds_conv.stride[0])
+
+
 def _stem(b: "_Builder", name, conv, bn, relu, device, batch: int):
     """pack8 + the stem conv; the TMA-window form when the shape allows it (and
     the network is not run by the persistent stage kernel, which gathers)."""
     kh, kw = conv.kernel_size
     st, pd = conv.stride[0], conv.padding[0]
     wo = (224 + 2 * pd - kw) // st + 1
-    padded = STAGE_MODE != "persistent" and kw <= 8 and wo <= 128
+    padded = _BUILD_MODE != "persistent" and kw <= 8 and wo <= 128
     layer = _stem_layer(name, conv, bn, relu, device, wo * wo, padded)
     b.need("input", batch * 3 * 224 * 224)
     if padded:
@@ -179,6 +203,7 @@ class Op:
     shape_in: tuple = ()
     shape_out: tuple = ()
     flops: int = 0
+    shape_in2: tuple | None = None   # conv with a fused 1x1 branch: the branch input ("res" names it)
 
 
 @dataclass
@@ -194,6 +219,7 @@ class Network:
     flops_per_image: int
     torch_model: nn.Module | None = None
     weight_bytes: int = 0
+    stage_mode: str = "layers"       # the execution mode the op forms were built for
 
     @property
     def n_stages(self) -> int:
@@ -293,7 +319,10 @@ def _resnet_ops(model, name, batch, device, split) -> Network:
         hw_out = hw // stride
         identity = x
         ds = None
-        if blk.downsample is not None:
+        # the downsample branch rides in the block's last conv as extra K blocks
+        # (bottlenecks, "layers" mode); otherwise it is its own launch
+        fuse_ds = blk.downsample is not None and hasattr(blk, "conv3") and _BUILD_MODE != "persistent"
+        if blk.downsample is not None and not fuse_ds:
             dl = _conv_layer(f"{bname}.downsample", blk.downsample[0], blk.downsample[1], 0, device, hw_out * hw_out)
             ds, _ = b.conv(dl, x, shape)
             identity = ds
@@ -303,8 +332,14 @@ def _resnet_ops(model, name, batch, device, split) -> Network:
             l2 = _conv_layer(f"{bname}.conv2", blk.conv2, blk.bn2, 1, device, hw_out * hw_out)
             t2, s2 = b.conv(l2, t1, s1)
             b.give(t1)
-            l3 = _conv_layer(f"{bname}.conv3", blk.conv3, blk.bn3, 1, device, hw_out * hw_out)
-            out, s3 = b.conv(l3, t2, s2, res=identity)
+            if fuse_ds:
+                l3 = _dual_layer(f"{bname}.conv3+downsample", blk.conv3, blk.bn3, blk.downsample[0],
+                                 blk.downsample[1], 1, device, hw_out * hw_out)
+                out, s3 = b.conv(l3, t2, s2, res=x)
+                b.ops[-1].shape_in2 = shape
+            else:
+                l3 = _conv_layer(f"{bname}.conv3", blk.conv3, blk.bn3, 1, device, hw_out * hw_out)
+                out, s3 = b.conv(l3, t2, s2, res=identity)
             b.give(t2)
         else:
             l1 = _conv_layer(f"{bname}.conv1", blk.conv1, blk.bn1, 1, device, hw_out * hw_out)
@@ -454,7 +489,12 @@ RESNET50_SPLITS = {1: [], 2: [7], 3: [3, 10], 4: [3, 7, 13]}  # 4 stages: layer1
 
 def build_network(name: str, *, batch: int = 1, n_stages: int | None = None, seed: int = 0,
                   device: torch.device | str = "cuda", keep_torch: bool = False,
-                  model: nn.Module | None = None) -> Network:
+                  model: nn.Module | None = None, stage_mode: str | None = None) -> Network:
+    """stage_mode (default: DARIS_STAGE_MODE) picks the op forms: "layers" uses the
+    TMA-window stem and the downsample-fused block conv; the persistent stage
+    kernel ("persistent") runs the plain forms."""
+    global _BUILD_MODE
+    _BUILD_MODE = stage_mode or STAGE_MODE
     device = torch.device(device)
     if model is None:
         model = make_torch_model(name, seed)
@@ -473,6 +513,7 @@ def build_network(name: str, *, batch: int = 1, n_stages: int | None = None, see
             raise ValueError(f"unknown model {name!r}; known: {MODELS}")
     if keep_torch:
         net.torch_model = model
+    net.stage_mode = _BUILD_MODE
     seen = set()
     wb = 0
     for op in net.ops:
@@ -499,7 +540,8 @@ def allocate_buffers(net: Network, sm_budget: int = 0) -> TaskBuffers:
         if op.kind == "conv":
             L = op.layer
             d = K.conv_desc(op.shape_in, L.cout, L.kh, L.kw, L.stride, L.pad, relu=L.relu, sm_budget=sm_budget,
-                            padded_input=L.padded_input)
+                            padded_input=L.padded_input, x2_shape=op.shape_in2 if L.dual_cin else None,
+                            stride2=L.dual_stride)
             p = K.conv_plan(d)
             ws = max(ws, p.workspace_floats)
             ctr = max(ctr, p.counters)
@@ -514,7 +556,7 @@ def _view(t: torch.Tensor, shape) -> torch.Tensor:
     return t.view(-1)[:n].view(shape)
 
 
-def run_op(op: Op, tb: TaskBuffers, stream, sm_budget: int = 0) -> None:
+def run_op(op: Op, tb: TaskBuffers, stream, sm_budget: int = 0, timestamps=None) -> None:
     B = tb.bufs
     if op.kind == "pack8":
         border, extra = op.layer if op.layer else (0, 0)
@@ -522,11 +564,17 @@ def run_op(op: Op, tb: TaskBuffers, stream, sm_budget: int = 0) -> None:
                     stream=stream)
     elif op.kind == "conv":
         L = op.layer
+        if L.dual_cin:  # fused 1x1 branch over the block input (named by op.res)
+            K.conv2d(_view(B[op.src], op.shape_in), L.weight, L.scale, L.bias, stride=L.stride, pad=L.pad,
+                     relu=L.relu, out=_view(B[op.dst], op.shape_out), workspace=tb.workspace,
+                     counters=tb.counters, sm_budget=sm_budget, stream=stream, kh=L.kh, kw=L.kw,
+                     x2=_view(B[op.res], op.shape_in2), stride2=L.dual_stride, timestamps=timestamps)
+            return
         res = _view(B[op.res], op.shape_out) if op.res else None
         K.conv2d(_view(B[op.src], op.shape_in), L.weight, L.scale, L.bias, stride=L.stride, pad=L.pad,
                  relu=L.relu, residual=res, out=_view(B[op.dst], op.shape_out), workspace=tb.workspace,
                  counters=tb.counters, sm_budget=sm_budget, stream=stream, padded_input=L.padded_input,
-                 kw=L.kw)
+                 kw=L.kw, timestamps=timestamps)
     elif op.kind == "maxpool":
         K.maxpool(_view(B[op.src], op.shape_in), 3, 2, 1, out=_view(B[op.dst], op.shape_out), stream=stream)
     elif op.kind == "maxpool2":
@@ -558,6 +606,7 @@ def run_op(op: Op, tb: TaskBuffers, stream, sm_budget: int = 0) -> None:
 import os as _os
 
 STAGE_MODE = _os.environ.get("DARIS_STAGE_MODE", "layers")
+_BUILD_MODE = STAGE_MODE
 # persistent mode: CTAs per stage kernel (0 = the partition's SM count)
 STAGE_GRID = int(_os.environ.get("DARIS_STAGE_GRID", "0"))
 
@@ -634,6 +683,9 @@ def stage_program(net: Network, stage: int, tb: TaskBuffers, grid: int) -> "K.St
 def run_stage(net: Network, stage: int, tb: TaskBuffers, stream, sm_budget: int = 0, mode: str | None = None) -> int:
     """Launch one stage; returns the number of kernel launches issued."""
     mode = mode or STAGE_MODE
+    if (mode == "persistent") != (net.stage_mode == "persistent"):
+        raise ValueError(f"network built for stage mode {net.stage_mode!r} cannot run in {mode!r} "
+                         "(build_network(stage_mode=...))")
     if mode == "persistent":
         grid = STAGE_GRID or (sm_budget if sm_budget > 0 else K.device_sms())
         stage_program(net, stage, tb, grid).launch(stream)

@@ -239,3 +239,23 @@ def test_stem_tma_window_mode_matches_conv(k, stride, pad, hw, batch):
                    padded_input=True, kw=k)
     torch.cuda.synchronize()
     _close(out, ref)
+
+
+@pytest.mark.parametrize("n,hw,cin,cout,hw2,cin2,stride2,sm", [(1, 28, 128, 512, 56, 256, 2, 23), (1, 56, 64, 256, 56, 64, 1, 23),
+                                                              (2, 7, 512, 2048, 14, 1024, 2, 23), (1, 14, 256, 1024, 28, 512, 2, 72)])
+def test_conv_dual_branch_matches_sum_of_convs(n, hw, cin, cout, hw2, cin2, stride2, sm):
+    """DARIS_CONV_DUAL: a 1x1 conv over x plus a 1x1 stride-s branch over x2 in one
+    GEMM (the ResNet downsample folded into the block's last conv)."""
+    from paper_2504_08795_b200 import kernels as K
+    dev = torch.device("cuda")
+    g = torch.Generator().manual_seed(cin + cin2)
+    x = torch.randn(n, hw, hw, cin, generator=g).bfloat16()
+    x2 = torch.randn(n, hw2, hw2, cin2, generator=g).bfloat16()
+    w = (torch.randn(cout, cin + cin2, generator=g) / (cin + cin2) ** 0.5).bfloat16()
+    bias = torch.randn(cout, generator=g) * 0.1
+    ref = x.float() @ w[:, :cin].float().t() + x2[:, ::stride2, ::stride2, :].float() @ w[:, cin:].float().t()
+    ref = (ref + bias).clamp_min(0)
+    out = K.conv2d(x.to(dev), w.to(dev), torch.ones(cout, device=dev), bias.to(dev), relu=1, kh=1, kw=1,
+                   x2=x2.to(dev), stride2=stride2, sm_budget=sm)
+    torch.cuda.synchronize()
+    _close(out, ref)

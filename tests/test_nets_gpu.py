@@ -20,7 +20,7 @@ COS = 0.998
 @pytest.mark.parametrize("batch", [1, 2])
 @pytest.mark.parametrize("mode", ["persistent", "layers"])
 def test_network_matches_torch_cpu(name, batch, mode):
-    net = nets.build_network(name, batch=batch, keep_torch=True)
+    net = nets.build_network(name, batch=batch, keep_torch=True, stage_mode=mode)
     tb = nets.allocate_buffers(net, sm_budget=74)
     g = torch.Generator().manual_seed(11)
     x = torch.randn(batch, 3, 224, 224, generator=g)
@@ -51,7 +51,7 @@ def test_persistent_stage_kernel_grid_and_relaunch(grid):
     scheduling, any co-residency) and its self-resetting counters must make
     back-to-back launches of one program identical; it must also agree with
     the one-launch-per-layer path to bf16 rounding."""
-    net = nets.build_network("resnet50", batch=1)
+    net = nets.build_network("resnet50", batch=1, stage_mode="persistent")
     tb = nets.allocate_buffers(net, sm_budget=grid)
     x = torch.randn(1, 3, 224, 224, generator=torch.Generator().manual_seed(3)).cuda()
     outs = []
@@ -61,8 +61,9 @@ def test_persistent_stage_kernel_grid_and_relaunch(grid):
             nets.run_stage(net, st, tb, None, grid, mode="persistent")
         outs.append(tb.output.clone())
     torch.cuda.synchronize()
-    tb2 = nets.allocate_buffers(net, sm_budget=74)
-    ref = nets.forward(net, tb2, x, sm_budget=74, mode="layers").clone()
+    net_l = nets.build_network("resnet50", batch=1, stage_mode="layers")  # same seed, same weights
+    tb2 = nets.allocate_buffers(net_l, sm_budget=74)
+    ref = nets.forward(net_l, tb2, x, sm_budget=74, mode="layers").clone()
     torch.cuda.synchronize()
     for o in outs[1:]:
         rel_rep = ((o - outs[0]).norm() / outs[0].norm()).item()
@@ -74,7 +75,7 @@ def test_persistent_stage_kernel_grid_and_relaunch(grid):
 def test_persistent_stage_kernel_concurrent_programs():
     """Several programs running concurrently on different streams (as DARIS
     tenants do) produce the same results as when run alone."""
-    net = nets.build_network("resnet18", batch=1)
+    net = nets.build_network("resnet18", batch=1, stage_mode="persistent")
     xs = [torch.randn(1, 3, 224, 224, generator=torch.Generator().manual_seed(20 + i)).cuda() for i in range(6)]
     alone = []
     for x in xs:

@@ -42,19 +42,15 @@ def main():
     for i, op in enumerate(net.ops):
         if op.kind == "conv":
             L = op.layer
-            p = K.conv_plan(K.conv_desc(op.shape_in, L.cout, L.kh, L.kw, L.stride, L.pad, sm_budget=args.sms))
+            p = K.conv_plan(K.conv_desc(op.shape_in, L.cout, L.kh, L.kw, L.stride, L.pad, sm_budget=args.sms,
+                                        padded_input=L.padded_input,
+                                        x2_shape=op.shape_in2 if L.dual_cin else None, stride2=L.dual_stride))
             ts[i] = torch.zeros(p.ctas * 16, dtype=torch.int64, device="cuda")
 
     def forward(stream):
         for i, op in enumerate(net.ops):
             if op.kind == "conv":
-                L = op.layer
-                B = tb.bufs
-                res = nets._view(B[op.res], op.shape_out) if op.res else None
-                K.conv2d(nets._view(B[op.src], op.shape_in), L.weight, L.scale, L.bias, stride=L.stride,
-                         pad=L.pad, relu=L.relu, residual=res, out=nets._view(B[op.dst], op.shape_out),
-                         workspace=tb.workspace, counters=tb.counters, sm_budget=args.sms, stream=stream,
-                         timestamps=ts[i])
+                nets.run_op(op, tb, stream, args.sms, timestamps=ts[i])
             else:
                 nets.run_op(op, tb, stream, args.sms)
 
