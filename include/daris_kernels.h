@@ -114,7 +114,8 @@ int daris_avgpool(const void* x, float* y, int32_t n, int32_t hw, int32_t c, voi
  * y fp32 (y_bf16=0) or bf16. k % 8 == 0. */
 /* Global average pool over hw pixels of [batch][hw][k] NHWC bf16 fused with the
  * fp32 classifier y[batch][o] = mean(x) . w^T + bias (batch <= 4; `grid` blocks,
- * 0 = 32). The last two ops of a ResNet (torchvision avgpool + fc) as one launch. */
+ * 0 = one output feature per warp). The last two ops of a ResNet (torchvision
+ * avgpool + fc) as one launch. */
 int daris_pool_linear(const void* x, const void* w, const float* bias, float* y, int32_t batch, int32_t hw,
                       int32_t k, int32_t o, int32_t grid, void* stream);
 int daris_linear(const void* x, int32_t x_bf16, const void* w, const float* bias, void* y, int32_t y_bf16,

@@ -125,29 +125,44 @@ __global__ void maxpool_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat1
   reinterpret_cast<uint4*>(y)[idx] = pk;
 }
 
-// one thread per (image, 8 channels); hw is small (49) so a serial loop is fine
+// (image, 8 channels) per group of 8 lanes; the lanes split the pixels and
+// reduce with shuffles, so each thread has only ~hw/8 loads in flight
 __global__ void avgpool_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ y, int n, int hw, int c) {
   pdl_wait();
   pdl_trigger();
   const int chunks = c / 8;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= n * chunks) return;
-  const int img = idx / chunks, ch = idx - (idx / chunks) * chunks;
+  const int gidx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int part = gidx & 7;
+  const int idx = gidx >> 3;
+  const bool valid = idx < n * chunks;
+  const int img = valid ? idx / chunks : 0, ch = valid ? idx - (idx / chunks) * chunks : 0;
   float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int p = 0; p < hw; ++p) {
-    uint4 v = __ldg(reinterpret_cast<const uint4*>(x + (static_cast<size_t>(img) * hw + p) * c) + ch);
-    uint32_t vv[4] = {v.x, v.y, v.z, v.w};
+  if (valid) {
+    const uint4* src = reinterpret_cast<const uint4*>(x + static_cast<size_t>(img) * hw * c) + ch;
+#pragma unroll 4
+    for (int p = part; p < hw; p += 8) {
+      const uint4 v = __ldg(src + static_cast<size_t>(p) * chunks);
+      const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      float2 f = unpack_bf16x2(vv[e]);
-      acc[2 * e] += f.x;
-      acc[2 * e + 1] += f.y;
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = unpack_bf16x2(vv[e]);
+        acc[2 * e] += f.x;
+        acc[2 * e + 1] += f.y;
+      }
     }
   }
-  const float inv = 1.f / static_cast<float>(hw);
-  float4* dst = reinterpret_cast<float4*>(y + static_cast<size_t>(img) * c + ch * 8);
-  dst[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-  dst[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 1);
+    acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 2);
+    acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 4);
+  }
+  if (valid && part == 0) {
+    const float inv = 1.f / static_cast<float>(hw);
+    float4* dst = reinterpret_cast<float4*>(y + static_cast<size_t>(img) * c + ch * 8);
+    dst[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+    dst[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+  }
 }
 
 // Weight-streaming linear: one warp per output feature, all batch rows at once
@@ -180,16 +195,72 @@ __device__ __forceinline__ void load_x8(const void* x, int x_bf16, size_t off, f
 __global__ void linear_kernel(const void* __restrict__ x, int x_bf16, const __nv_bfloat16* __restrict__ w,
                               const float* __restrict__ bias, void* __restrict__ y, int y_bf16, int batch, int k,
                               int o, int relu) {
-  pdl_wait();
-  pdl_trigger();
   const int warps_per_block = blockDim.x >> 5;
   const int out_idx = blockIdx.x * warps_per_block + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
+  constexpr int kPre = 16;  // rows up to 16 x 256 = 4096 elements: held in registers
+  if (k <= kPre * 256 && batch <= kLinB) {
+    // Weights do not depend on the previous layer: issue the whole row slice of
+    // this lane before griddepcontrol.wait, so the fetch overlaps the producer's tail.
+    uint4 wv[kPre];
+    const __nv_bfloat16* wrow = w + static_cast<size_t>(out_idx < o ? out_idx : 0) * k;
+#pragma unroll
+    for (int i = 0; i < kPre; ++i) {
+      const int kk = lane * 8 + i * 256;
+      wv[i] = (out_idx < o && kk < k) ? ld_stream(wrow + kk) : make_uint4(0, 0, 0, 0);
+    }
+    pdl_wait();
+    pdl_trigger();
+    if (out_idx >= o) return;
+    float acc[kLinB] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < kPre; ++i) {
+      const int kk = lane * 8 + i * 256;
+      if (kk < k) {
+        const uint32_t ww[4] = {wv[i].x, wv[i].y, wv[i].z, wv[i].w};
+        float wf[8];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = unpack_bf16x2(ww[e]);
+          wf[2 * e] = f.x;
+          wf[2 * e + 1] = f.y;
+        }
+#pragma unroll
+        for (int bb = 0; bb < kLinB; ++bb) {
+          if (bb < batch) {
+            float xv[8];
+            load_x8(x, x_bf16, static_cast<size_t>(bb) * k + kk, xv);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[bb] = fmaf(xv[e], wf[e], acc[bb]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int bb = 0; bb < kLinB; ++bb) {
+      float v = acc[bb];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+      if (lane == 0 && bb < batch) {
+        v += bias ? bias[out_idx] : 0.f;
+        if (relu) v = fmaxf(v, 0.f);
+        const size_t oi = static_cast<size_t>(bb) * o + out_idx;
+        if (y_bf16)
+          static_cast<__nv_bfloat16*>(y)[oi] = __float2bfloat16_rn(v);
+        else
+          static_cast<float*>(y)[oi] = v;
+      }
+    }
+    return;
+  }
+  pdl_wait();
+  pdl_trigger();
   if (out_idx >= o) return;
   const __nv_bfloat16* wrow = w + static_cast<size_t>(out_idx) * k;
   for (int b0 = 0; b0 < batch; b0 += kLinB) {
     float acc[kLinB] = {0.f, 0.f, 0.f, 0.f};
-    for (int kk = lane * 8; kk < k; kk += 32 * 8) {
+#pragma unroll 8
+    for (int kk = lane * 8; kk < k; kk += 32 * 8) {  // unrolled: 8 weight loads in flight per lane
       uint4 wv = ld_stream(wrow + kk);
       uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
       float wf[8];
@@ -273,6 +344,7 @@ __global__ void pool_linear_kernel(const __nv_bfloat16* __restrict__ x, const __
   for (int j = blockIdx.x * warps + warp; j < o; j += gridDim.x * warps) {
     const __nv_bfloat16* wrow = w + static_cast<size_t>(j) * k;
     float acc[kPoolLinMaxB] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 8
     for (int kk = lane * 8; kk < k; kk += 32 * 8) {
       const uint4 wv = ld_stream(wrow + kk);
       const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
@@ -402,7 +474,7 @@ extern "C" int daris_maxpool(const void* x, void* y, int32_t n, int32_t h, int32
 extern "C" int daris_avgpool(const void* x, float* y, int32_t n, int32_t hw, int32_t c, void* stream) {
   if (!x || !y) return DARIS_K_BAD_ARG;
   if (c % 8 != 0) return DARIS_K_BAD_SHAPE;
-  const int work = n * (c / 8);
+  const int work = n * (c / 8) * 8;  // 8 lanes per (image, 8 channels)
   cudaError_t return_code = launch_pdl(avgpool_kernel, dim3(grid_for(work, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream),
       static_cast<const __nv_bfloat16*>(x), y, n, hw, c);
   return static_cast<int>(return_code);
@@ -432,8 +504,10 @@ extern "C" int daris_pool_linear(const void* x, const void* w, const float* bias
     }
     if (smem > 64 * 1024) return DARIS_K_BAD_SHAPE;
   }
+  // one output feature per warp by default: the GEMV is latency-bound, so every
+  // output row's weight loads should be in flight at once (the pool is redone per block)
   const int warps = threads / 32;
-  int g = grid > 0 ? grid : 32;
+  int g = grid > 0 ? grid : (o + warps - 1) / warps;
   if (g > (o + warps - 1) / warps) g = (o + warps - 1) / warps;
   cudaError_t rc = launch_pdl(pool_linear_kernel, dim3(g), dim3(threads), smem, static_cast<cudaStream_t>(stream),
                               static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w), bias, y,

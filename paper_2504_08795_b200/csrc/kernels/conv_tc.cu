@@ -92,9 +92,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-template <int BN>
+template <int BN, int ST = Depth<BN>::kStages>
 struct SmemLayout {
-  static constexpr int kStages = Depth<BN>::kStages;
+  static constexpr int kStages = ST;
   static constexpr int kLag = kStages - 1;  // cp.async groups kept in flight per producer thread
   static constexpr int kABytes = kBM * 128;
   static constexpr int kBBytes = BN * 128;
@@ -151,12 +151,12 @@ __device__ __forceinline__ void finalize_row32(const ConvArgs& a, int m, int col
   for (int q = 0; q < 4; ++q) yp[q] = pk[q];
 }
 
-template <int BN>
+template <int BN, int ST>
 __global__ void __maxnreg__(112)
     conv_igemm_tc_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
                          const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap amap2,
                          const ConvArgs a) {
-  using L = SmemLayout<BN>;
+  using L = SmemLayout<BN, ST>;
   constexpr int kStages = L::kStages;
   constexpr int kLag = L::kLag;
   extern __shared__ uint8_t smem_raw[];
@@ -591,9 +591,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
-template <int BN>
+template <int BN, int ST = Depth<BN>::kStages>
 static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cudaStream_t st) {
-  using L = SmemLayout<BN>;
+  using L = SmemLayout<BN, ST>;
   auto encode = get_encode_fn();
   if (!encode) return DARIS_K_NO_DRIVER;
   const int K = ((d->flags & DARIS_CONV_PADDED_INPUT) ? d->kh * 64 : d->kh * d->kw * d->cin) +
@@ -682,7 +682,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
 
   static bool attr_set = false;  // per template instantiation
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(conv_igemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(conv_igemm_tc_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          L::kTotal);
     if (e != cudaSuccess) return e;
     attr_set = true;
@@ -741,7 +741,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
     attr[cfg.numAttrs].val.clusterDim.z = pl.cluster;
     cfg.numAttrs++;
   }
-  return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN>, map, amap, ymap, amap2, a));
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN, ST>, map, amap, ymap, amap2, a));
 }
 
 }  // namespace daris
@@ -841,9 +841,16 @@ extern "C" int daris_conv2d(const daris_conv_desc* d, void* stream) {
   if ((d->flags & DARIS_CONV_DUAL) && !d->x2) return DARIS_K_BAD_ARG;
   if (pl.splits > 1 && pl.cluster == 1 && (!d->workspace || !d->counters)) return DARIS_K_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // Deeper rings for long K loops by TMA (each CTA streams >= 12 K blocks): more
+  // bytes in flight per SM at the cost of co-residency (experiment knob for now)
+  static const bool deep = [] {
+    const char* e = std::getenv("DARIS_CONV_DEEP");
+    return e && std::atoi(e) != 0;
+  }();
+  const bool go_deep = deep && pl.tma_rows > 0 && pl.kb_per_split >= 12;
   switch (pl.block_n) {
-    case 64: return launch_bn<64>(d, pl, st);
-    case 128: return launch_bn<128>(d, pl, st);
+    case 64: return go_deep ? launch_bn<64, 5>(d, pl, st) : launch_bn<64>(d, pl, st);
+    case 128: return go_deep ? launch_bn<128, 4>(d, pl, st) : launch_bn<128>(d, pl, st);
     case 256: return launch_bn<256>(d, pl, st);
   }
   return DARIS_K_BAD_SHAPE;

@@ -284,14 +284,19 @@ class _Builder:
         return dst, out_shape
 
 
+# the fused pool + classifier launch measured slower than avgpool + linear at batch 1
+# (every block re-pools the whole feature map): opt-in until it is restructured
+POOL_LINEAR = __import__("os").environ.get("DARIS_POOL_LINEAR", "0") == "1"
+
+
 def _pool_classifier(b: "_Builder", lin: LinearLayer, x: str, shape, batch: int) -> None:
-    """Global average pool + the final linear layer: one fused launch for small
-    batches (daris_pool_linear), avgpool then linear otherwise."""
+    """Global average pool + the final linear layer: avgpool then linear, or one
+    fused launch (daris_pool_linear, DARIS_POOL_LINEAR=1, batch <= 4)."""
     feat = shape[3]
     b.need("pooled", batch * feat)          # the two-launch form (and the persistent stage kernel) use it
     b.need("logits", batch * lin.weight.shape[0])
     out_shape = (batch, lin.weight.shape[0])
-    if batch <= 4:
+    if batch <= 4 and POOL_LINEAR:
         b.ops.append(Op("pool_linear", lin, x, "logits", None, shape, out_shape, lin.flops_per_image * batch))
     else:
         b.ops.append(Op("avgpool", None, x, "pooled", None, shape, (batch, feat)))
@@ -592,7 +597,7 @@ def run_op(op: Op, tb: TaskBuffers, stream, sm_budget: int = 0, timestamps=None)
     elif op.kind == "pool_linear":
         L = op.layer
         K.pool_linear(_view(B[op.src], op.shape_in), L.weight, L.bias, out=_view(B[op.dst], op.shape_out),
-                      grid=sm_budget if sm_budget > 0 else 32, stream=stream)
+                      grid=0, stream=stream)
     elif op.kind == "dwconv":
         L = op.layer
         K.dwconv(_view(B[op.src], op.shape_in), L.weight, L.scale, L.bias, stride=L.stride, pad=L.pad, relu=L.relu,
