@@ -82,6 +82,8 @@ struct ConvArgs {
   int stem_tma;       // 1: 8-channel stem from a zero-bordered input, one TMA window box per kernel row
   int kb_seg1;        // K blocks of the primary input; blocks >= kb_seg1 come from x2 (DARIS_CONV_DUAL)
   int stride2;        // x2 sampling stride
+  int tma_r;          // 1: the residual tile arrives by TMA into the epilogue staging (BN >= 128)
+  int box_rows;       // rows of one output/residual TMA box
   unsigned long long* ts;  // optional per-CTA phase timestamps (globaltimer ns), 16 per CTA
   FDiv d_howo, d_wo, d_kw, d_cinb, d_tiles_h;
 };
@@ -155,7 +157,7 @@ template <int BN, int ST>
 __global__ void __maxnreg__(112)
     conv_igemm_tc_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
                          const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap amap2,
-                         const ConvArgs a) {
+                         const __grid_constant__ CUtensorMap rmap, const ConvArgs a) {
   using L = SmemLayout<BN, ST>;
   constexpr int kStages = L::kStages;
   constexpr int kLag = L::kLag;
@@ -208,6 +210,7 @@ __global__ void __maxnreg__(112)
       tma_prefetch_desc(&wmap);
       if (a.tma_a) tma_prefetch_desc(&amap);
       if (a.tma_c) tma_prefetch_desc(&ymap);
+      if (a.tma_r) tma_prefetch_desc(&rmap);
       if (a.kb_seg1 < a.num_kb) tma_prefetch_desc(&amap2);
     }
   }
@@ -297,7 +300,7 @@ __global__ void __maxnreg__(112)
     const bool has_res = a.res != nullptr && row_ok;
     const __nv_bfloat16* res_row = has_res ? a.res + static_cast<size_t>(m) * a.cout + n0 : nullptr;
     uint4 res_cur[4];
-    if (has_res) {
+    if (has_res && !a.tma_r) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) res_cur[q] = ldg_nc16(res_row + 8 * q);
     }
@@ -329,19 +332,39 @@ __global__ void __maxnreg__(112)
       // rows past the image / tensor end are clipped by the tensor map.
       uint8_t* stage = sA;
       const uint32_t swz = static_cast<uint32_t>(row & 7);
+      const int c1 = a.tma_a ? h0 * a.wo : m0;
+      const int c2 = a.tma_a ? img : 0;
+      if (a.tma_r) {
+        // wide tiles: the whole residual tile by TMA into the staging area (same
+        // swizzled layout), one exposed latency instead of one per 32-column chunk;
+        // each thread then rewrites its residual chunks in place with the output
+        if (threadIdx.x == 0) {
+          mbar_arrive_expect_tx(red_bar, static_cast<uint32_t>((BN / 64) * a.box_rows * 128));
+#pragma unroll
+          for (int h = 0; h < BN / 64; ++h) tma_load_3d(&rmap, red_bar, stage + h * (kBM * 128), n0 + h * 64, c1, c2);
+        }
+        mbar_wait(red_bar, 0);
+      }
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
         uint4 res_nxt[4];
-        if (has_res && c0 + 32 < BN) {
+        if (has_res && !a.tma_r && c0 + 32 < BN) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) res_nxt[q] = ldg_nc16(res_row + c0 + 32 + 8 * q);
         }
         tmem_ld_32x32b_x32(t_row + c0, r);
-        uint4 pk[4];
-        pack_row32(a, c0, reinterpret_cast<const float*>(r), s_scale, s_bias, has_res ? res_cur : nullptr, pk);
         uint8_t* rowp = stage + (c0 >> 6) * (kBM * 128) + row * 128;
         const uint32_t chunk0 = static_cast<uint32_t>((c0 & 63) >> 3);
+        uint4 rs[4];
+        const uint4* resp = has_res ? res_cur : nullptr;
+        if (a.tma_r) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) rs[q] = *reinterpret_cast<const uint4*>(rowp + (((chunk0 + q) ^ swz) << 4));
+          resp = rs;
+        }
+        uint4 pk[4];
+        pack_row32(a, c0, reinterpret_cast<const float*>(r), s_scale, s_bias, resp, pk);
 #pragma unroll
         for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(rowp + (((chunk0 + q) ^ swz) << 4)) = pk[q];
 #pragma unroll
@@ -350,8 +373,6 @@ __global__ void __maxnreg__(112)
       fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the TMA engine
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (threadIdx.x == 0) {
-        const int c1 = a.tma_a ? h0 * a.wo : m0;
-        const int c2 = a.tma_a ? img : 0;
 #pragma unroll
         for (int h = 0; h < BN / 64; ++h) tma_store_3d(&ymap, stage + h * (kBM * 128), n0 + h * 64, c1, c2);
         bulk_commit();
@@ -498,7 +519,8 @@ __global__ void __maxnreg__(112)
     cluster_sync();  // every split's MMAs are done (rings idle) and every receiver is armed
     if (ts && threadIdx.x == 0) ts[9] = gtimer();
     if (warp < 4) {
-      // push this thread's accumulator row to the CTA that owns it
+      // push this thread's accumulator row to the CTA that owns it (st.async;
+      // measured faster than staging locally + one bulk DMA per owner)
       const int row = warp * 32 + lane;
       const bool push = row < mvalid;
       const int owner = ((row + 1) * S - 1) / kBM;
@@ -646,8 +668,14 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   // whose box is one M tile (th whole output rows of one image, or 128 flat rows)
   static const bool no_tma_c = std::getenv("DARIS_NO_TMA_STORE") != nullptr;  // experiment knob
   const bool tma_c = !no_tma_c && pl.splits == 1;
-  CUtensorMap ymap;
+  // residual tile by TMA into the staging area: measured slower than the
+  // per-thread register prefetch (layer1 conv3 epilogue 5.4 vs 4.4 us) — opt-in knob
+  static const bool want_tma_r = std::getenv("DARIS_TMA_RESIDUAL") != nullptr;
+  const bool tma_r = tma_c && want_tma_r && d->residual != nullptr && BN >= 128;
+  CUtensorMap ymap, rmap;
   std::memset(&ymap, 0, sizeof(ymap));
+  std::memset(&rmap, 0, sizeof(rmap));
+  int box_rows = 0;
   if (tma_c) {
     const bool per_image = pl.tma_rows > 0;
     const cuuint64_t rows = per_image ? static_cast<cuuint64_t>(d->ho) * d->wo
@@ -660,6 +688,13 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return DARIS_K_BAD_ARG;
+    if (tma_r) {  // the residual: same geometry as the output
+      r = encode(&rmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(d->residual), ydims, ystr, ybox, yestr,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return DARIS_K_BAD_ARG;
+    }
+    box_rows = static_cast<int>(ybox[1]);
   }
 
   const bool dual = (d->flags & DARIS_CONV_DUAL) != 0;
@@ -714,6 +749,8 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   a.tma_a = pl.tma_rows > 0 ? 1 : 0;
   a.tma_c = tma_c ? 1 : 0;
   a.stem_tma = stem_tma ? 1 : 0;
+  a.tma_r = tma_r ? 1 : 0;
+  a.box_rows = box_rows;
   a.th = pl.tma_rows > 0 ? pl.tma_rows : 1;
   a.tiles_h = (d->ho + a.th - 1) / a.th;
   a.d_tiles_h = make_fdiv(a.tiles_h);
@@ -741,7 +778,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
     attr[cfg.numAttrs].val.clusterDim.z = pl.cluster;
     cfg.numAttrs++;
   }
-  return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN, ST>, map, amap, ymap, amap2, a));
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN, ST>, map, amap, ymap, amap2, rmap, a));
 }
 
 }  // namespace daris

@@ -85,6 +85,15 @@ __device__ __forceinline__ void st_async_v4(uint32_t remote_addr, float a, float
                "f"(a), "f"(b), "f"(c), "f"(d), "r"(remote_mbar)
                : "memory");
 }
+// Bulk DMA of `bytes` (multiple of 16) from this CTA's smem to a cluster peer's
+// smem, completing as complete_tx on the peer's mbarrier (dst/mbar from dsmem_map).
+__device__ __forceinline__ void bulk_copy_to_peer(uint32_t remote_dst, uint32_t local_src, uint32_t bytes,
+                                                  uint32_t remote_mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   remote_dst),
+               "r"(local_src), "r"(bytes), "r"(remote_mbar)
+               : "memory");
+}
 // (no "memory" clobber: a batch of these must be able to be in flight together;
 // ordering against the cluster barrier comes from the barrier's own clobber)
 __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
@@ -120,6 +129,13 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* m, uint64_t* bar,
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
           smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
 __device__ __forceinline__ void tma_load_4d(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1, int c2,

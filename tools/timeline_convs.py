@@ -88,6 +88,13 @@ def main():
                "teardown_us": statistics.median((a[:, 6] - a[:, 5]).tolist()),
                "span_us": end - released,
                "gap_from_prev_us": None if prev_end is None else released - prev_end}
+        raw = ts[i].view(-1, 16).cpu()
+        if (raw[:, 8] > 0).all():  # cluster split-K: sync / push+arrive / reduce / final wait
+            row["cluster_us"] = [statistics.median((a[:, 9] - a[:, 8]).tolist()),
+                                 statistics.median((a[:, 10] - a[:, 9]).tolist()),
+                                 statistics.median((a[:, 11] - a[:, 10]).tolist()),
+                                 statistics.median((a[:, 5] - a[:, 11]).tolist()),
+                                 statistics.median((a[:, 8] - a[:, 4]).tolist())]
         prev_end = end
         rows.append(row)
     total = rows[-1]["end"] - rows[0]["released"]
@@ -98,7 +105,9 @@ def main():
         print(f"{r['name']:28s} {r['ctas']:4d} {r['span_us']:5.1f} "
               f"{(r['gap_from_prev_us'] if r['gap_from_prev_us'] is not None else 0):5.2f} {r['setup_us']:5.2f} "
               f"{r['wait_us']:6.2f} {r['produce_us']:5.2f} {r['mma_tail_us']:5.2f} {r['epilogue_us']:5.2f}"
-              f"({r['epilogue_max_us']:5.2f}) {r['teardown_us']:5.2f}")
+              f"({r['epilogue_max_us']:5.2f}) {r['teardown_us']:5.2f}"
+              + ("  cluster[pre %.2f sync %.2f push %.2f reduce %.2f wait %.2f]" % (
+                  r["cluster_us"][4], *r["cluster_us"][:4]) if "cluster_us" in r else ""))
     gaps = [r["gap_from_prev_us"] for r in rows if r["gap_from_prev_us"] is not None]
     spans = [r["span_us"] for r in rows]
     print(f"sum span {sum(spans):.1f} us, sum gaps {sum(gaps):.1f} us (median gap {statistics.median(gaps):.2f})")
