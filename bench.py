@@ -257,6 +257,7 @@ def batching_baseline(batches=(1, 2, 4, 8, 16, 32, 64), reps: int = 20) -> dict:
 
 
 STALL_RETRIES = 6  # re-measurements of a window that contained a GPU-wide stall
+TIMED_ATTEMPTS = 10  # timed windows, stepping the rate down 5 % after each one that misses a deadline
 
 
 def run_clean(rt, duration: float, warmup: float, log, tag: str):
@@ -373,13 +374,16 @@ def ours(args) -> dict | None:
         return res, wall, clk.summary()
 
     # timed run at the knee; step down if the confirmation run breaks the constraints
-    for attempt in range(4):
+    # (a window that misses a deadline steps the rate down 5 %; a GPU-wide stall
+    # inside a window is re-measured by run_clean, not stepped down for)
+    for attempt in range(TIMED_ATTEMPTS):
         res, wall, clocks = timed(rate)
         ok = all_reduce([1.0 if feasible(res.report) else 0.0], "min")[0] > 0
         log(f"timed rate={rate:.1f} ok={ok} jps={res.report.jps:.0f} wall={wall:.2f}s")
-        if ok or attempt == 3:
+        if ok or attempt == TIMED_ATTEMPTS - 1:
             break
         rate *= 0.95
+    constraints_met = ok
     rep = res.report
     net0 = next(iter(rt.nets.values()))
     n_ops = {st: nets.stage_launches(net0, st) for st in range(net0.n_stages)}
@@ -395,10 +399,10 @@ def ours(args) -> dict | None:
     # end-to-end through host buffers (H2D input + D2H logits every job)
     rt.use_host_io(True)
     e2e_rate = rate
-    for attempt in range(4):
+    for attempt in range(TIMED_ATTEMPTS):
         res_e, wall_e, _ = timed(e2e_rate)
-        ok = all_reduce([1.0 if feasible(res_e.report) else 0.0], "min")[0] > 0
-        if ok or attempt == 3:
+        ok_e = all_reduce([1.0 if feasible(res_e.report) else 0.0], "min")[0] > 0
+        if ok_e or attempt == TIMED_ATTEMPTS - 1:
             break
         e2e_rate *= 0.95
     re = res_e.report
@@ -408,7 +412,8 @@ def ours(args) -> dict | None:
     e2e = {"value": round(e_done / window, 2), "unit": UNIT,
            "h2d_bytes_per_step": int(res_e.stats["h2d_bytes"] * frac / args.steps),
            "d2h_bytes_per_step": int(res_e.stats["d2h_bytes"] * frac / args.steps),
-           "rate_per_task": round(e2e_rate, 2), "hp_miss": int(re.missed_hp), "dmr_lp": re.dmr_lp}
+           "rate_per_task": round(e2e_rate, 2), "hp_miss": int(re.missed_hp), "dmr_lp": re.dmr_lp,
+           "constraints_met": bool(ok_e)}
     rt.use_host_io(False)
 
     roof = conv_roofline(rt, peaks) if rank == 0 else None
@@ -432,6 +437,7 @@ def ours(args) -> dict | None:
                              "pools (8 x 64 x 602 KB = 308 MB per GPU)",
                        "timing": "host steady clock over the periodic schedule, barrier + synchronize both "
                                  "sides, max over ranks; stage completions via CUDA events"},
+            "constraints_met": bool(constraints_met),
             "hp_miss": int(tot[1]), "dmr_lp": (tot[2] / tot[4]) if tot[4] else 0.0,
             "executor_stats": {k: res.stats[k] for k in ("graph_launches", "slot_waits", "polls",
                                                           "release_lag_max", "loop_gap_max", "progress_gap_max",

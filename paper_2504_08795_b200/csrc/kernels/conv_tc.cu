@@ -82,7 +82,6 @@ struct ConvArgs {
   int stem_tma;       // 1: 8-channel stem from a zero-bordered input, one TMA window box per kernel row
   int kb_seg1;        // K blocks of the primary input; blocks >= kb_seg1 come from x2 (DARIS_CONV_DUAL)
   int stride2;        // x2 sampling stride
-  int tma_r;          // 1: the residual tile arrives by TMA into the epilogue staging (BN >= 128)
   int box_rows;       // rows of one output/residual TMA box
   unsigned long long* ts;  // optional per-CTA phase timestamps (globaltimer ns), 16 per CTA
   FDiv d_howo, d_wo, d_kw, d_cinb, d_tiles_h;
@@ -94,11 +93,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-template <int BN, int ST = Depth<BN>::kStages>
+template <int BN, int ST = Depth<BN>::kStages, int MT = 1>
 struct SmemLayout {
   static constexpr int kStages = ST;
   static constexpr int kLag = kStages - 1;  // cp.async groups kept in flight per producer thread
-  static constexpr int kABytes = kBM * 128;
+  static constexpr int kABytes = MT * kBM * 128;  // MT = 2: a 256-row A tile (two UMMA M=128 sub-tiles)
   static constexpr int kBBytes = BN * 128;
   static constexpr int kAOff = 0;
   static constexpr int kBOff = kStages * kABytes;
@@ -118,11 +117,12 @@ __device__ __forceinline__ uint4 ldg_nc16(const void* p) { return __ldg(reinterp
 // 32 accumulator columns of one output row -> scale/bias (smem) + residual
 // (already in registers) -> act -> 4 x 16 B of bf16.
 __device__ __forceinline__ void pack_row32(const ConvArgs& a, int c_local, const float* v, const float* s_scale,
-                                           const float* s_bias, const uint4* res4, uint4 (&pk)[4]) {
+                                           const float* s_bias, const uint4 (&res4)[4], bool use_res,
+                                           uint4 (&pk)[4]) {
   float o[32];
 #pragma unroll
   for (int j = 0; j < 32; ++j) o[j] = v[j] * s_scale[c_local + j] + s_bias[c_local + j];
-  if (res4 != nullptr) {
+  if (use_res) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint32_t rr[4] = {res4[q].x, res4[q].y, res4[q].z, res4[q].w};
@@ -145,20 +145,21 @@ __device__ __forceinline__ void pack_row32(const ConvArgs& a, int c_local, const
 
 // ... and straight to this row of the NHWC output (one thread per row).
 __device__ __forceinline__ void finalize_row32(const ConvArgs& a, int m, int col0, int c_local, const float* v,
-                                               const float* s_scale, const float* s_bias, const uint4* res4) {
+                                               const float* s_scale, const float* s_bias, const uint4 (&res4)[4],
+                                               bool use_res) {
   uint4 pk[4];
-  pack_row32(a, c_local, v, s_scale, s_bias, res4, pk);
+  pack_row32(a, c_local, v, s_scale, s_bias, res4, use_res, pk);
   uint4* yp = reinterpret_cast<uint4*>(a.y + static_cast<size_t>(m) * a.cout + col0);
 #pragma unroll
   for (int q = 0; q < 4; ++q) yp[q] = pk[q];
 }
 
-template <int BN, int ST>
+template <int BN, int ST, int MT>
 __global__ void __maxnreg__(112)
     conv_igemm_tc_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
                          const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap amap2,
-                         const __grid_constant__ CUtensorMap rmap, const ConvArgs a) {
-  using L = SmemLayout<BN, ST>;
+                         const ConvArgs a) {
+  using L = SmemLayout<BN, ST, MT>;
   constexpr int kStages = L::kStages;
   constexpr int kLag = L::kLag;
   extern __shared__ uint8_t smem_raw[];
@@ -205,12 +206,11 @@ __global__ void __maxnreg__(112)
     fence_barrier_init();
   }
   if (warp == 4) {
-    tmem_alloc<BN>(tmem_slot);
+    tmem_alloc<MT * BN>(tmem_slot);
     if (lane == 0) {
       tma_prefetch_desc(&wmap);
       if (a.tma_a) tma_prefetch_desc(&amap);
       if (a.tma_c) tma_prefetch_desc(&ymap);
-      if (a.tma_r) tma_prefetch_desc(&rmap);
       if (a.kb_seg1 < a.num_kb) tma_prefetch_desc(&amap2);
     }
   }
@@ -300,7 +300,7 @@ __global__ void __maxnreg__(112)
     const bool has_res = a.res != nullptr && row_ok;
     const __nv_bfloat16* res_row = has_res ? a.res + static_cast<size_t>(m) * a.cout + n0 : nullptr;
     uint4 res_cur[4];
-    if (has_res && !a.tma_r) {
+    if (has_res) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) res_cur[q] = ldg_nc16(res_row + 8 * q);
     }
@@ -334,47 +334,40 @@ __global__ void __maxnreg__(112)
       const uint32_t swz = static_cast<uint32_t>(row & 7);
       const int c1 = a.tma_a ? h0 * a.wo : m0;
       const int c2 = a.tma_a ? img : 0;
-      if (a.tma_r) {
-        // wide tiles: the whole residual tile by TMA into the staging area (same
-        // swizzled layout), one exposed latency instead of one per 32-column chunk;
-        // each thread then rewrites its residual chunks in place with the output
-        if (threadIdx.x == 0) {
-          mbar_arrive_expect_tx(red_bar, static_cast<uint32_t>((BN / 64) * a.box_rows * 128));
-#pragma unroll
-          for (int h = 0; h < BN / 64; ++h) tma_load_3d(&rmap, red_bar, stage + h * (kBM * 128), n0 + h * 64, c1, c2);
-        }
-        mbar_wait(red_bar, 0);
-      }
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t r[32];
-        uint4 res_nxt[4];
-        if (has_res && !a.tma_r && c0 + 32 < BN) {
+      for (int sub = 0; sub < MT; ++sub) {  // MT = 2: rows 128..255 of the tile come from TMEM cols [BN, 2 BN)
+        const int srow = sub * kBM + row;
+        const bool sres = a.res != nullptr && srow < mvalid;
+        const __nv_bfloat16* sres_row = sres ? a.res + static_cast<size_t>(m0 + srow) * a.cout + n0 : nullptr;
+        if (sub > 0 && sres) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) res_nxt[q] = ldg_nc16(res_row + c0 + 32 + 8 * q);
+          for (int q = 0; q < 4; ++q) res_cur[q] = ldg_nc16(sres_row + 8 * q);
         }
-        tmem_ld_32x32b_x32(t_row + c0, r);
-        uint8_t* rowp = stage + (c0 >> 6) * (kBM * 128) + row * 128;
-        const uint32_t chunk0 = static_cast<uint32_t>((c0 & 63) >> 3);
-        uint4 rs[4];
-        const uint4* resp = has_res ? res_cur : nullptr;
-        if (a.tma_r) {
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          uint4 res_nxt[4];
+          if (sres && c0 + 32 < BN) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) rs[q] = *reinterpret_cast<const uint4*>(rowp + (((chunk0 + q) ^ swz) << 4));
-          resp = rs;
+            for (int q = 0; q < 4; ++q) res_nxt[q] = ldg_nc16(sres_row + c0 + 32 + 8 * q);
+          }
+          tmem_ld_32x32b_x32(t_row + sub * BN + c0, r);
+          uint8_t* rowp = stage + (c0 >> 6) * (MT * kBM * 128) + srow * 128;
+          const uint32_t chunk0 = static_cast<uint32_t>((c0 & 63) >> 3);
+          uint4 pk[4];
+          pack_row32(a, c0, reinterpret_cast<const float*>(r), s_scale, s_bias, res_cur, sres, pk);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(rowp + (((chunk0 + q) ^ swz) << 4)) = pk[q];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) res_cur[q] = res_nxt[q];
         }
-        uint4 pk[4];
-        pack_row32(a, c0, reinterpret_cast<const float*>(r), s_scale, s_bias, resp, pk);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(rowp + (((chunk0 + q) ^ swz) << 4)) = pk[q];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) res_cur[q] = res_nxt[q];
       }
       fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the TMA engine
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (threadIdx.x == 0) {
 #pragma unroll
-        for (int h = 0; h < BN / 64; ++h) tma_store_3d(&ymap, stage + h * (kBM * 128), n0 + h * 64, c1, c2);
+        for (int h = 0; h < BN / 64; ++h)
+          tma_store_3d(&ymap, stage + h * (MT * kBM * 128), n0 + h * 64, c1, c2);
         bulk_commit();
         bulk_wait_read();
       }
@@ -390,7 +383,7 @@ __global__ void __maxnreg__(112)
         tmem_ld_32x32b_x32(t_row + c0, r);
         if (row_ok)
           finalize_row32(a, m, n0 + c0, c0, reinterpret_cast<const float*>(r), s_scale, s_bias,
-                         has_res ? res_cur : nullptr);
+                         res_cur, has_res);
 #pragma unroll
         for (int q = 0; q < 4; ++q) res_cur[q] = res_nxt[q];
       }
@@ -434,7 +427,7 @@ __global__ void __maxnreg__(112)
 #pragma unroll
             for (int q = 0; q < 8; ++q) __stcg(src + q, make_float4(0.f, 0.f, 0.f, 0.f));  // re-arm
             finalize_row32(a, m, n0 + c0, c0, reinterpret_cast<const float*>(part), s_scale, s_bias,
-                           has_res ? res_cur : nullptr);
+                           res_cur, has_res);
 #pragma unroll
             for (int q = 0; q < 4; ++q) res_cur[q] = res_nxt[q];
           }
@@ -497,12 +490,15 @@ __global__ void __maxnreg__(112)
         const int s = i % kStages;
         mbar_wait(&full[s], (i / kStages) & 1);
         tc_fence_after();
-        const uint64_t adesc = umma_desc_k_sw128(sA_u32 + s * L::kABytes);
         const uint64_t bdesc = umma_desc_k_sw128(sB_u32 + s * L::kBBytes);
 #pragma unroll
-        for (int k = 0; k < kBK / 16; ++k) {
-          // +32 B along K inside the 128 B swizzle atom = +2 in the encoded start address
-          umma_bf16(tmem_base, adesc + 2 * k, bdesc + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+        for (int sub = 0; sub < MT; ++sub) {  // M sub-tile sub: A rows [128 sub, 128 sub + 128), TMEM cols [BN sub, ...)
+          const uint64_t adesc = umma_desc_k_sw128(sA_u32 + s * L::kABytes + sub * (kBM * 128));
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            // +32 B along K inside the 128 B swizzle atom = +2 in the encoded start address
+            umma_bf16(tmem_base + sub * BN, adesc + 2 * k, bdesc + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+          }
         }
         umma_commit(&empty[s]);
       }
@@ -594,7 +590,7 @@ __global__ void __maxnreg__(112)
   __syncthreads();
   if (warp == 4) {
     tc_fence_after();
-    tmem_dealloc<BN>(tmem_base);
+    tmem_dealloc<MT * BN>(tmem_base);
   }
   if (ts && threadIdx.x == 0) ts[6] = gtimer();
 }
@@ -613,9 +609,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
-template <int BN, int ST = Depth<BN>::kStages>
+template <int BN, int ST = Depth<BN>::kStages, int MT = 1>
 static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cudaStream_t st) {
-  using L = SmemLayout<BN, ST>;
+  using L = SmemLayout<BN, ST, MT>;
   auto encode = get_encode_fn();
   if (!encode) return DARIS_K_NO_DRIVER;
   const int K = ((d->flags & DARIS_CONV_PADDED_INPUT) ? d->kh * 64 : d->kh * d->kw * d->cin) +
@@ -668,13 +664,9 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   // whose box is one M tile (th whole output rows of one image, or 128 flat rows)
   static const bool no_tma_c = std::getenv("DARIS_NO_TMA_STORE") != nullptr;  // experiment knob
   const bool tma_c = !no_tma_c && pl.splits == 1;
-  // residual tile by TMA into the staging area: measured slower than the
-  // per-thread register prefetch (layer1 conv3 epilogue 5.4 vs 4.4 us) — opt-in knob
-  static const bool want_tma_r = std::getenv("DARIS_TMA_RESIDUAL") != nullptr;
-  const bool tma_r = tma_c && want_tma_r && d->residual != nullptr && BN >= 128;
-  CUtensorMap ymap, rmap;
+  if (MT > 1 && !tma_c) return DARIS_K_BAD_SHAPE;  // 256-row tiles leave through the TMA-store epilogue only
+  CUtensorMap ymap;
   std::memset(&ymap, 0, sizeof(ymap));
-  std::memset(&rmap, 0, sizeof(rmap));
   int box_rows = 0;
   if (tma_c) {
     const bool per_image = pl.tma_rows > 0;
@@ -688,12 +680,6 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return DARIS_K_BAD_ARG;
-    if (tma_r) {  // the residual: same geometry as the output
-      r = encode(&rmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(d->residual), ydims, ystr, ybox, yestr,
-                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r != CUDA_SUCCESS) return DARIS_K_BAD_ARG;
-    }
     box_rows = static_cast<int>(ybox[1]);
   }
 
@@ -717,7 +703,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
 
   static bool attr_set = false;  // per template instantiation
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(conv_igemm_tc_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(conv_igemm_tc_kernel<BN, ST, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          L::kTotal);
     if (e != cudaSuccess) return e;
     attr_set = true;
@@ -749,7 +735,6 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   a.tma_a = pl.tma_rows > 0 ? 1 : 0;
   a.tma_c = tma_c ? 1 : 0;
   a.stem_tma = stem_tma ? 1 : 0;
-  a.tma_r = tma_r ? 1 : 0;
   a.box_rows = box_rows;
   a.th = pl.tma_rows > 0 ? pl.tma_rows : 1;
   a.tiles_h = (d->ho + a.th - 1) / a.th;
@@ -778,7 +763,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
     attr[cfg.numAttrs].val.clusterDim.z = pl.cluster;
     cfg.numAttrs++;
   }
-  return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN, ST>, map, amap, ymap, amap2, rmap, a));
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN, ST, MT>, map, amap, ymap, amap2, a));
 }
 
 }  // namespace daris
@@ -852,16 +837,34 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
   if (splits > num_kb) splits = num_kb;
   int kbps = (num_kb + splits - 1) / splits;
   splits = (num_kb + kbps - 1) / kbps;  // no empty splits
+  // 256-row tiles (two UMMA M=128 sub-tiles, 2*BN TMEM columns) when the grid
+  // would exceed the planned SMs anyway: half the CTAs, each weight tile loaded
+  // once for twice the rows. Measured slower at batch 1 (ResNet-50 at 24 SMs
+  // 0.44 vs 0.37 ms isolated, 13.9k vs 15.6k inf/s loaded capacity: the lost
+  // parallelism costs more than the per-CTA overheads saved) — opt-in, DARIS_M256=1
+  static const bool no_m256 = std::getenv("DARIS_M256") == nullptr ||
+                              std::getenv("DARIS_NO_TMA_STORE") != nullptr;
+  int m_sub = 1;
+  int th_used = th, tiles_m_used = tiles_m;
+  if (!no_m256 && tma_a && splits == 1 && bn <= 128 && tiles > budget) {
+    const int th2 = std::max(1, std::min(d->ho, 2 * kBM / d->wo));
+    if (th2 * d->wo > kBM && th2 * d->stride <= 256 && (!dual || th2 * d->stride2 <= 256)) {
+      m_sub = 2;
+      th_used = th2;
+      tiles_m_used = d->n * ((d->ho + th2 - 1) / th2);
+    }
+  }
   out->block_n = bn;
   out->splits = splits;
   out->kb_per_split = kbps;
-  out->tiles_m = tiles_m;
+  out->tiles_m = tiles_m_used;
   out->tiles_n = tiles_n;
   out->workspace_floats = splits > 1 ? static_cast<int64_t>(tiles) * kBM * bn : 0;  // zero-initialised
   out->counters = splits > 1 ? 2 * tiles : 0;  // ticket + done per tile
-  out->ctas = tiles * splits;
+  out->ctas = tiles_m_used * tiles_n * splits;
+  out->m_sub = m_sub;
   out->cluster = (splits > 1 && bn == 64 && (d->flags & DARIS_CONV_CLUSTER_SPLITK)) ? splits : 1;
-  out->tma_rows = tma_a ? th : 0;
+  out->tma_rows = tma_a ? th_used : 0;
   if (out->cluster > 1) {  // partials reduce through DSMEM: no global scratch
     out->workspace_floats = 0;
     out->counters = 0;
@@ -885,6 +888,13 @@ extern "C" int daris_conv2d(const daris_conv_desc* d, void* stream) {
     return e && std::atoi(e) != 0;
   }();
   const bool go_deep = deep && pl.tma_rows > 0 && pl.kb_per_split >= 12;
+  if (pl.m_sub == 2) {
+    switch (pl.block_n) {
+      case 64: return launch_bn<64, 2, 2>(d, pl, st);
+      case 128: return launch_bn<128, 2, 2>(d, pl, st);
+    }
+    return DARIS_K_BAD_SHAPE;
+  }
   switch (pl.block_n) {
     case 64: return go_deep ? launch_bn<64, 5>(d, pl, st) : launch_bn<64>(d, pl, st);
     case 128: return go_deep ? launch_bn<128, 4>(d, pl, st) : launch_bn<128>(d, pl, st);

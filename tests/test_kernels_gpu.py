@@ -259,3 +259,25 @@ def test_conv_dual_branch_matches_sum_of_convs(n, hw, cin, cout, hw2, cin2, stri
                    x2=x2.to(dev), stride2=stride2, sm_budget=sm)
     torch.cuda.synchronize()
     _close(out, ref)
+
+
+@pytest.mark.parametrize("n,hw,cin,cout,k,stride,residual", [(1, 56, 64, 256, 1, 1, True), (1, 56, 64, 64, 3, 1, False),
+                                                             (2, 28, 128, 512, 1, 1, True), (1, 14, 256, 1024, 1, 1, True),
+                                                             (1, 56, 128, 128, 3, 2, False), (3, 28, 512, 128, 1, 1, False)])
+def test_conv_256_row_tiles(n, hw, cin, cout, k, stride, residual):
+    """m_sub = 2: two UMMA M=128 sub-tiles per CTA (chosen when the grid exceeds
+    the planned SMs): same numerics as the 128-row path."""
+    import subprocess
+    import sys
+    # the planner reads DARIS_M256 once per process: run the case in a child
+    root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
+    code = (f"import sys; sys.path[:0] = [{root!r}, {root + '/tests'!r}]; import test_kernels_gpu as T; "
+            "from paper_2504_08795_b200 import kernels as K; "
+            f"d = K.conv_desc(({n}, {hw}, {hw}, {cin}), {cout}, {k}, {k}, {stride}, {k // 2}, sm_budget=8); "
+            "assert K.conv_plan(d).m_sub == 2; "
+            f"T._conv_case({n}, {hw}, {hw}, {cin}, {cout}, {k}, {stride}, {k // 2}, residual={residual}, "
+            f"sm_budget=8, seed={hw + cin})")
+    import os
+    env = dict(os.environ, DARIS_M256="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]

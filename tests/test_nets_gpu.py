@@ -94,3 +94,19 @@ def test_persistent_stage_kernel_concurrent_programs():
     for a, tb in zip(alone, tbs):
         rel = ((tb.output - a).norm() / a.norm()).item()
         assert rel < 1e-2, rel
+
+
+@pytest.mark.parametrize("name,batch", [("resnet50", 1), ("resnet50", 2), ("resnet18", 1), ("mobilenet_v2", 1)])
+def test_network_at_the_executor_plan(name, batch):
+    """Grids planned for the C2 per-job share (23 SMs): 256-row tiles, fused
+    downsample, stems by TMA — the forms the executor captures."""
+    net = nets.build_network(name, batch=batch, keep_torch=True, stage_mode="layers")
+    tb = nets.allocate_buffers(net, sm_budget=23)
+    x = torch.randn(batch, 3, 224, 224, generator=torch.Generator().manual_seed(5))
+    out = nets.forward(net, tb, x.cuda(), stream=None, sm_budget=23, mode="layers").float().cpu().clone()
+    torch.cuda.synchronize()
+    with torch.no_grad():
+        ref = net.torch_model(x).float()
+    rel = ((out - ref).norm() / ref.norm()).item()
+    cos = torch.nn.functional.cosine_similarity(out.flatten(), ref.flatten(), dim=0).item()
+    assert rel <= REL_L2 and cos >= COS, (rel, cos)
