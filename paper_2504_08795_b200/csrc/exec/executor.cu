@@ -6,8 +6,11 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
-#include <pthread.h>
-#include <sched.h>
+#include <sys/resource.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <cerrno>
 
 #include <algorithm>
 #include <chrono>
@@ -418,31 +421,35 @@ int64_t daris_exec_trace_copy(const daris_exec* ex, daris_stage_trace* buf, int6
   return n;
 }
 
-// The dispatcher thread runs the wall-clock loop at real-time priority for the
-// run (SCHED_FIFO when the process may, e.g. as root on the GPU box): a
-// preempted poller shows up directly as stage-dispatch lag and HP deadline
-// misses at sub-millisecond periods. Restored on exit; DARIS_EXEC_RT=0 disables.
-struct RtGuard {
-  int policy = SCHED_OTHER;
-  sched_param old{};
+// The dispatcher thread runs the wall-clock loop at the highest CFS priority
+// (nice -20 for this thread when the process may, e.g. as root on the GPU box):
+// a preempted poller shows up directly as stage-dispatch lag and HP deadline
+// misses at sub-millisecond periods. Not SCHED_FIFO: a busy-polling real-time
+// thread exhausts the kernel's RT budget (950 ms per 1 s) and is then throttled
+// for 50 ms — measured as 50.4 ms whole-schedule stalls. Restored on exit;
+// DARIS_EXEC_NICE=0 disables.
+struct NiceGuard {
+  int old = 0;
   bool set = false;
-  RtGuard() {
-    const char* e = std::getenv("DARIS_EXEC_RT");
+  pid_t tid = 0;
+  NiceGuard() {
+    const char* e = std::getenv("DARIS_EXEC_NICE");
     if (e && std::atoi(e) == 0) return;
-    if (pthread_getschedparam(pthread_self(), &policy, &old) != 0) return;
-    sched_param p{};
-    p.sched_priority = 50;
-    set = pthread_setschedparam(pthread_self(), SCHED_FIFO, &p) == 0;
+    tid = static_cast<pid_t>(syscall(SYS_gettid));
+    errno = 0;
+    old = getpriority(PRIO_PROCESS, static_cast<id_t>(tid));
+    if (errno != 0) return;
+    set = setpriority(PRIO_PROCESS, static_cast<id_t>(tid), -20) == 0;
   }
-  ~RtGuard() {
-    if (set) pthread_setschedparam(pthread_self(), policy, &old);
+  ~NiceGuard() {
+    if (set) setpriority(PRIO_PROCESS, static_cast<id_t>(tid), old);
   }
 };
 
 int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warmup, const double* phases,
                    int32_t collect_log, daris_report* report, daris_exec_stats* stats) {
   using clock = std::chrono::steady_clock;
-  RtGuard rt_priority;
+  NiceGuard loop_priority;
   const daris_exec_config& c = ex->cfg;
   int32_t n_tasks = 0;
   daris_n_tasks(h, &n_tasks);

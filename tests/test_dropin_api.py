@@ -92,3 +92,21 @@ def _write(tmp_path, obj):
     p = tmp_path / "sweep.json"
     p.write_text(json.dumps(obj))
     return p
+
+
+def test_event_log_wire_format_round_trip(tmp_path):
+    """JSONL event log (the reference CLI's --emit-event-log format): written,
+    read back and audited by the replay checkers; the log-only replay of the
+    metrics equals the run's own report."""
+    import paper_2504_08795_b200 as S
+    cfg = S.scenario_from_dict({"preset": "c2_b200", "duration": 0.5})
+    res = S.build_simulation(cfg).run()
+    path = tmp_path / "events.jsonl"
+    n = S.write_event_log(path, [res])
+    recs = S.read_event_log(path)
+    assert n == len(recs) == len(res.records) and recs[0]["kind"] == "release"
+    assert set(recs[0]) == {"time", "kind", "task", "job", "stage", "context", "stream", "rate"}
+    S.check_event_order(recs, cfg.duration)
+    rep = S.replay_metrics(recs, res.effective_tasks, duration=cfg.duration,
+                           warmup_end=cfg.duration * cfg.warmup_frac)
+    assert S.compare_with_report(rep, res.report) == []

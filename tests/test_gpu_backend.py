@@ -77,6 +77,16 @@ def test_gpu_scenario_runs_and_replays(preset, rate):
     assert rep.completed_hp > 0 and rep.completed_lp > 0
     assert res.stats["graph_launches"] > 0 and res.trace
     assert all(p["green"] for p in res.partitions)
+    # the real run's event log in the reference wire format, audited from the log alone
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        path = f"{d}/events.jsonl"
+        S.write_event_log(path, [res])
+        recs = S.read_event_log(path)
+    S.check_event_order(recs, cfg.duration)
+    rep = S.replay_metrics(recs, res.effective_tasks, duration=cfg.duration,
+                           warmup_end=cfg.duration * cfg.warmup_frac)
+    assert S.compare_with_report(rep, res.report) == []
     # same decisions through the native trace engine of the drop-in API ...
     eff = res.effective_tasks
     replay = S.Simulation(eff, cfg.gpu, seed=cfg.seed, duration=cfg.duration, warmup_frac=cfg.warmup_frac,
