@@ -6,9 +6,11 @@ instance per GPU, tasks sharded by the box placer; weak scaling).
 
 Workload at N=1 (BASELINE.json configs[1]): 8 periodic ResNet-50 tasks
 (4 HP / 4 LP), batch 1, 224x224, 4 stages, 4 contexts x 2 streams with
-oversubscription 2 (four 74-SM green-context partitions), run at the knee
-point — the highest per-task rate that keeps HP misses at 0 and LP misses
-under 2 % (found by a short search, then confirmed by the timed run).
+oversubscription 2 (four 72-SM green-context partitions), run at the knee
+point — the per-task rate with the most completed inferences/s that keeps HP
+misses at 0 and LP misses under 2 %, an LP job rejected by admission control
+counting as missed (found by a short search, then confirmed by the timed run,
+stepping down 5 % until a timed window meets the constraints).
 
 A "step" is one scheduling window of `--step-seconds` of periodic releases;
 `value` = inferences completed for jobs released in the K timed steps ÷ the
@@ -161,9 +163,21 @@ def c2_tasks(rate: float, ids: list[int]):
             for i, g in enumerate(ids)]
 
 
+def lp_loss(rep) -> float:
+    """LP jobs lost to a miss OR to admission rejection, over LP jobs released."""
+    return (rep.missed_lp + rep.rejected_lp) / rep.released_lp if rep.released_lp else 0.0
+
+
 def feasible(rep) -> bool:
+    """HP miss = 0 and LP miss < 2 %, where an LP job rejected by admission
+    control counts as missed. The reference's DMR (engine.py:153-220) counts
+    misses over ADMITTED jobs only, under which a schedule that rejects every LP
+    job is "feasible" at half the throughput — past the knee DARIS admission
+    flips into exactly that state (MRET-based utilisation estimates rise, LP
+    admission tests fail, the rejected load never returns), so the headline
+    uses the stricter loss rate; `dmr_lp` is reported alongside."""
     done = rep.completed_hp + rep.completed_lp
-    return done > 0 and rep.missed_hp == 0 and rep.dmr_lp < 0.02
+    return done > 0 and rep.missed_hp == 0 and rep.dmr_lp < 0.02 and lp_loss(rep) < 0.02
 
 
 def conv_roofline(rt, peaks) -> dict:
@@ -398,10 +412,16 @@ def ours(args) -> dict | None:
 
     # end-to-end through host buffers (H2D input + D2H logits every job)
     rt.use_host_io(True)
-    e2e_rate = rate
+    # its own knee: the H2D input copy sits on the critical path of every job
+    e2e_rate = knee_search(rt, 0.8 * rate, args.probe_seconds, log)
+    e2e_rate = all_reduce([e2e_rate], "min")[0]
     for attempt in range(TIMED_ATTEMPTS):
         res_e, wall_e, _ = timed(e2e_rate)
         ok_e = all_reduce([1.0 if feasible(res_e.report) else 0.0], "min")[0] > 0
+        r_ = res_e.report
+        log(f"e2e rate={e2e_rate:.1f} ok={ok_e} jps={r_.jps:.0f} miss_hp={r_.missed_hp} dmr_lp={r_.dmr_lp:.3f} "
+            f"rej_lp={r_.rejected_lp} p99_hp={r_.response_hp.p99 * 1e3:.3f}ms "
+            f"loop_gap_max={res_e.stats['loop_gap_max'] * 1e6:.0f}us slot_waits={res_e.stats['slot_waits']}")
         if ok_e or attempt == TIMED_ATTEMPTS - 1:
             break
         e2e_rate *= 0.95
@@ -413,6 +433,7 @@ def ours(args) -> dict | None:
            "h2d_bytes_per_step": int(res_e.stats["h2d_bytes"] * frac / args.steps),
            "d2h_bytes_per_step": int(res_e.stats["d2h_bytes"] * frac / args.steps),
            "rate_per_task": round(e2e_rate, 2), "hp_miss": int(re.missed_hp), "dmr_lp": re.dmr_lp,
+           "lp_loss": round(lp_loss(re), 5),
            "constraints_met": bool(ok_e)}
     rt.use_host_io(False)
 
@@ -439,6 +460,7 @@ def ours(args) -> dict | None:
                                  "sides, max over ranks; stage completions via CUDA events"},
             "constraints_met": bool(constraints_met),
             "hp_miss": int(tot[1]), "dmr_lp": (tot[2] / tot[4]) if tot[4] else 0.0,
+            "lp_loss": round(lp_loss(rep), 5),
             "executor_stats": {k: res.stats[k] for k in ("graph_launches", "slot_waits", "polls",
                                                           "release_lag_max", "loop_gap_max", "progress_gap_max",
                                                           "stalls", "wall_seconds")},
