@@ -101,6 +101,29 @@ __global__ void maxpool_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat1
   float best[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) best[e] = -INFINITY;
+  if (k == 3) {  // ResNet's 3x3 stem pool: all 9 window loads in flight at once
+    uint4 v[9];
+    bool ok[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      const int ih = oh * stride - pad + q / 3, iw = ow * stride - pad + q % 3;
+      ok[q] = ih >= 0 && ih < h && iw >= 0 && iw < w;
+      v[q] = ok[q] ? __ldg(reinterpret_cast<const uint4*>(x + ((static_cast<size_t>(img) * h + ih) * w + iw) * c) + ch)
+                   : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+      if (!ok[q]) continue;
+      const uint32_t vv[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = unpack_bf16x2(vv[e]);
+        best[2 * e] = fmaxf(best[2 * e], f.x);
+        best[2 * e + 1] = fmaxf(best[2 * e + 1], f.y);
+      }
+    }
+    k = 0;  // done
+  }
   for (int r = 0; r < k; ++r) {
     const int ih = oh * stride - pad + r;
     if (ih < 0 || ih >= h) continue;

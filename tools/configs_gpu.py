@@ -41,6 +41,7 @@ def emit(d):
 
 def summary(rep) -> dict:
     return {"jps": round(rep.jps, 1), "hp_miss": int(rep.missed_hp), "dmr_lp": round(rep.dmr_lp, 4),
+            "lp_loss": round(bench.lp_loss(rep), 4), "constraints_met": bench.feasible(rep),
             "rejected_lp": int(rep.rejected_lp), "p99_hp_ms": round(rep.response_hp.p99 * 1e3, 3),
             "p99_lp_ms": round(rep.response_lp.p99 * 1e3, 3)}
 
@@ -51,13 +52,16 @@ def knee_factor(rt, set_factor, f0: float, probe: float) -> tuple[float, None]:
 
 
 def confirm(rt, set_factor, f: float, seconds: float):
-    """Timed confirmation at the knee; step down 5 % while it breaks the constraints."""
-    for _ in range(4):
+    """Timed confirmation at the knee; step down 5 % while it breaks the constraints
+    (bench.TIMED_ATTEMPTS windows; the result records whether they were met)."""
+    for _ in range(bench.TIMED_ATTEMPTS):
         set_factor(f)
         res = bench.run_clean(rt, seconds, seconds * 0.1, log, f"confirm {f:.3g}")[0]
         if bench.feasible(res.report):
+            res.constraints_met = True
             return f, res
         f *= 0.95
+    res.constraints_met = False
     return f, res
 
 
