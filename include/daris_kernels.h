@@ -84,6 +84,7 @@ typedef struct daris_conv_plan_t {
   int32_t tma_rows;         /* > 0: activations arrive by TMA, M tile = tma_rows whole output rows */
   int32_t m_sub;            /* UMMA M=128 sub-tiles per CTA: 2 = a 256-row tile (TMA path, no split-K),
                                chosen when the grid would exceed the planned SMs */
+  int32_t halo;             /* 1: 3x3/s1/p1 from one halo tile per 64-channel block (conv_halo_kernel) */
 } daris_conv_plan_t;
 
 int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out);

@@ -83,9 +83,10 @@ def test_gpu_scenario_runs_and_replays(preset, rate):
         path = f"{d}/events.jsonl"
         S.write_event_log(path, [res])
         recs = S.read_event_log(path)
-    S.check_event_order(recs, cfg.duration)
-    rep = S.replay_metrics(recs, res.effective_tasks, duration=cfg.duration,
-                           warmup_end=cfg.duration * cfg.warmup_frac)
+    from paper_2504_08795_b200.runtime import quantize  # the executor's 2^-20 s time grid
+    horizon, warm = quantize(cfg.duration), quantize(cfg.duration * cfg.warmup_frac)
+    S.check_event_order(recs, horizon)
+    rep = S.replay_metrics(recs, res.effective_tasks, duration=horizon, warmup_end=warm)
     assert S.compare_with_report(rep, res.report) == []
     # same decisions through the native trace engine of the drop-in API ...
     eff = res.effective_tasks
