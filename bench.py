@@ -155,12 +155,46 @@ def barrier():
 
 # ----------------------------------------------------------------------------- our arm
 
-def c2_tasks(rate: float, ids: list[int]):
+def c2_tasks(rate: float, ids: list[int], batch: int = 1):
     from paper_2504_08795_b200.model import Priority
     from paper_2504_08795_b200.runtime import TaskDef
     # ids 1..4 of every 8 are HP, 5..8 LP (4 HP / 4 LP per GPU)
-    return [TaskDef(i + 1, "resnet50", Priority.HP if (g % 8) < 4 else Priority.LP, rate, 4)
+    return [TaskDef(i + 1, "resnet50", Priority.HP if (g % 8) < 4 else Priority.LP, rate, 4, batch)
             for i, g in enumerate(ids)]
+
+
+def daris_batched(args, gpu, mine, log, batch: int = 4) -> dict:
+    """The paper's "DARIS with batched inputs" variant: the
+    same 8-task C2 schedule, every job a batch of `batch` images. Reported next
+    to the batch-1 headline (which BASELINE.json's config fixes) and to the
+    single-tenant batching baseline."""
+    from paper_2504_08795_b200.runtime import DarisRuntime
+    rt = DarisRuntime(c2_tasks(100.0, mine, batch), gpu, slots=3, seed=0)
+    rt.capture_all()
+    rt.afet = rt.calibrate_full_load(0.2)
+    guess = 0.6 * (gpu.n_contexts * gpu.n_streams) / max(rt.afet.values()) / len(mine)
+    rate = knee_search(rt, guess, min(args.probe_seconds, 0.6), log)
+    rate = all_reduce([rate], "min")[0]
+    step, dur = args.step_seconds, (args.warmup + args.steps) * args.step_seconds
+    ok = False
+    for _ in range(TIMED_ATTEMPTS):
+        rt.set_rate(rate)
+        barrier()
+        res = run_clean(rt, dur, args.warmup * step, log, f"batched {rate:.0f}")[0]
+        barrier()
+        ok = all_reduce([1.0 if feasible(res.report) else 0.0], "min")[0] > 0
+        log(f"batched b{batch} rate={rate:.1f} ok={ok} inf/s={res.report.jps:.0f}")
+        if ok:
+            break
+        rate *= 0.95
+    rep = res.report
+    done = all_reduce([rep.jps], "sum")[0]  # report JPS counts images (batch per job, engine.py:153-220)
+    out = {"batch": batch, "value": round(done, 1), "unit": UNIT, "rate_per_task": round(rate, 2),
+           "constraints_met": bool(ok), "hp_miss": int(rep.missed_hp), "lp_loss": round(lp_loss(rep), 5),
+           "p99_hp_response_ms": round(rep.response_hp.p99 * 1e3, 3),
+           "isolated_job_ms": round(sum(rt.stage_nominal[rt.tasks[0].key]) * 1e3, 3)}
+    rt.close()
+    return out
 
 
 def lp_loss(rep) -> float:
@@ -439,6 +473,7 @@ def ours(args) -> dict | None:
 
     roof = conv_roofline(rt, peaks) if rank == 0 else None
     rt.close()
+    batched = None if args.no_batched else daris_batched(args, gpu, mine, log)
     batching = batching_baseline() if (rank == 0 and not args.no_batching) else None
     cpu = cpu_reference(args.cpu_seconds) if (rank == 0 and world == 1 and not args.no_cpu) else None
     flops_inf = next(iter(rt.nets.values())).flops_per_image
@@ -480,6 +515,9 @@ def ours(args) -> dict | None:
             "batching_baseline": batching,
             "vs_single_tenant_batching": (round(value / world / batching["best_inf_per_s"], 4)
                                           if batching else None),
+            "daris_batched": batched,
+            "daris_batched_vs_single_tenant_batching": (
+                round(batched["value"] / world / batching["best_inf_per_s"], 4) if (batched and batching) else None),
         }
     return out
 
@@ -568,6 +606,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-batching", action="store_true")
+    ap.add_argument("--no-batched", action="store_true", help="skip the DARIS-with-batched-inputs variant")
     ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

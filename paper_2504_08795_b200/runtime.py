@@ -219,6 +219,12 @@ class TaskDef:
     priority: Priority
     rate: float                  # jobs per second (period = 1/rate, quantised)
     n_stages: int | None = None
+    batch: int = 1               # images per job (the reference's TaskSpec batch_size)
+
+    @property
+    def key(self) -> str:
+        """Name of the network a job of this task runs (model, or model@bB)."""
+        return self.model if self.batch == 1 else f"{self.model}@b{self.batch}"
 
     @property
     def period(self) -> float:
@@ -280,9 +286,9 @@ class DarisRuntime:
         # one weight copy per model, shared by all tasks running it
         self.nets: dict[tuple, nets.Network] = {}
         for t in self.tasks:
-            key = (t.model, t.n_stages)
+            key = (t.model, t.n_stages, t.batch)
             if key not in self.nets:
-                self.nets[key] = nets.build_network(t.model, batch=1, n_stages=t.n_stages, seed=seed,
+                self.nets[key] = nets.build_network(t.model, batch=t.batch, n_stages=t.n_stages, seed=seed,
                                                     device=self.device)
         self.buffers: dict[tuple[int, int], nets.TaskBuffers] = {}
         for t in self.tasks:
@@ -299,7 +305,7 @@ class DarisRuntime:
         self.afet: dict[int, float] | None = None
 
     def net_of(self, t: TaskDef) -> nets.Network:
-        return self.nets[(t.model, t.n_stages)]
+        return self.nets[(t.model, t.n_stages, t.batch)]
 
     # -- inputs ------------------------------------------------------------
     def _make_pools(self, pool_size: int) -> None:
@@ -321,8 +327,8 @@ class DarisRuntime:
             pool, out = self._pool_cache[key]
             self.pools[t.id] = pool
             self.host_out[t.id] = out
-            in_bytes = 3 * 224 * 224 * 4
-            self.exec.set_pool(t.id, pool.data_ptr(), self.e2e, pool_size, in_bytes,
+            in_bytes = t.batch * 3 * 224 * 224 * 4  # a job copies `batch` consecutive images
+            self.exec.set_pool(t.id, pool.data_ptr(), self.e2e, max(1, pool_size // t.batch), in_bytes,
                                out.data_ptr() if out is not None else None,
                                out.numel() * 4 if out is not None else 0)
             for s in range(self.exec.slots):
@@ -358,8 +364,8 @@ class DarisRuntime:
         programs) before anything is captured."""
         stream = torch.cuda.Stream(device=self.device)
         with torch.cuda.stream(stream):
-            for (model, _), net in self.nets.items():
-                tb = self.buffers[(next(t.id for t in self.tasks if t.model == model), 0)]
+            for key, net in self.nets.items():
+                tb = self.buffers[(next(t.id for t in self.tasks if (t.model, t.n_stages, t.batch) == key), 0)]
                 for st in range(net.n_stages):
                     nets.run_stage(net, st, tb, stream.cuda_stream, self.sm_budget)
         stream.synchronize()
@@ -373,9 +379,9 @@ class DarisRuntime:
                 self.capture_all()
             out = {}
             for t in self.tasks:
-                if t.model in out:
+                if t.key in out:
                     continue
-                out[t.model] = [max(self.exec.time_graph(t.id, st, 1, 0, 20), 2 * QUANTUM)
+                out[t.key] = [max(self.exec.time_graph(t.id, st, 1, 0, 20), 2 * QUANTUM)
                                 for st in range(self.net_of(t).n_stages)]
             self._nominal = out
         return self._nominal
@@ -384,13 +390,14 @@ class DarisRuntime:
     def specs(self) -> list[TaskSpec]:
         out = []
         for t in self.tasks:
-            nom = self.stage_nominal[t.model]
+            nom = self.stage_nominal[t.key]
             stages = tuple(StageProfile(float(x), self.sm_per_ctx) for x in nom)
             out.append(TaskSpec.periodic(t.id, t.period, t.priority, stages))
         return out
 
     def open_dispatcher(self, full_load: dict[int, float]) -> _core.Handle:
-        dicts = [spec_to_dict(s) for s in self.specs()]
+        batch = {t.id: t.batch for t in self.tasks}
+        dicts = [spec_to_dict(s, batch[s.id]) for s in self.specs()]
         opts = _core.options_struct(window_size=self.window_size, no_last=self.flags.no_last,
                                     no_prior=self.flags.no_prior, no_fixed=self.flags.no_fixed, hpa=self.hpa,
                                     placement_order=self.placement_order,
@@ -413,7 +420,7 @@ class DarisRuntime:
         by_model: dict[str, float] = {}
         out = {}
         for t in self.tasks:
-            if t.model not in by_model:
+            if t.key not in by_model:
                 # random co-runners, each task at most `slots` times (one buffer set per concurrent copy)
                 if len(ids) * self.exec.slots < n_slots:
                     raise ValueError(f"AFET calibration needs {n_slots} concurrent jobs but {len(ids)} tasks x "
@@ -423,9 +430,9 @@ class DarisRuntime:
                     c = rng.choice(ids)
                     if slot_tasks.count(c) < self.exec.slots:
                         slot_tasks.append(c)
-                by_model[t.model] = quantize(max(self.exec.busy_calibrate(counts, slot_tasks, seconds),
+                by_model[t.key] = quantize(max(self.exec.busy_calibrate(counts, slot_tasks, seconds),
                                                  2 * QUANTUM))
-            out[t.id] = by_model[t.model]
+            out[t.id] = by_model[t.key]
         self.afet = out
         return out
 

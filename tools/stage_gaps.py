@@ -45,9 +45,10 @@ def main():
         rt.set_rate(rate)
         res = rt.run(args.duration, args.duration * 0.1, full_load=rt.afet)
         per_job = defaultdict(dict)
-        for t in res.trace:
+        gpu_times = rt.exec.trace_gpu()  # aligned with res.trace
+        for t, g in zip(res.trace, gpu_times):
             task, job, stage = t[0], t[1], t[2]
-            per_job[(task, job)][stage] = t
+            per_job[(task, job)][stage] = tuple(t) + tuple(g)
         execs = defaultdict(list)
         gaps = defaultdict(list)
         host_obs = []
