@@ -158,6 +158,8 @@ int daris_task_ids(const daris_handle* h, int32_t* out);               /* sorted
 int daris_task_stage_count(const daris_handle* h, int32_t task_id, int32_t* out);
 int daris_task_info(const daris_handle* h, int32_t task_id, double* period, int32_t* n_stages,
                     int32_t* priority);
+/* Images per job of a task (TaskSpec batch_size; the JPS accounting unit). */
+int daris_task_batch(const daris_handle* h, int32_t task_id, int32_t* batch);
 
 int daris_full_load_sim(daris_handle* h, int32_t task_id, int32_t repetitions, const int32_t* draws,
                         double* out);

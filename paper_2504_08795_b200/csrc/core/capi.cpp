@@ -91,6 +91,10 @@ int daris_task_info(const daris_handle* h, int32_t task_id, double* period, int3
   });
 }
 
+int daris_task_batch(const daris_handle* h, int32_t task_id, int32_t* batch) {
+  return guard(const_cast<daris_handle*>(h), [&] { *batch = h->d->task(task_id).batch; });
+}
+
 int daris_full_load_sim(daris_handle* h, int32_t task_id, int32_t repetitions, const int32_t* draws, double* out) {
   return guard(h, [&] { *out = daris::full_load_time(*h->d, task_id, repetitions, draws); });
 }

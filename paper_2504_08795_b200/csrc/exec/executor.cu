@@ -81,7 +81,7 @@ struct Running {
 };
 
 struct TaskInfo {
-  int id = 0, n_stages = 0, prio = 0;
+  int id = 0, n_stages = 0, prio = 0, batch = 1;
   double period = 0;
 };
 
@@ -461,6 +461,7 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
     TaskInfo& t = info[ids[i]];
     t.id = ids[i];
     daris_task_info(h, t.id, &t.period, &t.n_stages, &t.prio);
+    daris_task_batch(h, t.id, &t.batch);
     if (t.n_stages > c.max_stages) return fail(ex, "task has more stages than the executor supports");
   }
   (void)collect_log;
@@ -723,7 +724,7 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
         if (released >= acc.warmup) {
           const int hp = info[rr.task].prio == DARIS_HP ? 0 : 1;
           acc.cmp[hp]++;
-          acc.inputs += 1;
+          acc.inputs += info[rr.task].batch;  // JPS counts images (engine.py:153-220)
           acc.resp[hp].push_back(t - released);
           if (missed) acc.miss[hp]++;
         }

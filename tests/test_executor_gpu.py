@@ -8,7 +8,7 @@ import torch
 from oracle import stagesim_oracle as O
 from paper_2504_08795_b200.gpu import GpuConfig, Policy
 from paper_2504_08795_b200.model import Priority
-from paper_2504_08795_b200.runtime import DarisRuntime, TaskDef
+from paper_2504_08795_b200.runtime import DarisRuntime, TaskDef, quantize
 
 pytestmark = pytest.mark.gpu
 
@@ -73,4 +73,28 @@ def test_e2e_mode_copies_inputs_and_outputs():
     assert res.stats["copies_h2d"] > 0 and res.stats["copies_d2h"] > 0
     out = rt.host_out[1]
     assert torch.isfinite(out).all() and out.abs().sum() > 0
+    rt.close()
+
+
+def test_batched_jobs_count_images_and_replay():
+    """Tasks whose jobs are batches of images (the reference's batch_size): the
+    report counts images, and the recorded trace replays to the same decisions."""
+    gpu = GpuConfig(148, 2, 2, 1.0, Policy.MPS_STR)
+    tasks = [TaskDef(1, "resnet18", Priority.HP, 150.0, 3, 4), TaskDef(2, "resnet18", Priority.LP, 150.0, 3, 4)]
+    rt = DarisRuntime(tasks, gpu, slots=2)
+    res = rt.run(duration=0.5, warmup=0.05)
+    rep = res.report
+    jobs = rep.completed_hp + rep.completed_lp
+    assert jobs > 0 and rep.missed_hp == 0
+    assert abs(rep.jps * (quantize(0.5) - quantize(0.05)) - 4 * jobs) < 1e-6 * 4 * jobs + 1e-9
+    assert "resnet18@b4" in rt.stage_nominal
+    durations = {(t[0], t[1], t[2]): t[7] - t[6] for t in res.trace}
+    otasks = [{"id": s.id, "period": s.period, "deadline": s.deadline, "hp": s.priority is Priority.HP,
+               "stages": [(p.nominal_time, p.width) for p in s.stages], "batch": 4, "curve": None,
+               "full_load": res.full_load[s.id]} for s in res.tasks]
+    ogpu = {"total_sms": 148, "n_contexts": 2, "n_streams": 2, "oversubscription": 1.0, "policy": "mps-str",
+            "kappa": 0.0}
+    recs, _, _, _ = O.simulate(otasks, ogpu, duration=0.5, warmup_frac=0.1, durations=durations,
+                               phases_override={s.id: ph for s, ph in zip(res.tasks, res.phases)})
+    assert _decisions(res.records, 0.5) == _decisions(recs, 0.5)
     rt.close()
