@@ -60,7 +60,7 @@ class GpuSimulation:
                  flags: AblationFlags = AblationFlags(), mode: SchedulerMode = SchedulerMode(),
                  phasing: str = "random", placement_order: str = "descending_util",
                  edf_on_job_deadline: bool = False, stage_migration: bool = False, slots: int = 3, e2e: bool = False,
-                 calibrate_seconds: float = 0.2, device: int = 0):
+                 calibrate_seconds: float = 0.2, device: int = 0, batch_sizes: dict[int, int] | None = None):
         if flags.no_staging:
             raise InvalidScenario("the gpu backend runs real stage splits; use n_stages=1 instead of "
                                   "the no_staging ablation")
@@ -88,12 +88,13 @@ class GpuSimulation:
         self.e2e = e2e
         self.calibrate_seconds = calibrate_seconds
         self.device = device
+        self.batch_sizes = dict(batch_sizes or {})  # images per job (TaskSpec batch_size)
         self.runtime = None
 
     def build_runtime(self):
         from .runtime import DarisRuntime, TaskDef
         defs = [TaskDef(t.id, self.gpu_tasks[t.id].model, t.priority, 1.0 / t.period,
-                        self.gpu_tasks[t.id].n_stages) for t in self.tasks]
+                        self.gpu_tasks[t.id].n_stages, self.batch_sizes.get(t.id, 1)) for t in self.tasks]
         self.runtime = DarisRuntime(defs, self.config, slots=self.slots, window_size=self.window_size,
                                     flags=self.flags, hpa=self.mode.hpa_enabled,
                                     stage_migration=self.stage_migration, seed=self.seed, e2e=self.e2e,

@@ -44,8 +44,10 @@ def test_gpu_backend_schema():
         S.scenario_from_dict({**base, "backend": "tpu"})
     with pytest.raises(InvalidScenario):      # unet has no network: fail closed, no fallback
         S.scenario_from_dict({**base, "workload": {"preset": "unet"}})
+    cfg = S.scenario_from_dict({**base, "workload": {"preset": "c2_resnet50_b200", "batch_size": 4}})
+    assert set(cfg.batch_sizes.values()) == {4}   # batched jobs run as real batch-4 networks
     with pytest.raises(InvalidScenario):
-        S.scenario_from_dict({**base, "workload": {"preset": "c2_resnet50_b200", "batch_size": 4}})
+        S.scenario_from_dict({**base, "workload": {"preset": "c2_resnet50_b200", "batch_size": 128}})
 
 
 def test_gpu_backend_has_no_cpu_fallback():
