@@ -473,7 +473,7 @@ def ours(args) -> dict | None:
 
     roof = conv_roofline(rt, peaks) if rank == 0 else None
     rt.close()
-    batched = None if args.no_batched else [daris_batched(args, gpu, mine, log, b) for b in (4, 8)]
+    batched = None if args.no_batched else [daris_batched(args, gpu, mine, log, b) for b in (4, 8, 16)]
     batching = batching_baseline() if (rank == 0 and not args.no_batching) else None
     cpu = cpu_reference(args.cpu_seconds) if (rank == 0 and world == 1 and not args.no_cpu) else None
     flops_inf = next(iter(rt.nets.values())).flops_per_image
