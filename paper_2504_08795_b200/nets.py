@@ -18,6 +18,7 @@ buffer set).
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 from typing import Callable
 
@@ -286,7 +287,7 @@ class _Builder:
 
 # the fused pool + classifier launch measured slower than avgpool + linear at batch 1
 # (every block re-pools the whole feature map): opt-in until it is restructured
-POOL_LINEAR = __import__("os").environ.get("DARIS_POOL_LINEAR", "0") == "1"
+POOL_LINEAR = os.environ.get("DARIS_POOL_LINEAR", "0") == "1"
 
 
 def _pool_classifier(b: "_Builder", lin: LinearLayer, x: str, shape, batch: int) -> None:
@@ -608,12 +609,10 @@ def run_op(op: Op, tb: TaskBuffers, stream, sm_budget: int = 0, timestamps=None)
 
 # stage execution mode: "persistent" = one stage-kernel launch per stage
 # (csrc/kernels/stage_tc.cu), "layers" = one launch per op (conv_tc.cu + aux.cu)
-import os as _os
-
-STAGE_MODE = _os.environ.get("DARIS_STAGE_MODE", "layers")
+STAGE_MODE = os.environ.get("DARIS_STAGE_MODE", "layers")
 _BUILD_MODE = STAGE_MODE
 # persistent mode: CTAs per stage kernel (0 = the partition's SM count)
-STAGE_GRID = int(_os.environ.get("DARIS_STAGE_GRID", "0"))
+STAGE_GRID = int(os.environ.get("DARIS_STAGE_GRID", "0"))
 
 
 def stage_ops(net: Network, stage: int, tb: TaskBuffers) -> list:

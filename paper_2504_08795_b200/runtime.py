@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import random
 import time
 from dataclasses import dataclass, field
@@ -279,7 +280,6 @@ class DarisRuntime:
         # Planning for the device's share per concurrent job (x1.25) measured
         # +42 % closed-loop capacity at 4x2 OS=2 and ~2x at 16 streams
         # (tools/capacity_probe.py, profiles/r01_capacity_*). DARIS_PLAN_SMS overrides.
-        import os
         self.partition_sms = min(p["sm_count"] for p in self.exec.partitions)
         share = int(round(1.25 * gpu.total_sms / (gpu.n_contexts * gpu.n_streams)))
         self.sm_budget = int(os.environ.get("DARIS_PLAN_SMS", "0")) or max(8, min(self.partition_sms, share))
