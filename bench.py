@@ -249,9 +249,9 @@ def conv_roofline(rt, peaks) -> dict:
     achieved = flops / t_conv / 1e12
     return {"kernel": "conv_igemm_tc_kernel", "bound": "tensor", "achieved": round(achieved, 3),
             "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_tflops"], 5),
-            "traffic": 1536000, "algorithmic_bytes_per_launch": 1925000,
-            "traffic_note": "dram__bytes_read+write per conv launch, mean over the 53 convs of one forward "
-                            "(81.4 MB / 53; algorithmic weights+in+out+residual 102.0 MB / 53), ncu --set full, "
+            "traffic": 1656000, "algorithmic_bytes_per_launch": 1997000,
+            "traffic_note": "dram__bytes_read+write per conv launch, mean over 46 conv launches of one forward "
+                            "(76.2 MB; algorithmic weights+in+out+residual 91.9 MB), ncu --set full, "
                             "profiles/r01_ncu_full_convs_resnet50_plan23.csv",
             "launches_per_inference": len(conv), "flops_per_launch_avg": flops // len(conv),
             "avg_launch_us": round(t_conv / len(conv) * 1e6, 3), "share_of_inference": round(t_conv / t_all, 4),
