@@ -883,6 +883,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
 
   static bool attr_set = false;  // per template instantiation
   if (!attr_set) {
+    set_max_carveout(reinterpret_cast<const void*>(conv_igemm_tc_kernel<BN, ST, MT>));
     cudaError_t e = cudaFuncSetAttribute(conv_igemm_tc_kernel<BN, ST, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          L::kTotal);
     if (e != cudaSuccess) return e;
@@ -1007,6 +1008,7 @@ static int launch_halo(const daris_conv_desc* d, const daris_conv_plan_t& pl, cu
   const int smem = 1024 + kHaloHS * a.stage_bytes + kHaloWS * 64 * 128 + 1024;
   static int attr_smem = 0;
   if (smem > attr_smem) {
+    set_max_carveout(reinterpret_cast<const void*>(conv_halo_kernel));
     cudaError_t e = cudaFuncSetAttribute(conv_halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr_smem = smem;

@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <utility>
 
 namespace daris {
@@ -240,12 +241,33 @@ __device__ __forceinline__ float2 unpack_bf16x2(uint32_t v) {
   return __bfloat1622float2(b);
 }
 
+// Every kernel of the stage path asks for the maximum shared-memory carveout,
+// so consecutive layers (and other tenants' layers on the same SM) never need
+// a different L1/shared split: a carveout change waits for the SM to drain,
+// which would serialise PDL-overlapped layers and concurrent jobs.
+// DARIS_CARVEOUT=-1 leaves the driver default (experiment knob).
+inline void set_max_carveout(const void* kernel) {
+  static const int carveout = [] {
+    const char* e = std::getenv("DARIS_CARVEOUT");
+    return e ? std::atoi(e) : static_cast<int>(cudaSharedmemCarveoutMaxShared);
+  }();
+  if (carveout >= 0) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+}
+
 // Host: launch with programmatic stream serialization so, in a stream or a
 // captured graph, this kernel may begin while its predecessor drains
 // (kernels call pdl_wait() before touching the predecessor's outputs).
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args&&... args) {
+  static const void* configured[64] = {};  // kernels whose carveout is set (per KArgs instantiation)
+  bool seen = false;
+  for (const void* k : configured) seen = seen || k == reinterpret_cast<const void*>(kernel);
+  if (!seen) {
+    set_max_carveout(reinterpret_cast<const void*>(kernel));
+    for (auto& k : configured)
+      if (!k) { k = reinterpret_cast<const void*>(kernel); break; }
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
