@@ -607,7 +607,7 @@ __global__ void __maxnreg__(112)
 // Activation traffic per channel block drops from 9 boxes to 1, and the
 // weight tiles (8 KB) get a deep ring of their own.
 constexpr int kHaloHS = 2;  // halo stages
-constexpr int kHaloWS = 4;  // weight stages (BN = 64: 8 KB each)
+constexpr int kHaloWSMax = 8;  // weight stages (BN = 64: 8 KB each), a.ws <= this
 
 struct HaloArgs {
   const float* scale;
@@ -615,6 +615,9 @@ struct HaloArgs {
   int cin, cout, h, w, ho, wo, relu;
   int wh, th, tiles_h, cin_blocks, stage_bytes;  // W_h, rows per tile, tiles per image, 64-ch blocks, halo stage
   int bo_mode;        // descriptor base offset for row-shifted A starts: 0 none, 1 (addr >> 7) & 7
+  int ws;             // weight ring depth (8 KB stages)
+  int cb_per_split;   // split-K over channel blocks: a cluster of gridDim.z CTAs, partials reduced over DSMEM
+  __nv_bfloat16* y;   // output (the split path stores its owned rows directly)
   FDiv d_tiles_h;
   unsigned long long* ts;
 };
@@ -635,13 +638,14 @@ __global__ void __maxnreg__(112)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sH = smem;                                   // kHaloHS x stage_bytes
-  uint8_t* sW = smem + kHaloHS * a.stage_bytes;         // kHaloWS x 8 KB
-  uint64_t* hfull = reinterpret_cast<uint64_t*>(sW + kHaloWS * BN * 128);
+  uint8_t* sW = smem + kHaloHS * a.stage_bytes;         // a.ws x 8 KB
+  uint64_t* hfull = reinterpret_cast<uint64_t*>(sW + a.ws * BN * 128);
   uint64_t* hempty = hfull + kHaloHS;
   uint64_t* wfull = hempty + kHaloHS;
-  uint64_t* wempty = wfull + kHaloWS;
-  uint64_t* tmem_full = wempty + kHaloWS;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* wempty = wfull + a.ws;
+  uint64_t* tmem_full = wempty + a.ws;
+  uint64_t* red_bar = tmem_full + 1;  // split-K: this CTA's rows of every split have landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_bar + 1);
   float* s_scale = reinterpret_cast<float*>(tmem_slot + 4);
   float* s_bias = s_scale + BN;
 
@@ -650,14 +654,19 @@ __global__ void __maxnreg__(112)
   const int img = fdiv(tile_m, a.d_tiles_h);
   const int h0 = (tile_m - img * a.tiles_h) * a.th;
   const int n0 = tile_n * BN;
-  const int ncb = a.cin_blocks;
-  unsigned long long* ts = a.ts ? a.ts + 16ull * (blockIdx.x + gridDim.x * blockIdx.y) : nullptr;
+  const int S = gridDim.z, split = blockIdx.z;
+  const int cb_begin = split * a.cb_per_split;
+  const int ncb = min(a.cin_blocks, cb_begin + a.cb_per_split) - cb_begin;
+  const int mvalid = a.th * a.wh;  // tile rows holding output pixels (+ the discarded columns)
+  unsigned long long* ts =
+      a.ts ? a.ts + 16ull * (blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) : nullptr;
   if (ts && threadIdx.x == 0) ts[0] = gtimer();
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kHaloHS; ++i) { mbar_init(&hfull[i], 1); mbar_init(&hempty[i], 1); }
-    for (int i = 0; i < kHaloWS; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }
+    for (int i = 0; i < a.ws; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }
     mbar_init(tmem_full, 1);
+    mbar_init(red_bar, 1);
     fence_barrier_init();
   }
   if (warp == 4) {
@@ -665,7 +674,7 @@ __global__ void __maxnreg__(112)
     if (lane == 0) {
       tma_prefetch_desc(&wmap);
       tma_prefetch_desc(&hmap);
-      tma_prefetch_desc(&ymap);
+      if (S == 1) tma_prefetch_desc(&ymap);
     }
   }
   tc_fence_before();
@@ -679,26 +688,26 @@ __global__ void __maxnreg__(112)
       // K order: channel block cb, then the 9 kernel positions; weight K coordinate
       // of (p, cb) = p * cin + cb * 64 in the [cout][3][3][cin] layout
       const int total = ncb * 9;
-      const int pre = min(total, kHaloWS);
+      const int pre = min(total, a.ws);
       for (int j = 0; j < pre; ++j) {  // weights do not depend on the previous layer
         mbar_arrive_expect_tx(&wfull[j], BN * 128);
-        tma_load_2d(&wmap, &wfull[j], sW + j * (BN * 128), (j % 9) * a.cin + (j / 9) * kBK, n0);
+        tma_load_2d(&wmap, &wfull[j], sW + j * (BN * 128), (j % 9) * a.cin + (cb_begin + j / 9) * kBK, n0);
       }
       pdl_wait();
-      if (ts) ts[2] = gtimer();
+      if (ts) ts[2] = ts[3] = gtimer();
       const uint32_t halo_bytes = static_cast<uint32_t>((a.th + 2) * a.wh * 128);
       for (int cb = 0; cb < ncb; ++cb) {
         const int hs = cb % kHaloHS;
         if (cb >= kHaloHS) mbar_wait(&hempty[hs], ((cb / kHaloHS) & 1) ^ 1);
         mbar_arrive_expect_tx(&hfull[hs], halo_bytes);
-        tma_load_4d(&hmap, &hfull[hs], sH + hs * a.stage_bytes, cb * kBK, -1, h0 - 1, img);
+        tma_load_4d(&hmap, &hfull[hs], sH + hs * a.stage_bytes, (cb_begin + cb) * kBK, -1, h0 - 1, img);
         for (int p = 0; p < 9; ++p) {
           const int j = cb * 9 + p;
           if (j < pre) continue;
-          const int ws = j % kHaloWS;
-          mbar_wait(&wempty[ws], ((j / kHaloWS) & 1) ^ 1);
+          const int ws = j % a.ws;
+          mbar_wait(&wempty[ws], ((j / a.ws) & 1) ^ 1);
           mbar_arrive_expect_tx(&wfull[ws], BN * 128);
-          tma_load_2d(&wmap, &wfull[ws], sW + ws * (BN * 128), p * a.cin + cb * kBK, n0);
+          tma_load_2d(&wmap, &wfull[ws], sW + ws * (BN * 128), p * a.cin + (cb_begin + cb) * kBK, n0);
         }
       }
     }
@@ -711,8 +720,8 @@ __global__ void __maxnreg__(112)
         mbar_wait(&hfull[hs], (cb / kHaloHS) & 1);
         for (int p = 0; p < 9; ++p) {
           const int j = cb * 9 + p;
-          const int ws = j % kHaloWS;
-          mbar_wait(&wfull[ws], (j / kHaloWS) & 1);
+          const int ws = j % a.ws;
+          mbar_wait(&wfull[ws], (j / a.ws) & 1);
           tc_fence_after();
           const int r = p / 3, sx = p - (p / 3) * 3;
           const uint64_t adesc = umma_desc_k_sw128_at(sH_u32 + hs * a.stage_bytes + (r * a.wh + sx) * 128, a.bo_mode);
@@ -738,6 +747,78 @@ __global__ void __maxnreg__(112)
     tc_fence_after();
     if (threadIdx.x == 0) pdl_trigger();
     if (ts && threadIdx.x == 0) ts[4] = gtimer();
+    const int row = warp * 32 + lane;
+    const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
+    if (S > 1) {
+      if (threadIdx.x == 0) {
+        const int r_begin = (split * kBM) / S, r_end = ((split + 1) * kBM) / S;
+        const int valid = max(0, min(r_end, mvalid) - r_begin);
+        mbar_arrive_expect_tx(red_bar, static_cast<uint32_t>(S * valid * BN * 4));
+      }
+    }
+  }
+  if (S > 1) {
+    // split-K over channel blocks inside one cluster (as conv_igemm_tc_kernel): CTA r
+    // owns rows [r*128/S, (r+1)*128/S) and receives those rows of every partial
+    const int rpc_max = (kBM + S - 1) / S;
+    float* recv = reinterpret_cast<float*>(sH);  // [S][rpc_max][BN] fp32 in the idle halo ring
+    __syncwarp();
+    cluster_sync();
+    if (warp < 4) {
+      const int row = warp * 32 + lane;
+      const bool push = row < mvalid;
+      const int owner = ((row + 1) * S - 1) / kBM;
+      const int j = row - (owner * kBM) / S;
+      const uint32_t dst = dsmem_map(smem_u32(recv + (static_cast<size_t>(split) * rpc_max + j) * BN), owner);
+      const uint32_t bar = dsmem_map(smem_u32(red_bar), owner);
+      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
+#pragma unroll
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_row + c0, r);
+        if (push) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            st_async_v4(dst + (c0 + 4 * q) * 4, __uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                        __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]), bar);
+        }
+      }
+    }
+    __syncwarp();
+    cluster_arrive();
+    if (warp < 4) {
+      const int r_begin = (split * kBM) / S, r_end = ((split + 1) * kBM) / S;
+      const int valid = max(0, min(r_end, mvalid) - r_begin);
+      mbar_wait(red_bar, 0);
+      const int items = valid * (BN / 8);
+      for (int it = threadIdx.x; it < items; it += 128) {
+        const int j = it / (BN / 8), g = it % (BN / 8);
+        const int trow = r_begin + j;  // tile row -> output pixel (th rows of W_h, 2 discarded columns)
+        const int oh = h0 + trow / a.wh, ow = trow - (trow / a.wh) * a.wh;
+        if (ow >= a.wo || oh >= a.ho) continue;
+        const int c = g * 8;
+        float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int k = 0; k < S; ++k) {
+          const float4* src = reinterpret_cast<const float4*>(recv + (static_cast<size_t>(k) * rpc_max + j) * BN + c);
+          const float4 p0 = src[0], p1 = src[1];
+          v[0] += p0.x; v[1] += p0.y; v[2] += p0.z; v[3] += p0.w;
+          v[4] += p1.x; v[5] += p1.y; v[6] += p1.z; v[7] += p1.w;
+        }
+        float o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = act_apply(v[e] * s_scale[c + e] + s_bias[c + e], a.relu);
+        uint4 pk;
+        pk.x = pack_bf16x2(o[0], o[1]);
+        pk.y = pack_bf16x2(o[2], o[3]);
+        pk.z = pack_bf16x2(o[4], o[5]);
+        pk.w = pack_bf16x2(o[6], o[7]);
+        const size_t m = (static_cast<size_t>(img) * a.ho + oh) * a.wo + ow;
+        *reinterpret_cast<uint4*>(a.y + m * a.cout + n0 + c) = pk;
+      }
+    }
+    __syncwarp();
+    cluster_wait();
+  } else if (warp < 4) {
     const int row = warp * 32 + lane;
     const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
     uint8_t* stage = sH;  // the halo ring is idle once the accumulator is complete
@@ -1005,7 +1086,16 @@ static int launch_halo(const daris_conv_desc* d, const daris_conv_plan_t& pl, cu
     return e ? std::atoi(e) : 0;
   }();
   a.bo_mode = bo_mode;
-  const int smem = 1024 + kHaloHS * a.stage_bytes + kHaloWS * 64 * 128 + 1024;
+  a.cb_per_split = pl.kb_per_split;  // halo plan: K units are 64-channel blocks
+  a.y = static_cast<__nv_bfloat16*>(d->y);
+  // weight ring depth: 4 x 8 KB (8 measured no faster — the mainloop is not bound
+  // by bytes in flight — and costs co-residency); DARIS_HALO_WS overrides
+  static const int ws_env = [] {
+    const char* e = std::getenv("DARIS_HALO_WS");
+    return e ? std::atoi(e) : 0;
+  }();
+  a.ws = ws_env > 0 ? std::min(ws_env, kHaloWSMax) : 4;
+  const int smem = 1024 + kHaloHS * a.stage_bytes + a.ws * 64 * 128 + 1024;
   static int attr_smem = 0;
   if (smem > attr_smem) {
     set_max_carveout(reinterpret_cast<const void*>(conv_halo_kernel));
@@ -1014,15 +1104,22 @@ static int launch_halo(const daris_conv_desc* d, const daris_conv_plan_t& pl, cu
     attr_smem = smem;
   }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(pl.tiles_m, pl.tiles_n, 1);
+  cfg.gridDim = dim3(pl.tiles_m, pl.tiles_n, pl.splits);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (pl.splits > 1) {
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 1;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = pl.splits;
+    cfg.numAttrs = 2;
+  }
   return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_halo_kernel, wmap, hmap, ymap, a));
 }
 
@@ -1133,19 +1230,25 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
     return e ? std::atoi(e) : 1;
   }();
   out->halo = 0;
-  if (halo_mode > 0 && (splits == 1 || halo_mode == 2) && d->kh == 3 && d->kw == 3 && d->stride == 1 && d->pad == 1 && d->cin % kBK == 0 &&
+  const bool clusters_ok = (d->flags & DARIS_CONV_CLUSTER_SPLITK) != 0;
+  if (halo_mode > 0 && (splits == 1 || clusters_ok || halo_mode == 2) && d->kh == 3 && d->kw == 3 && d->stride == 1 && d->pad == 1 && d->cin % kBK == 0 &&
       d->cout % 64 == 0 && !d->residual && !dual && !padded && d->wo + 2 <= kBM && d->h == d->ho && d->w == d->wo) {
     const int wh = d->wo + 2;
     const int thh = std::max(1, std::min(d->ho, kBM / wh));
+    // split-K over 64-channel blocks where the regular plan splits (clusters <= 8 CTAs)
+    const int ncb = d->cin / kBK;
+    int hs = (splits > 1 && clusters_ok) ? std::min(std::min(splits, ncb), 8) : 1;
+    const int cbps = (ncb + hs - 1) / hs;
+    hs = (ncb + cbps - 1) / cbps;
     out->halo = 1;
     out->block_n = 64;
-    out->splits = 1;
-    out->kb_per_split = num_kb;
+    out->splits = hs;
+    out->kb_per_split = cbps;  // in channel blocks
     out->tma_rows = thh;
     out->tiles_m = d->n * ((d->ho + thh - 1) / thh);
     out->tiles_n = d->cout / 64;
-    out->ctas = out->tiles_m * out->tiles_n;
-    out->cluster = 1;
+    out->ctas = out->tiles_m * out->tiles_n * hs;
+    out->cluster = hs;
     out->m_sub = 1;
     out->workspace_floats = 0;
     out->counters = 0;

@@ -283,8 +283,9 @@ def test_conv_256_row_tiles(n, hw, cin, cout, k, stride, residual):
     assert r.returncode == 0, r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("cluster", [False, True])
 @pytest.mark.parametrize("n,hw,c", [(1, 56, 64), (1, 28, 128), (1, 14, 256), (1, 7, 512), (2, 14, 256), (3, 7, 128)])
-def test_conv3x3_halo_mode(n, hw, c):
+def test_conv3x3_halo_mode(n, hw, c, cluster):
     """conv_halo_kernel (DARIS_CONV_HALO=1): 3x3/s1/p1 with the nine kernel
     positions read from one halo tile per channel block through shifted UMMA
     descriptors; same numerics as the per-position TMA path."""
@@ -294,9 +295,10 @@ def test_conv3x3_halo_mode(n, hw, c):
     root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
     code = (f"import sys; sys.path[:0] = [{root!r}, {root + '/tests'!r}]; import test_kernels_gpu as T; "
             "from paper_2504_08795_b200 import kernels as K; "
-            f"d = K.conv_desc(({n}, {hw}, {hw}, {c}), {c}, 3, 3, 1, 1, sm_budget=23); "
-            "assert K.conv_plan(d).halo == 1; "
-            f"T._conv_case({n}, {hw}, {hw}, {c}, {c}, 3, 1, 1, sm_budget=23, seed={hw + c})")
+            f"d = K.conv_desc(({n}, {hw}, {hw}, {c}), {c}, 3, 3, 1, 1, sm_budget=23, cluster={cluster}); "
+            "p = K.conv_plan(d); assert p.halo == 1; "
+            f"assert {cluster} or p.splits == 1; "
+            f"T._conv_case({n}, {hw}, {hw}, {c}, {c}, 3, 1, 1, sm_budget=23, seed={hw + c}, cluster={cluster})")
     env = dict(os.environ, DARIS_CONV_HALO="2")  # halo kernel even where the regular plan splits K
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
