@@ -2,6 +2,7 @@
 // depthwise conv and the small-batch linear (weight-streaming GEMV).
 // All use 16-byte vector accesses along the contiguous NHWC channel axis.
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cstdint>
 #include "sm100.cuh"

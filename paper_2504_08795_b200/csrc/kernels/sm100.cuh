@@ -241,11 +241,11 @@ __device__ __forceinline__ float2 unpack_bf16x2(uint32_t v) {
   return __bfloat1622float2(b);
 }
 
-// Every kernel of the stage path asks for the maximum shared-memory carveout,
-// so consecutive layers (and other tenants' layers on the same SM) never need
-// a different L1/shared split: a carveout change waits for the SM to drain,
-// which would serialise PDL-overlapped layers and concurrent jobs.
-// DARIS_CARVEOUT=-1 leaves the driver default (experiment knob).
+// The tcgen05 conv kernels ask for the maximum shared-memory carveout (they
+// live in shared memory; measured neutral vs the driver default). Not the aux
+// kernels: they use no shared memory and need L1 — the classifier GEMV re-reads
+// its input vector per warp, and with a max-shared carveout VGG-16's FC1 ran at
+// 445 GB/s instead of streaming at HBM speed. DARIS_CARVEOUT=-1: driver default.
 inline void set_max_carveout(const void* kernel) {
   static const int carveout = [] {
     const char* e = std::getenv("DARIS_CARVEOUT");
@@ -260,14 +260,7 @@ inline void set_max_carveout(const void* kernel) {
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args&&... args) {
-  static const void* configured[64] = {};  // kernels whose carveout is set (per KArgs instantiation)
-  bool seen = false;
-  for (const void* k : configured) seen = seen || k == reinterpret_cast<const void*>(kernel);
-  if (!seen) {
-    set_max_carveout(reinterpret_cast<const void*>(kernel));
-    for (auto& k : configured)
-      if (!k) { k = reinterpret_cast<const void*>(kernel); break; }
-  }
+
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

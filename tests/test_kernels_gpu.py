@@ -302,3 +302,22 @@ def test_conv3x3_halo_mode(n, hw, c, cluster):
     env = dict(os.environ, DARIS_CONV_HALO="2")  # halo kernel even where the regular plan splits K
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("batch,k,o,x_bf16,relu", [(1, 25088, 4096, False, 1), (3, 25088, 300, False, 0),
+                                                  (1, 4104, 1000, True, 1), (4, 8192, 777, True, 0)])
+def test_linear_wide_k(batch, k, o, x_bf16, relu):
+    """linear_wide_kernel (K > 4096: VGG's classifier): the input staged in shared
+    memory per K tile, weight rows streamed, first tile prefetched before the wait."""
+    from paper_2504_08795_b200 import kernels as K
+    dev = torch.device("cuda")
+    g = torch.Generator().manual_seed(k + o)
+    x = torch.randn(batch, k, generator=g)
+    if x_bf16:
+        x = x.bfloat16()
+    w = (torch.randn(o, k, generator=g) / k ** 0.5).bfloat16()
+    bias = torch.randn(o, generator=g)
+    y = K.linear(x.to(dev), w.to(dev), bias.to(dev), relu=relu)
+    torch.cuda.synchronize()
+    ref = x.float() @ w.float().t() + bias
+    _close(y, ref.clamp_min(0) if relu else ref)
