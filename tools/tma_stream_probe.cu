@@ -1,0 +1,103 @@
+// Per-SM streaming rate of bulk TMA copies (global -> shared) as a function of
+// bytes in flight: G CTAs (one per SM), each streams `per_cta` bytes through a
+// ring of S stages of B bytes (one elected thread issues cp.async.bulk, the
+// consumer only waits and re-arms). L2-resident (8 MB buffer, re-read) vs
+// HBM (1 GB buffer). Answers: is ~40 GB/s per CTA (the conv mainloops) a
+// hardware limit or a pipeline-depth limit?
+//
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/tma_stream_probe.bin tools/tma_stream_probe.cu
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__global__ void stream_kernel(const uint8_t* __restrict__ src, size_t span, size_t per_cta, int S, int B,
+                              unsigned long long* cycles_out) {
+  extern __shared__ __align__(1024) uint8_t ring[];
+  __shared__ uint64_t full[16], empty[16];
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[i])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  const size_t n = per_cta / B;
+  const size_t base = (static_cast<size_t>(blockIdx.x) * per_cta) % span;
+  long long t0 = 0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  if (tid == 0) {  // producer
+    for (size_t i = 0; i < n; ++i) {
+      const int s = static_cast<int>(i % S);
+      if (i >= static_cast<size_t>(S)) {
+        const uint32_t par = static_cast<uint32_t>(((i / S) & 1) ^ 1);
+        asm volatile(
+            "{\n\t.reg .pred p;\nW1_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W1_%=;\n\t}" ::"r"(
+                smem_u32(&empty[s])),
+            "r"(par));
+      }
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[s])), "r"(B));
+      const uint8_t* g = src + (base + i * B) % span;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(ring + s * B)),
+                   "l"(g), "r"(B), "r"(smem_u32(&full[s]))
+                   : "memory");
+    }
+  } else if (tid == 32) {  // consumer
+    for (size_t i = 0; i < n; ++i) {
+      const int s = static_cast<int>(i % S);
+      const uint32_t par = static_cast<uint32_t>((i / S) & 1);
+      asm volatile(
+          "{\n\t.reg .pred p;\nW2_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W2_%=;\n\t}" ::"r"(
+              smem_u32(&full[s])),
+          "r"(par));
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[s])));
+    }
+    long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    cycles_out[blockIdx.x] = static_cast<unsigned long long>(t1 - t0);
+  }
+}
+
+int main() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const size_t big = size_t(1) << 30, small = size_t(8) << 20;
+  uint8_t* buf;
+  cudaMalloc(&buf, big);
+  cudaMemset(buf, 1, big);
+  unsigned long long* ns;
+  cudaMalloc(&ns, 1024 * sizeof(unsigned long long));
+  cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  printf("span  ctas stages stage_KB inflight_KB  per_cta_GBps  total_GBps\n");
+  for (size_t span : {small, big}) {
+    for (int G : {1, 24, sms}) {
+      for (int B : {8192, 16384, 32768}) {
+        for (int S : {2, 4, 8}) {
+          if (S * B > 192 * 1024) continue;
+          const size_t per_cta = (span == small) ? (size_t(4) << 20) : (size_t(6) << 20);
+          stream_kernel<<<G, 64, S * B>>>(buf, span, per_cta, S, B, ns);  // warm
+          stream_kernel<<<G, 64, S * B>>>(buf, span, per_cta, S, B, ns);
+          cudaDeviceSynchronize();
+          unsigned long long h[1024];
+          cudaMemcpy(h, ns, G * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+          double mx = 0, sum = 0;
+          for (int i = 0; i < G; ++i) {
+            mx = h[i] > mx ? h[i] : mx;
+            sum += per_cta / (h[i] * 1e-9) / 1e9;
+          }
+          printf("%s %4d %6d %8d %11d %13.1f %11.1f\n", span == small ? "L2 " : "HBM", G, S, B / 1024, S * B / 1024,
+                 sum / G, G * per_cta / (mx * 1e-9) / 1e9);
+        }
+      }
+    }
+  }
+  cudaError_t e = cudaGetLastError();
+  printf("status: %s\n", cudaGetErrorString(e));
+  return 0;
+}
