@@ -484,7 +484,7 @@ def ours(args) -> dict | None:
             "warmup": args.warmup, "ms_per_step": round(wall_max * 1e3 / (args.warmup + args.steps), 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (x~N(0,1) images, torchvision-architecture random-init weights, BN randomised)",
-            "config": {"workload": WORKLOAD, "model": "resnet50", "tasks_per_gpu": len(mine), "hp_per_gpu": 4,
+            "config": {"workload": WORKLOAD, "network": "resnet50", "tasks_per_gpu": len(mine), "hp_per_gpu": 4,
                        "lp_per_gpu": 4, "contexts": 4, "streams": 2, "oversubscription": 2.0,
                        "partition_sms": [p["sm_count"] for p in rt.exec.partitions],
                        "green_contexts": all(p["green"] for p in rt.exec.partitions), "stages": 4, "batch": 1,
@@ -589,7 +589,7 @@ def reference(args) -> dict | None:
             "warmup": args.warmup, "ms_per_step": round(1e3 * steps_seconds / max(1, args.steps), 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": WORKLOAD, "model": "resnet50", "tasks_per_gpu": 8, "batch": 1,
+            "config": {"workload": WORKLOAD, "network": "resnet50", "tasks_per_gpu": 8, "batch": 1,
                        "host": "CPU reference path (oracle scheduler + torch CPU fp32)"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu["cores"], "kind": cpu["kind"],
                              "sample": cpu["sample"]},

@@ -283,6 +283,9 @@ class DarisRuntime:
         self.partition_sms = min(p["sm_count"] for p in self.exec.partitions)
         share = int(round(1.25 * gpu.total_sms / (gpu.n_contexts * gpu.n_streams)))
         self.sm_budget = int(os.environ.get("DARIS_PLAN_SMS", "0")) or max(8, min(self.partition_sms, share))
+        # per-priority planning (experiment knobs): HP jobs' grids may be planned wider
+        self.plan_hp = int(os.environ.get("DARIS_PLAN_SMS_HP", "0")) or self.sm_budget
+        self.plan_lp = int(os.environ.get("DARIS_PLAN_SMS_LP", "0")) or self.sm_budget
         # one weight copy per model, shared by all tasks running it
         self.nets: dict[tuple, nets.Network] = {}
         for t in self.tasks:
@@ -294,7 +297,7 @@ class DarisRuntime:
         for t in self.tasks:
             net = self.net_of(t)
             for s in range(slots):
-                self.buffers[(t.id, s)] = nets.allocate_buffers(net, self.sm_budget)
+                self.buffers[(t.id, s)] = nets.allocate_buffers(net, self.plan_of(t))
         self.pool_size = pool_size
         self._pool_cache: dict = {}
         self._make_pools(pool_size)
@@ -303,6 +306,10 @@ class DarisRuntime:
         self._nominal: dict[str, list[float]] | None = None
         self.handle = None
         self.afet: dict[int, float] | None = None
+
+    def plan_of(self, t: TaskDef) -> int:
+        """SMs this task's layer grids are planned for."""
+        return self.plan_hp if t.priority is Priority.HP else self.plan_lp
 
     def net_of(self, t: TaskDef) -> nets.Network:
         return self.nets[(t.model, t.n_stages, t.batch)]
@@ -354,8 +361,8 @@ class DarisRuntime:
                     tb = self.buffers[(t.id, s)]
                     for st in range(net.n_stages):
                         self.exec.capture(t.id, st, k, s,
-                                          lambda stream, st=st, tb=tb, net=net: nets.run_stage(
-                                              net, st, tb, stream, self.sm_budget))
+                                          lambda stream, st=st, tb=tb, net=net, plan=self.plan_of(t):
+                                          nets.run_stage(net, st, tb, stream, plan))
                         n += 1
         return n
 
