@@ -83,6 +83,7 @@ struct ConvArgs {
   int kb_seg1;        // K blocks of the primary input; blocks >= kb_seg1 come from x2 (DARIS_CONV_DUAL)
   int stride2;        // x2 sampling stride
   int box_rows;       // rows of one output/residual TMA box
+  int plain_push;     // cluster split-K: plain remote stores + cluster barrier instead of st.async + mbarrier
   unsigned long long* ts;  // optional per-CTA phase timestamps (globaltimer ns), 16 per CTA
   FDiv d_howo, d_wo, d_kw, d_cinb, d_tiles_h;
 };
@@ -529,19 +530,30 @@ __global__ void __maxnreg__(112)
         uint32_t r[32];
         tmem_ld_32x32b_x32(t_row + c0, r);  // warp-collective (.sync.aligned): every lane loads
         if (push) {
+          if (a.plain_push) {
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            st_async_v4(dst + (c0 + 4 * q) * 4, __uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                        __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]), bar);
+            for (int q = 0; q < 8; ++q)
+              st_cluster_v4(dst + (c0 + 4 * q) * 4, __uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                            __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              st_async_v4(dst + (c0 + 4 * q) * 4, __uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                          __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]), bar);
+          }
         }
       }
     }
     __syncwarp();
-    cluster_arrive();  // (released before exit: no CTA leaves while peers may still push to it)
+    if (a.plain_push) {
+      cluster_sync();  // every partial row has landed in its owner (release/acquire)
+    } else {
+      cluster_arrive();  // (released before exit: no CTA leaves while peers may still push to it)
+    }
     if (warp < 4) {
       const int r_begin = (split * kBM) / S, r_end = ((split + 1) * kBM) / S;
       const int valid = max(0, min(r_end, mvalid) - r_begin);
-      mbar_wait(red_bar, 0);
+      if (!a.plain_push) mbar_wait(red_bar, 0);
       if (ts && threadIdx.x == 0) ts[10] = gtimer();
       float* s_scale = reinterpret_cast<float*>(smem + L::kEpiOff);
       float* s_bias = s_scale + BN;
@@ -583,7 +595,7 @@ __global__ void __maxnreg__(112)
     }
     __syncwarp();
     if (ts && threadIdx.x == 0) ts[11] = gtimer();
-    cluster_wait();
+    if (!a.plain_push) cluster_wait();
   }
   if (ts && threadIdx.x == 0) ts[5] = gtimer();
   tc_fence_before();
@@ -996,6 +1008,11 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   a.cluster_split = pl.cluster > 1 ? 1 : 0;
   a.tma_a = pl.tma_rows > 0 ? 1 : 0;
   a.tma_c = tma_c ? 1 : 0;
+  static const bool plain_push = [] {  // experiment knob (A/B against st.async + mbarrier)
+    const char* e = std::getenv("DARIS_SPLIT_PLAIN");
+    return e && std::atoi(e) != 0;
+  }();
+  a.plain_push = plain_push ? 1 : 0;
   a.stem_tma = stem_tma ? 1 : 0;
   a.box_rows = box_rows;
   a.th = pl.tma_rows > 0 ? pl.tma_rows : 1;

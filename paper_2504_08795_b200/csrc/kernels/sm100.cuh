@@ -86,6 +86,13 @@ __device__ __forceinline__ void st_async_v4(uint32_t remote_addr, float a, float
                "f"(a), "f"(b), "f"(c), "f"(d), "r"(remote_mbar)
                : "memory");
 }
+// Plain (weak) 16-B store into a cluster peer's shared memory; visibility comes
+// from a later barrier.cluster arrive.release / wait.acquire.
+__device__ __forceinline__ void st_cluster_v4(uint32_t remote_addr, float a, float b, float c, float d) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(remote_addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
 // Bulk DMA of `bytes` (multiple of 16) from this CTA's smem to a cluster peer's
 // smem, completing as complete_tx on the peer's mbarrier (dst/mbar from dsmem_map).
 __device__ __forceinline__ void bulk_copy_to_peer(uint32_t remote_dst, uint32_t local_src, uint32_t bytes,
