@@ -1216,11 +1216,16 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
   // once for twice the rows. Measured slower at batch 1 (ResNet-50 at 24 SMs
   // 0.44 vs 0.37 ms isolated, 13.9k vs 15.6k inf/s loaded capacity: the lost
   // parallelism costs more than the per-CTA overheads saved) — opt-in, DARIS_M256=1
-  static const bool no_m256 = std::getenv("DARIS_M256") == nullptr ||
-                              std::getenv("DARIS_NO_TMA_STORE") != nullptr;
+  // DARIS_M256=1: everywhere; DARIS_M256=stem: the 8-channel stem only
+  static const int m256_mode = [] {
+    const char* e = std::getenv("DARIS_M256");
+    if (!e || std::getenv("DARIS_NO_TMA_STORE")) return 0;
+    return std::strcmp(e, "stem") == 0 ? 2 : 1;
+  }();
+  const bool m256_here = m256_mode == 1 || (m256_mode == 2 && padded);
   int m_sub = 1;
   int th_used = th, tiles_m_used = tiles_m;
-  if (!no_m256 && tma_a && splits == 1 && bn <= 128 && tiles > budget) {
+  if (m256_here && tma_a && splits == 1 && bn <= 128 && tiles > budget) {
     const int th2 = std::max(1, std::min(d->ho, 2 * kBM / d->wo));
     if (th2 * d->wo > kBM && th2 * d->stride <= 256 && (!dual || th2 * d->stride2 <= 256)) {
       m_sub = 2;
