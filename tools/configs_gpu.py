@@ -6,7 +6,8 @@
           migration off vs on
   c4      OS in {1,1.5,2,3} x contexts {2,4,8} x streams {1,2,4} (OS <= contexts) for the C2 task
           set (8 ResNet-50, 4 HP / 4 LP): knee inferences/s per cell
-  tasks   C5 per GPU: ResNet-50 task count {8,12,16,24} at 4x2 OS=2, knee per count
+  tasks   ResNet-50 task count {8,12,16,24} at 4x2 OS=2, knee per count
+  c5      C5 on one GPU: task count raised at a fixed per-task rate until the first HP miss
 
 Every knee uses bench.py's search (HP miss = 0, LP DMR < 2 %) and its GPU-stall
 re-measure rule. One JSON object per cell on stdout.
@@ -158,14 +159,39 @@ def task_scaling(args):
         rt.close()
 
 
+def c5(args):
+    """BASELINE config 5 on one GPU: the C2 mix (half HP, half LP) at a fixed
+    per-task rate, task count raised until the first HP deadline miss (or LP
+    loss >= 2 %); the last feasible count is this GPU's share of the box."""
+    gpu = GpuConfig(148, 4, 2, 2.0, Policy.MPS_STR)
+    rate = args.c5_rate
+    last_ok = None
+    for n in range(8, 65, 4):
+        rt = DarisRuntime(bench.c2_tasks(rate, list(range(n))), gpu, slots=3, seed=0)
+        rt.capture_all()
+        rt.afet = rt.calibrate_full_load(0.2)
+        res = bench.run_clean(rt, 1.5, 0.15, log, f"c5 n={n}")[0]
+        ok = bench.feasible(res.report)
+        row = {"config": "c5", "tasks": n, "rate_per_task": rate, **summary(res.report)}
+        log(f"c5 tasks={n} ok={ok} {summary(res.report)}")
+        rt.close()
+        if not ok:
+            emit({**row, "first_failing": True, "max_feasible_tasks": last_ok["tasks"] if last_ok else 0,
+                  "max_feasible_jps": last_ok["jps"] if last_ok else 0.0})
+            return
+        last_ok = row
+        emit(row)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", nargs="+", choices=["c1", "c3", "c4", "tasks"])
+    ap.add_argument("which", nargs="+", choices=["c1", "c3", "c4", "tasks", "c5"])
+    ap.add_argument("--c5-rate", type=float, default=500.0, help="per-task JPS for the c5 task-count scan")
     ap.add_argument("--probe-seconds", type=float, default=0.6)
     ap.add_argument("--c4-cells", default="")
     args = ap.parse_args()
     for w in args.which:
-        {"c1": c1, "c3": c3, "c4": c4, "tasks": task_scaling}[w](args)
+        {"c1": c1, "c3": c3, "c4": c4, "tasks": task_scaling, "c5": c5}[w](args)
 
 
 if __name__ == "__main__":
