@@ -109,7 +109,7 @@ def c3(args):
         for t in rt.tasks:
             per_model.setdefault(t.model, 0.0)
             per_model[t.model] += t.rate
-        flops = {m: rt.nets[(m, stages[m])].flops_per_image for m in models}
+        flops = {m: rt.nets[(m, stages[m], 1)].flops_per_image for m in models}
         tflops = sum(per_model[m] * flops[m] for m in models) / 1e12
         emit({"config": "c3", "stage_migration": mig, "knee_factor": round(f, 4),
               "isolated_ms": {m: round(v * 1e3, 3) for m, v in iso.items()},
