@@ -1180,7 +1180,11 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
   const int tiles_m = tma_a ? d->n * tiles_h : (M + kBM - 1) / kBM;
   int bn = d->block_n;
   if (bn == 0) {
-    bn = (d->cout % 128 == 0) ? 128 : 64;
+    static const int bn_max = [] {  // experiment knob: widest automatic tile
+      const char* e = std::getenv("DARIS_CONV_BN_MAX");
+      return e ? std::atoi(e) : 128;
+    }();
+    bn = (d->cout % 128 == 0 && bn_max >= 128) ? 128 : 64;
     // prefer narrower tiles when the grid would not cover the partition
     if (bn == 128 && tiles_m * (d->cout / 128) < budget) bn = 64;
   }
