@@ -217,7 +217,8 @@ int daris_trace_run(daris_handle* h, double duration, double warmup_frac, const 
     std::unordered_map<long long, double> m;
     m.reserve(static_cast<size_t>(n_trace) * 2 + 1);
     for (int64_t i = 0; i < n_trace; ++i)
-      m[(static_cast<long long>(trace[i].job) << 8) | static_cast<long long>(trace[i].stage)] = trace[i].duration;
+      m[(static_cast<long long>(trace[i].task) << 40) | (static_cast<long long>(trace[i].job) << 8) |
+        static_cast<long long>(trace[i].stage)] = trace[i].duration;
     h->d->collect_log = collect_log != 0;
     daris::sim_run(*h->d, duration, warmup_frac, phases, out, &m);
   });

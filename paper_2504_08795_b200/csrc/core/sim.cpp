@@ -334,7 +334,9 @@ void sim_run(Dispatcher& d, double duration, double warmup_frac, const double* p
       if (trace) {
         work_buf.resize(spec.work.size());
         for (size_t j = 0; j < spec.work.size(); ++j) {
-          const long long key = (static_cast<long long>(job_counter) << 8) | static_cast<long long>(j);
+          // keyed (task, job, stage) like the recorded trace and the reference shim
+          const long long key = (static_cast<long long>(tid) << 40) | (static_cast<long long>(job_counter) << 8) |
+                                static_cast<long long>(j);
           auto it = trace->find(key);
           // jobs the recorded run rejected never execute: any placeholder works
           work_buf[j] = it == trace->end() ? spec.work[j] : it->second;

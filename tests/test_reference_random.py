@@ -82,3 +82,58 @@ def test_native_equals_reference_on_random_instances(block):
         assert got[1] == want[1], f"instance {k}: admission audits differ"
         assert got[2] == want[2], f"instance {k}: reports differ"
         assert got[3] == want[3], f"instance {k}: AFET values differ"
+
+
+def _trace_instance(rng):
+    nc, ns, sms, os_, tasks, _ = _instance(rng)
+    tasks = [(tid, period, hp, stages) for tid, period, hp, stages, _, _ in tasks]
+    # per-(task, job, stage) durations, like a recorded GPU trace; jobs are numbered
+    # globally in release order, so cover every job id the run can reach
+    durations = {}
+    for job in range(1, 800):
+        for tid, _, _, stages in tasks:
+            for j, (nom, _) in enumerate(stages):
+                durations[(tid, job, j)] = round(nom * rng.uniform(0.6, 2.5), 9)
+    full = {tid: round(sum(n for n, _ in st) * rng.uniform(1.0, 2.0), 9) for tid, _, _, st in tasks}
+    return nc, ns, sms, os_, tasks, durations, full
+
+
+@pytest.mark.parametrize("block", range(4))
+def test_trace_replay_equals_reference_on_random_traces(block, monkeypatch):
+    """P2's replay engine: fixed per-stage durations and given AFETs
+    through this package's native trace engine vs the unmodified reference with
+    the trace shim (unit rates, traced stage work, traced AFETs)."""
+    import paper_2504_08795_b200 as ours
+    ref = _ref()
+    import stagesim.engine as E
+    from stagesim.gpu import RateAllocation
+
+    per = 50
+    for k in range(block * per, (block + 1) * per):
+        rng = random.Random(40_000 + k)
+        nc, ns, sms, os_, tasks, durations, full = _trace_instance(rng)
+        orig_make_job = E.make_job
+
+        def traced_make_job(task, release_time, tracker, _orig=orig_make_job, **kw):
+            job = _orig(task, release_time, tracker, **kw)
+            for st in job.stage_jobs:
+                st.remaining_work = durations[(job.task_id, job.job_id, st.stage_index)]
+            return job
+
+        monkeypatch.setattr(E, "make_job", traced_make_job)
+        monkeypatch.setattr(E, "allocate_rates",
+                            lambda active, config: RateAllocation([0.0] * len(active), [1.0] * len(active), 1.0, {}))
+        monkeypatch.setattr(E.Simulation, "_measure_full_load", lambda self, eff: {t.id: full[t.id] for t in eff})
+
+        def specs(mod):
+            return [mod.TaskSpec.periodic(tid, period, mod.Priority.HP if hp else mod.Priority.LP,
+                                          tuple(mod.StageProfile(n, w) for n, w in st))
+                    for tid, period, hp, st in tasks]
+
+        ref_res = ref.Simulation(specs(ref), ref.GpuConfig(sms, nc, ns, os_, ref.Policy.MPS_STR), seed=k,
+                                 duration=0.2).run()
+        monkeypatch.undo()
+        ours_res = ours.Simulation(specs(ours), ours.GpuConfig(sms, nc, ns, os_, ours.Policy.MPS_STR), seed=k,
+                                   duration=0.2).run_trace(durations, full)
+        assert [tuple(r) for r in ours_res.records] == [tuple(r) for r in ref_res.records], f"trace {k}"
+        assert ours_res.report.to_dict() == ref_res.report.to_dict(), f"trace {k}"
