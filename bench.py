@@ -246,17 +246,41 @@ def conv_roofline(rt, peaks) -> dict:
     t_conv = sum(t for _, t in conv)
     t_all = sum(t for _, t in per_op)
     flops = sum(op.flops for op, _ in conv)
-    achieved = flops / t_conv / 1e12
-    return {"kernel": "conv_igemm_tc_kernel", "bound": "tensor", "achieved": round(achieved, 3),
-            "peak": peaks["bf16_tflops"], "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_tflops"], 5),
-            "traffic": 1656000, "algorithmic_bytes_per_launch": 1997000,
+    nbytes = sum(conv_algorithmic_bytes(op) for op, _ in conv)
+    ai = flops / nbytes
+    ridge = peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    gbs = nbytes / t_conv / 1e9
+    tflops = flops / t_conv / 1e12
+    n = len(conv)
+    return {"kernel": "conv_igemm_tc_kernel", "bound": "hbm" if ai < ridge else "tensor",
+            "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(gbs / peaks["hbm_gbs"], 5),
+            "traffic": 1656000, "algorithmic_bytes_per_launch": nbytes // n,
+            "arithmetic_intensity_flop_per_byte": round(ai, 1), "ridge_flop_per_byte": round(ridge, 1),
+            "tensor_view": {"achieved": round(tflops, 3), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                            "frac": round(tflops / peaks["bf16_tflops"], 5)},
+            "frac_of_sm_share": round(gbs / (peaks["hbm_gbs"] * rt.sm_budget / 148), 4),
             "traffic_note": "dram__bytes_read+write per conv launch, mean over 46 conv launches of one forward "
                             "(76.2 MB; algorithmic weights+in+out+residual 91.9 MB), ncu --set full, "
                             "profiles/r01_ncu_full_convs_resnet50_plan23.csv",
-            "launches_per_inference": len(conv), "flops_per_launch_avg": flops // len(conv),
-            "avg_launch_us": round(t_conv / len(conv) * 1e6, 3), "share_of_inference": round(t_conv / t_all, 4),
+            "algorithmic_bytes_note": "per launch: bf16 weights + input + output (+ residual / fused-branch input), "
+                                      "each read or written once",
+            "launches_per_inference": n, "flops_per_launch_avg": flops // n,
+            "avg_launch_us": round(t_conv / n * 1e6, 3), "share_of_inference": round(t_conv / t_all, 4),
             "partition_sms": rt.partition_sms, "plan_sms": rt.sm_budget,
-            "peak_kind": f"bf16 dense burst ({peaks['source']})"}
+            "peak_kind": f"HBM copy bandwidth ({peaks['source']}); frac_of_sm_share scales it by plan_sms/148"}
+
+
+def conv_algorithmic_bytes(op) -> int:
+    """Minimum HBM bytes of one conv launch: weights + input + output, plus the
+    residual or the fused 1x1 branch's input (bf16, each touched once)."""
+    import math
+    n = op.layer.weight.numel() + math.prod(op.shape_in) + math.prod(op.shape_out)
+    if op.shape_in2:
+        n += math.prod(op.shape_in2)
+    elif op.res:
+        n += math.prod(op.shape_out)
+    return 2 * n
 
 
 def batching_baseline(batches=(1, 2, 4, 8, 16, 32, 64), reps: int = 20) -> dict:

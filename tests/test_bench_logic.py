@@ -81,3 +81,17 @@ def test_reference_arm_prints_the_contract_line():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_conv_algorithmic_bytes_resnet50():
+    """The roofline's algorithmic bytes: every conv's weights + input + output
+    (+ residual / fused branch input) once; ResNet-50 b1 convs sit below the
+    B200 ridge point, so the roofline that bounds them is HBM."""
+    import torch
+    from paper_2504_08795_b200 import nets
+    net = nets.build_network("resnet50", batch=1, n_stages=4, device=torch.device("cpu"))
+    convs = [op for op in net.ops if op.kind == "conv"]
+    nbytes = sum(bench.conv_algorithmic_bytes(op) for op in convs)
+    wbytes = sum(op.layer.weight.numel() * 2 for op in convs)
+    assert wbytes < nbytes < wbytes + 60e6
+    assert sum(op.flops for op in convs) / nbytes < 1642e12 / 6547.8e9
