@@ -38,6 +38,7 @@ struct Driver {
   PFN_cuGreenCtxDestroy_v12040 greenDestroy = nullptr;
   PFN_cuGreenCtxStreamCreate_v12050 greenStream = nullptr;
   PFN_cuDeviceGet_v2000 deviceGet = nullptr;
+  PFN_cuStreamWriteValue32_v11070 writeValue32 = nullptr;  // optional: completion flags
   bool ok = false;
 };
 
@@ -60,6 +61,7 @@ Driver& driver() {
            entry("cuDevResourceGenerateDesc", d.genDesc) && entry("cuGreenCtxCreate", d.greenCreate) &&
            entry("cuGreenCtxDestroy", d.greenDestroy) && entry("cuGreenCtxStreamCreate", d.greenStream) &&
            entry("cuDeviceGet", d.deviceGet);
+    if (!entry("cuStreamWriteValue32", d.writeValue32)) d.writeValue32 = nullptr;
   }
   return d;
 }
@@ -110,6 +112,11 @@ struct daris_exec {
   std::string err;
   int64_t graph_count = 0;
   double stall_threshold = 1e-3;
+  // DARIS_EXEC_FLAGS=1: stage completion as a stream memory write of a sequence
+  // number into host-mapped memory (one word per (context, stream) slot), polled
+  // with a plain load instead of cudaEventQuery
+  uint32_t* flags = nullptr;
+  CUdeviceptr flags_dev = 0;
 
   size_t gidx(int task, int stage, int ctx, int slot) const {
     return ((static_cast<size_t>(task - 1) * cfg.max_stages + stage) * cfg.n_contexts + (ctx - 1)) *
@@ -304,6 +311,7 @@ void daris_exec_destroy(daris_exec* ex) {
   for (auto g : ex->graphs)
     if (g) cudaGraphExecDestroy(g);
   for (auto e : ex->slot_free) cudaEventDestroy(e);
+  if (ex->flags) cudaFreeHost(ex->flags);
   for (auto& p : ex->parts) {
     for (auto e : p.done) cudaEventDestroy(e);
     for (auto s : p.streams) cudaStreamDestroy(s);
@@ -533,6 +541,20 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
   job_seq.reserve(1024);
   std::vector<std::vector<Running>> run(c.n_contexts, std::vector<Running>(c.n_streams));
   int job_counter = 0;
+  const char* fe = std::getenv("DARIS_EXEC_FLAGS");
+  const bool use_flags = fe && fe[0] == '1' && driver().writeValue32;
+  std::vector<uint32_t> flag_seq(static_cast<size_t>(c.n_contexts * c.n_streams), 0);
+  if (use_flags) {
+    if (!ex->flags) {
+      void* hp = nullptr;
+      CUDA_TRY(ex, cudaHostAlloc(&hp, flag_seq.size() * sizeof(uint32_t), cudaHostAllocMapped | cudaHostAllocPortable));
+      ex->flags = static_cast<uint32_t*>(hp);
+      void* dp = nullptr;
+      CUDA_TRY(ex, cudaHostGetDevicePointer(&dp, hp, 0));
+      ex->flags_dev = reinterpret_cast<CUdeviceptr>(dp);
+    }
+    for (size_t i = 0; i < flag_seq.size(); ++i) flag_seq[i] = ex->flags[i];
+  }
   int in_flight = 0;
 
   auto launch = [&](const daris_stage_ref& r) -> int {
@@ -582,7 +604,14 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
       }
       CUDA_TRY(ex, cudaEventRecord(ex->slot_free[si], s));
     }
-    CUDA_TRY(ex, cudaEventRecord(p.done[r.stream], s));
+    if (use_flags) {
+      const size_t fi = static_cast<size_t>((r.context - 1) * c.n_streams + r.stream);
+      if (driver().writeValue32(reinterpret_cast<CUstream>(s), ex->flags_dev + fi * sizeof(uint32_t), ++flag_seq[fi],
+                                CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+        return fail(ex, "cuStreamWriteValue32 failed", DARIS_E_INTERNAL);
+    } else {
+      CUDA_TRY(ex, cudaEventRecord(p.done[r.stream], s));
+    }
     Running& rr = run[r.context - 1][r.stream];
     rr.busy = true;
     rr.task = r.task;
@@ -687,7 +716,19 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
         Running& rr = run[k][s];
         if (!rr.busy) continue;
         st.polls++;
-        cudaError_t q = cudaEventQuery(ex->parts[k].done[s]);
+        cudaError_t q;
+        if (use_flags) {
+          const size_t fi = static_cast<size_t>(k * c.n_streams + s);
+          q = *reinterpret_cast<volatile uint32_t*>(ex->flags + fi) == flag_seq[fi] ? cudaSuccess : cudaErrorNotReady;
+          // a faulted stage never writes its flag: surface the error during a stall
+          if (q != cudaSuccess && in_stall) {
+            cudaError_t e = cudaStreamQuery(run[k][s].task && info[run[k][s].task].prio == DARIS_HP
+                                                ? ex->parts[k].streams_hi[s] : ex->parts[k].streams[s]);
+            if (e != cudaSuccess && e != cudaErrorNotReady) q = e;
+          }
+        } else {
+          q = cudaEventQuery(ex->parts[k].done[s]);
+        }
         if (q == cudaSuccess) {
           done.push_back({k + 1, s, rr.job, rr.stage});
           last_progress = raw_now;

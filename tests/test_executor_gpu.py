@@ -40,8 +40,11 @@ def _decisions(records, horizon):
     return keep
 
 
-@pytest.mark.parametrize("model", ["resnet18", "resnet50"])
-def test_real_run_and_trace_replay_parity(model):
+@pytest.mark.parametrize("model,flags", [("resnet18", "0"), ("resnet50", "0"), ("resnet50", "1")])
+def test_real_run_and_trace_replay_parity(model, flags, monkeypatch):
+    """flags=1: stage completions observed through host-mapped flags written by
+    cuStreamWriteValue32 (DARIS_EXEC_FLAGS=1) instead of event polling."""
+    monkeypatch.setenv("DARIS_EXEC_FLAGS", flags)
     rt = _runtime(model=model, rate=150.0)
     res = rt.run(duration=1.0, warmup=0.1)
     rep = res.report
