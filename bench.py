@@ -516,7 +516,9 @@ def ours(args) -> dict | None:
                        "l2": "inputs larger than L2: each job copies a distinct image from 64-image per-task "
                              "pools (8 x 64 x 602 KB = 308 MB per GPU)",
                        "timing": "host steady clock over the periodic schedule, barrier + synchronize both "
-                                 "sides, max over ranks; stage completions via CUDA events"},
+                                 "sides, max over ranks; stage completions via "
+                                 + ("host-mapped flags (cuStreamWriteValue32)"
+                                    if os.environ.get("DARIS_EXEC_FLAGS", "") == "1" else "CUDA event polling")},
             "constraints_met": bool(constraints_met),
             "hp_miss": int(tot[1]), "dmr_lp": (tot[2] / tot[4]) if tot[4] else 0.0,
             "lp_loss": round(lp_loss(rep), 5),
