@@ -65,10 +65,13 @@ def _cut(records, horizon):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("preset,rate", [("c1_b200", 200.0), ("c3_b200", 250.0)])
+@pytest.mark.parametrize("preset,rate", [("c1_b200", 200.0), ("c3_b200", 250.0), ("c2_b200", 1500.0)])
 def test_gpu_scenario_runs_and_replays(preset, rate):
+    """c2_b200 at 1500 JPS/task is BASELINE config C2 at full size near its knee
+    (8 ResNet-50 tasks, 4x2 contexts/streams, OS 2: ~7k stage decisions/0.6 s)."""
     cfg = S.scenario_from_dict({"preset": preset, "backend": "gpu", "duration": 0.6,
                                 "workload": {"preset": {"c1_b200": "c1_resnet18_b200",
+                                                        "c2_b200": "c2_resnet50_b200",
                                                         "c3_b200": "c3_mixed_b200"}[preset]}})
     # one rate for every task so the run is light enough for any box
     from dataclasses import replace
