@@ -488,6 +488,8 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
       }
   }
   ex->trace.clear();
+  // every buffer set is idle between runs (each run ends with a device sync)
+  std::fill(ex->slot_owner.begin(), ex->slot_owner.end(), 0);
   daris_exec_stats st{};
   Acc acc;
   acc.warmup = warmup;
@@ -747,6 +749,15 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
       Running& rr = run[d.ctx - 1][d.stream];
       double t = now;
       if (t <= rr.start) t = rr.start + kQuantum;  // a stage always takes at least one quantum
+      if (t > duration) {
+        // past the horizon the reference's event loop has ended (SIM_END at
+        // `duration`, engine.py:508-531): the stage drains on the GPU but is
+        // neither logged, traced, counted nor followed by another dispatch
+        rr.busy = false;
+        in_flight--;
+        progressed = true;
+        continue;
+      }
       int32_t job_done = 0, missed = 0;
       int rc = daris_complete(h, d.job, d.stage, t, &job_done, &missed);
       if (rc != DARIS_OK) {
@@ -779,6 +790,7 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
     }
     if (status != DARIS_OK) break;
     if (heap.empty() && in_flight == 0) {
+      if (now > duration) break;
       int32_t ready = 0;
       daris_ready_total(h, &ready);
       if (ready == 0) break;
