@@ -752,7 +752,10 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
       if (t > duration) {
         // past the horizon the reference's event loop has ended (SIM_END at
         // `duration`, engine.py:508-531): the stage drains on the GPU but is
-        // neither logged, traced, counted nor followed by another dispatch
+        // neither logged, counted nor followed by another dispatch; its
+        // duration stays in the trace so a replay also finishes it late
+        ex->trace.push_back(daris_stage_trace{rr.task, rr.job, rr.stage, d.ctx, d.stream, rr.slot, rr.start, t,
+                                              static_cast<double>(rr.ev), NAN});
         rr.busy = false;
         in_flight--;
         progressed = true;
