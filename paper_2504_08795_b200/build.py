@@ -68,7 +68,8 @@ def build_gpu(force: bool = False) -> Path:
             obj = LIB / (src.stem + ".o")
             cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                    "-Xcompiler", "-ffp-contract=off", "--expt-relaxed-constexpr",
-                   f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(src), "-o", str(obj)]
+                   f"-I{INCLUDE}", f"-I{CSRC}", *os.environ.get("DARIS_NVCC_EXTRA", "").split(),
+                   "-c", str(src), "-o", str(obj)]
             _run(cmd)
             objs.append(str(obj))
         cmd = [NVCC, *ARCH, "-shared", "--cudart", "shared", "-o", str(out), *objs, f"-L{LIB}", "-ldaris_core",

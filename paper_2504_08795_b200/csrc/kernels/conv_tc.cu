@@ -38,6 +38,14 @@ namespace daris {
 constexpr int kBM = 128;
 constexpr int kBK = 64;            // bf16 elements per K block = 128 B rows
 constexpr int kThreads = 192;
+// Register cap of the conv kernels. Registers are split over the SM's four
+// sub-partitions (16K each) and a 6-warp CTA puts 2 warps on two of them: at
+// 112 regs/thread a sub-partition holds 4 warps -> 2 CTAs per SM; at 96 it
+// holds 5 -> 3 CTAs per SM (shared memory allows 3 at BN <= 128). ptxas spills
+// 16 B at 96 (a stack slot in L1).
+#ifndef DARIS_CONV_MAXNREG
+#define DARIS_CONV_MAXNREG 96
+#endif
 // Pipeline depth per tile width: shallow rings keep smem per CTA small so three
 // CTAs (of different tenants' kernels) fit on one SM — at batch 1 the layers
 // are latency-bound and co-residency, not pipeline depth, sets throughput.
@@ -156,7 +164,7 @@ __device__ __forceinline__ void finalize_row32(const ConvArgs& a, int m, int col
 }
 
 template <int BN, int ST, int MT>
-__global__ void __maxnreg__(112)
+__global__ void __maxnreg__(DARIS_CONV_MAXNREG)
     conv_igemm_tc_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
                          const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap amap2,
                          const ConvArgs a) {
@@ -178,7 +186,12 @@ __global__ void __maxnreg__(112)
   const int lane = threadIdx.x & 31;
   const int tile_m = blockIdx.x, tile_n = blockIdx.y, split = blockIdx.z;
   unsigned long long* ts = a.ts ? a.ts + 16ull * (blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) : nullptr;
-  if (ts && threadIdx.x == 0) ts[0] = gtimer();
+  if (ts && threadIdx.x == 0) {
+    ts[0] = gtimer();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    ts[15] = smid;
+  }
   // M tile -> first output pixel m0 and number of valid rows. Gather mode: 128
   // consecutive flattened pixels. TMA mode: th whole output rows of one image
   // (th * wo <= 128 rows; the rest of the 128-row MMA tile is ignored).
@@ -643,7 +656,7 @@ __device__ __forceinline__ uint64_t umma_desc_k_sw128_at(uint32_t smem_addr, int
   return bo_mode ? (d | (static_cast<uint64_t>((smem_addr >> 7) & 7) << 49)) : d;
 }
 
-__global__ void __maxnreg__(112)
+__global__ void __maxnreg__(DARIS_CONV_MAXNREG)
     conv_halo_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap hmap,
                      const __grid_constant__ CUtensorMap ymap, const HaloArgs a) {
   constexpr int BN = 64;
@@ -981,6 +994,24 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
                                          L::kTotal);
     if (e != cudaSuccess) return e;
     attr_set = true;
+    if (std::getenv("DARIS_PRINT_OCC")) {  // diagnostics: resident CTAs per SM for this instantiation
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, conv_igemm_tc_kernel<BN, ST, MT>, kThreads, L::kTotal);
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, conv_igemm_tc_kernel<BN, ST, MT>);
+      std::fprintf(stderr, "conv_igemm_tc_kernel<%d,%d,%d>: %d CTAs/SM (smem %d B dyn + %zu static, %d regs)\n", BN, ST,
+                   MT, occ, L::kTotal, fa.sharedSizeBytes, fa.numRegs);
+      for (int sm : {0, 16384, 32768, 49152, 65536, 70000, 100000}) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, conv_igemm_tc_kernel<BN, ST, MT>, kThreads, sm);
+        std::fprintf(stderr, "   dyn smem %d: %d CTAs/SM\n", sm, occ);
+      }
+      int carve = -1, maxdyn = -1;
+      cudaFuncGetAttributes(&fa, conv_igemm_tc_kernel<BN, ST, MT>);
+      carve = fa.preferredShmemCarveout;
+      maxdyn = fa.maxDynamicSharedSizeBytes;
+      std::fprintf(stderr, "   carveout attr %d, max dyn %d, maxThreads %d, localBytes %zu\n", carve, maxdyn,
+                   fa.maxThreadsPerBlock, fa.localSizeBytes);
+    }
   }
   ConvArgs a;
   a.x = static_cast<const __nv_bfloat16*>(d->x);

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--model", default="resnet50")
     ap.add_argument("--sms", type=int, default=74)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--dump", nargs="*", default=[], help="layer names whose per-CTA stamps to print")
     args = ap.parse_args()
     ex = Executor(max(1, 148 // args.sms), 1, args.sms, slots=1, max_tasks=1, max_stages=8)
     net = nets.build_network(args.model, batch=1)
@@ -70,6 +71,7 @@ def main():
     for i, op in enumerate(net.ops):
         if op.kind != "conv":
             continue
+        raw_sm = ts[i].view(-1, 16)[:, 15].cpu().tolist()
         a = ts[i].view(-1, 16).cpu().double()
         if t_origin is None:
             t_origin = a[:, 0].min().item()
@@ -95,6 +97,13 @@ def main():
                                  statistics.median((a[:, 11] - a[:, 10]).tolist()),
                                  statistics.median((a[:, 5] - a[:, 11]).tolist()),
                                  statistics.median((a[:, 8] - a[:, 4]).tolist())]
+        if op.layer.name in args.dump:
+            print(f"--- {op.layer.name}: per CTA (us from the layer's first release): sm start released "
+                  f"prod_done acc_ready epi_done exit")
+            order = sorted(range(a.shape[0]), key=lambda c: a[c, 0].item())
+            for c in order:
+                print(f"  cta {c:3d} sm {int(raw_sm[c]):3d} " + " ".join(
+                    f"{a[c, k].item() - released:7.2f}" for k in (0, 2, 3, 4, 5, 6)))
         prev_end = end
         rows.append(row)
     total = rows[-1]["end"] - rows[0]["released"]
