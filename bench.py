@@ -262,7 +262,7 @@ def conv_roofline(rt, peaks) -> dict:
             "frac_of_sm_share": round(gbs / (peaks["hbm_gbs"] * rt.sm_budget / 148), 4),
             "traffic_note": "dram__bytes_read+write per conv launch, mean over 46 conv launches of one forward "
                             "(76.2 MB; algorithmic weights+in+out+residual 91.9 MB), ncu --set full, "
-                            "profiles/r01_ncu_full_convs_resnet50_plan23.csv",
+                            "profiles/r01_ncu_full_convs_resnet50_plan23_regcap96.csv",
             "algorithmic_bytes_note": "per launch: bf16 weights + input + output (+ residual / fused-branch input), "
                                       "each read or written once",
             "launches_per_inference": n, "flops_per_launch_avg": flops // n,
