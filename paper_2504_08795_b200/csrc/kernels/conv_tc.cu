@@ -1279,12 +1279,16 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
   out->m_sub = m_sub;
   out->cluster = (splits > 1 && bn == 64 && (d->flags & DARIS_CONV_CLUSTER_SPLITK)) ? splits : 1;
   out->tma_rows = tma_a ? th_used : 0;
-  // 3x3 / stride 1 / pad 1 from a halo tile (see conv_halo_kernel) where the regular
-  // plan does not split K (the halo kernel has no split-K); DARIS_CONV_HALO=0: off,
-  // DARIS_CONV_HALO=2: also where the regular plan would split
+  // 3x3 / stride 1 / pad 1 from a halo tile (see conv_halo_kernel). Opt-in:
+  // DARIS_CONV_HALO=1 where the regular plan does not split K (or clusters are
+  // allowed), 2: everywhere. Off by default since the register cap admits 3
+  // implicit-GEMM CTAs per SM while a halo CTA's ring (82-98 KB) admits 2:
+  // isolated forwards tie (414.6 us at 24 SMs either way) but loaded capacity is
+  // higher without it (4x2: 15.2k vs 14.9k, 16 jobs: 21.5k vs 20.2k inf/s,
+  // profiles/r01_halo_ab.jsonl)
   static const int halo_mode = [] {
     const char* e = std::getenv("DARIS_CONV_HALO");
-    return e ? std::atoi(e) : 1;
+    return e ? std::atoi(e) : 0;
   }();
   out->halo = 0;
   const bool clusters_ok = (d->flags & DARIS_CONV_CLUSTER_SPLITK) != 0;
