@@ -49,7 +49,10 @@ constexpr int kThreads = 192;
 // Pipeline depth per tile width: shallow rings keep smem per CTA small so three
 // CTAs (of different tenants' kernels) fit on one SM — at batch 1 the layers
 // are latency-bound and co-residency, not pipeline depth, sets throughput.
-template <int BN> struct Depth { static constexpr int kStages = 3; };
+#ifndef DARIS_BN64_STAGES
+#define DARIS_BN64_STAGES 3
+#endif
+template <int BN> struct Depth { static constexpr int kStages = DARIS_BN64_STAGES; };
 template <> struct Depth<128> { static constexpr int kStages = 2; };
 template <> struct Depth<256> { static constexpr int kStages = 2; };
 
