@@ -6,6 +6,7 @@ back in cell-major order and are identical to a sequential run."""
 from __future__ import annotations
 
 import json
+import multiprocessing
 from concurrent.futures import ProcessPoolExecutor
 from dataclasses import dataclass, field, replace
 from pathlib import Path
@@ -171,7 +172,9 @@ def run_sweep(spec: SweepSpec, base: ScenarioConfig, *, collect_log: bool = Fals
     jobs = [(base, c, s, collect_log) for c in cells for s in spec.seeds]
     out = SweepOutcome(skipped=skipped)
     if processes > 1 and len(jobs) > 1:
-        with ProcessPoolExecutor(max_workers=processes) as pool:
+        # spawn, not fork: the parent may hold threads (torch, the native
+        # library) and a forked child could inherit a held lock
+        with ProcessPoolExecutor(max_workers=processes, mp_context=multiprocessing.get_context("spawn")) as pool:
             results = list(pool.map(_run_cell, jobs))
     else:
         results = [_run_cell(j) for j in jobs]
