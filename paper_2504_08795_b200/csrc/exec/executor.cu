@@ -107,6 +107,7 @@ struct daris_exec {
   };
   std::vector<Pool> pools;
   std::vector<cudaEvent_t> slot_free;  // per (task, slot)
+  std::vector<cudaEvent_t> in_ready;   // per (task, slot): the job's input copy is done
   std::vector<int> slot_owner;          // job id using the buffer set, 0 = free
   std::vector<daris_stage_trace> trace;
   std::string err;
@@ -294,12 +295,14 @@ int daris_exec_create(const daris_exec_config* cfg, daris_exec** out, char* err,
   ex->dev_out.assign(ns, nullptr);
   ex->slot_owner.assign(ns, 0);
   ex->slot_free.resize(ns);
-  for (auto& e : ex->slot_free) {
-    if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
-      ex->err = "event creation failed";
-      return bail(DARIS_E_INTERNAL);
+  ex->in_ready.resize(ns);
+  for (auto* v : {&ex->slot_free, &ex->in_ready})
+    for (auto& e : *v) {
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) {
+        ex->err = "event creation failed";
+        return bail(DARIS_E_INTERNAL);
+      }
     }
-  }
   ex->pools.resize(cfg->max_tasks);
   *out = ex.release();
   return DARIS_OK;
@@ -311,6 +314,7 @@ void daris_exec_destroy(daris_exec* ex) {
   for (auto g : ex->graphs)
     if (g) cudaGraphExecDestroy(g);
   for (auto e : ex->slot_free) cudaEventDestroy(e);
+  for (auto e : ex->in_ready) cudaEventDestroy(e);
   if (ex->flags) cudaFreeHost(ex->flags);
   for (auto& p : ex->parts) {
     for (auto e : p.done) cudaEventDestroy(e);
@@ -559,6 +563,50 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
   }
   int in_flight = 0;
 
+  // A job's input (one image or batch from the task's pool) is copied into its
+  // buffer set when the job is admitted — the moment its data exists — on a
+  // copy stream per context, so the transfer overlaps the job's wait for a
+  // stream slot; stage 0 then waits on the copy's event on the GPU.
+  std::vector<cudaStream_t> copy_streams(c.n_contexts, nullptr);
+  {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    for (auto& cs : copy_streams) CUDA_TRY(ex, cudaStreamCreateWithPriority(&cs, cudaStreamNonBlocking, hi));
+  }
+  struct StreamsGuard {
+    std::vector<cudaStream_t>& v;
+    ~StreamsGuard() {
+      cudaDeviceSynchronize();
+      for (auto cs : v)
+        if (cs) cudaStreamDestroy(cs);
+    }
+  } copy_guard{copy_streams};
+  std::unordered_map<int, int> staged_in;  // admitted jobs whose input copy is issued (stage 0 not yet launched)
+  staged_in.reserve(1024);
+  auto stage_input = [&](int task, int job, int context) -> int {
+    const auto& pool = ex->pools[task - 1];
+    const size_t si = ex->sidx(task, job_slot[job]);
+    if (!(pool.src && pool.n > 0 && ex->dev_in[si])) return DARIS_OK;
+    cudaStream_t cs = copy_streams[context - 1];
+    const int owner = ex->slot_owner[si];
+    if (owner != 0 && owner != job) {  // the buffer set's previous job may still be reading it
+      CUDA_TRY(ex, cudaStreamWaitEvent(cs, ex->slot_free[si], 0));
+      st.slot_waits++;
+    }
+    ex->slot_owner[si] = job;
+    const char* src = pool.src + static_cast<int64_t>(job_seq[job] % pool.n) * pool.in_bytes;
+    CUDA_TRY(ex, cudaMemcpyAsync(ex->dev_in[si], src, static_cast<size_t>(pool.in_bytes),
+                                 pool.on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, cs));
+    CUDA_TRY(ex, cudaEventRecord(ex->in_ready[si], cs));
+    staged_in[job] = 1;
+    if (pool.on_host) {
+      st.copies_h2d++;
+      st.h2d_bytes += pool.in_bytes;
+    } else {
+      st.copies_d2d++;
+    }
+    return DARIS_OK;
+  };
   auto launch = [&](const daris_stage_ref& r) -> int {
     Partition& p = ex->parts[r.context - 1];
     const TaskInfo& t = info[r.task];
@@ -566,24 +614,14 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
     const int slot = job_slot[r.job];
     const size_t si = ex->sidx(r.task, slot);
     if (r.stage == 0) {
-      const int owner = ex->slot_owner[si];
-      if (owner != 0 && owner != r.job) {
+      if (staged_in.count(r.job)) {
+        CUDA_TRY(ex, cudaStreamWaitEvent(s, ex->in_ready[si], 0));
+        staged_in.erase(r.job);
+      } else if (ex->slot_owner[si] != 0 && ex->slot_owner[si] != r.job) {
         CUDA_TRY(ex, cudaStreamWaitEvent(s, ex->slot_free[si], 0));
         st.slot_waits++;
       }
       ex->slot_owner[si] = r.job;
-      const auto& pool = ex->pools[r.task - 1];
-      if (pool.src && pool.n > 0 && ex->dev_in[si]) {
-        const char* src = pool.src + static_cast<int64_t>(job_seq[r.job] % pool.n) * pool.in_bytes;
-        CUDA_TRY(ex, cudaMemcpyAsync(ex->dev_in[si], src, static_cast<size_t>(pool.in_bytes),
-                                     pool.on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
-        if (pool.on_host) {
-          st.copies_h2d++;
-          st.h2d_bytes += pool.in_bytes;
-        } else {
-          st.copies_d2d++;
-        }
-      }
     }
     cudaGraphExec_t g = ex->graphs[ex->gidx(r.task, r.stage, r.context, slot)];
     if (!g) return fail(ex, "no graph for dispatched stage", DARIS_E_INTERNAL);
@@ -701,6 +739,8 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
         job_slot[job_counter] = static_cast<int>(seq[tid] % c.slots_per_task);
         job_seq[job_counter] = static_cast<int>(seq[tid]);
         job_rel[job_counter] = tr;
+        status = stage_input(tid, job_counter, pl.context);
+        if (status != DARIS_OK) break;
       }
       seq[tid] += 1;
       rel_idx[tid] += 1;
