@@ -583,7 +583,10 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
   } copy_guard{copy_streams};
   std::unordered_map<int, int> staged_in;  // admitted jobs whose input copy is issued (stage 0 not yet launched)
   staged_in.reserve(1024);
+  const char* sie = std::getenv("DARIS_STAGE_INPUT");  // 0: copy at stage-0 dispatch on the stage's stream
+  const bool input_at_admission = !(sie && sie[0] == '0');
   auto stage_input = [&](int task, int job, int context) -> int {
+    if (!input_at_admission) return DARIS_OK;
     const auto& pool = ex->pools[task - 1];
     const size_t si = ex->sidx(task, job_slot[job]);
     if (!(pool.src && pool.n > 0 && ex->dev_in[si])) return DARIS_OK;
@@ -617,9 +620,23 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
       if (staged_in.count(r.job)) {
         CUDA_TRY(ex, cudaStreamWaitEvent(s, ex->in_ready[si], 0));
         staged_in.erase(r.job);
-      } else if (ex->slot_owner[si] != 0 && ex->slot_owner[si] != r.job) {
-        CUDA_TRY(ex, cudaStreamWaitEvent(s, ex->slot_free[si], 0));
-        st.slot_waits++;
+      } else {
+        if (ex->slot_owner[si] != 0 && ex->slot_owner[si] != r.job) {
+          CUDA_TRY(ex, cudaStreamWaitEvent(s, ex->slot_free[si], 0));
+          st.slot_waits++;
+        }
+        const auto& pool = ex->pools[r.task - 1];
+        if (!input_at_admission && pool.src && pool.n > 0 && ex->dev_in[si]) {
+          const char* src = pool.src + static_cast<int64_t>(job_seq[r.job] % pool.n) * pool.in_bytes;
+          CUDA_TRY(ex, cudaMemcpyAsync(ex->dev_in[si], src, static_cast<size_t>(pool.in_bytes),
+                                       pool.on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, s));
+          if (pool.on_host) {
+            st.copies_h2d++;
+            st.h2d_bytes += pool.in_bytes;
+          } else {
+            st.copies_d2d++;
+          }
+        }
       }
       ex->slot_owner[si] = r.job;
     }
