@@ -1219,8 +1219,11 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
       return e ? std::atoi(e) : 128;
     }();
     bn = (d->cout % 128 == 0 && bn_max >= 128) ? 128 : 64;
-    // prefer narrower tiles when the grid would not cover the partition
-    if (bn == 128 && tiles_m * (d->cout / 128) < budget) bn = 64;
+    // 128-wide tiles only when their grid fills every resident CTA slot of the
+    // planned SMs (3 per SM); otherwise twice the 64-wide CTAs, each with half
+    // the epilogue, finish sooner (batch 1, planned 23 SMs: loaded capacity
+    // 15.3k -> 15.7k inf/s at 4x2, 21.5k -> 22.8k at 16 jobs; profiles/r01_bnmax_ab.jsonl)
+    if (bn == 128 && tiles_m * (d->cout / 128) < 3 * budget) bn = 64;
   }
   if (bn != 64 && bn != 128 && bn != 256) return DARIS_K_BAD_SHAPE;
   if (d->cout % bn != 0) return DARIS_K_BAD_SHAPE;
