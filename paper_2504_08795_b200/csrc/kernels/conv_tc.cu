@@ -1223,7 +1223,15 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
     // planned SMs (3 per SM); otherwise twice the 64-wide CTAs, each with half
     // the epilogue, finish sooner (batch 1, planned 23 SMs: loaded capacity
     // 15.3k -> 15.7k inf/s at 4x2, 21.5k -> 22.8k at 16 jobs; profiles/r01_bnmax_ab.jsonl)
-    if (bn == 128 && tiles_m * (d->cout / 128) < 3 * budget) bn = 64;
+    // DARIS_BN_RULE=0: the earlier rule (narrow only below one CTA per SM);
+    // 2: additionally keep 128 when the 64-wide grid would overflow the slots
+    static const int bn_rule = [] {
+      const char* e = std::getenv("DARIS_BN_RULE");
+      return e ? std::atoi(e) : 1;
+    }();
+    const int t128 = tiles_m * (d->cout / 128), t64 = 2 * t128;
+    if (bn == 128 && (bn_rule == 0 ? t128 < budget : t128 < 3 * budget && (bn_rule != 2 || t64 <= 3 * budget)))
+      bn = 64;
   }
   if (bn != 64 && bn != 128 && bn != 256) return DARIS_K_BAD_SHAPE;
   if (d->cout % bn != 0) return DARIS_K_BAD_SHAPE;
