@@ -1219,15 +1219,16 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
       return e ? std::atoi(e) : 128;
     }();
     bn = (d->cout % 128 == 0 && bn_max >= 128) ? 128 : 64;
-    // 128-wide tiles only when their grid fills every resident CTA slot of the
-    // planned SMs (3 per SM); otherwise twice the 64-wide CTAs, each with half
-    // the epilogue, finish sooner (batch 1, planned 23 SMs: loaded capacity
-    // 15.3k -> 15.7k inf/s at 4x2, 21.5k -> 22.8k at 16 jobs; profiles/r01_bnmax_ab.jsonl)
+    // 64-wide tiles when the 128-wide grid leaves resident CTA slots of the
+    // planned SMs idle (3 per SM) and the 64-wide grid still fits in them:
+    // twice the CTAs, each with half the epilogue, finish sooner. Batch 1 at 23
+    // planned SMs: loaded capacity 15.2k -> 15.6k inf/s at 4x2, 21.5k -> 22.7k at
+    // 16 jobs; large batches keep their 128-wide plans (profiles/r01_bn_rule_ab.txt).
     // DARIS_BN_RULE=0: the earlier rule (narrow only below one CTA per SM);
-    // 2: additionally keep 128 when the 64-wide grid would overflow the slots
+    // 1: narrow whenever the 128-wide grid is below 3 CTAs per SM
     static const int bn_rule = [] {
       const char* e = std::getenv("DARIS_BN_RULE");
-      return e ? std::atoi(e) : 1;
+      return e ? std::atoi(e) : 2;
     }();
     const int t128 = tiles_m * (d->cout / 128), t64 = 2 * t128;
     if (bn == 128 && (bn_rule == 0 ? t128 < budget : t128 < 3 * budget && (bn_rule != 2 || t64 <= 3 * budget)))
