@@ -255,14 +255,14 @@ def conv_roofline(rt, peaks) -> dict:
     return {"kernel": "conv_igemm_tc_kernel", "bound": "hbm" if ai < ridge else "tensor",
             "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": round(gbs / peaks["hbm_gbs"], 5),
-            "traffic": 1656000, "algorithmic_bytes_per_launch": nbytes // n,
+            "traffic": 1662737, "algorithmic_bytes_per_launch": nbytes // n,
             "arithmetic_intensity_flop_per_byte": round(ai, 1), "ridge_flop_per_byte": round(ridge, 1),
             "tensor_view": {"achieved": round(tflops, 3), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
                             "frac": round(tflops / peaks["bf16_tflops"], 5)},
             "frac_of_sm_share": round(gbs / (peaks["hbm_gbs"] * rt.sm_budget / 148), 4),
             "traffic_note": "dram__bytes_read+write per conv launch, mean over 46 conv launches of one forward "
-                            "(76.2 MB; algorithmic weights+in+out+residual 91.9 MB), ncu --set full, "
-                            "profiles/r01_ncu_full_convs_resnet50_plan23_regcap96.csv",
+                            "(76.5 MB; algorithmic weights+in+out+residual 91.9 MB), ncu --set full, "
+                            "profiles/r01_ncu_full_convs_resnet50_plan23_final.csv",
             "algorithmic_bytes_note": "per launch: bf16 weights + input + output (+ residual / fused-branch input), "
                                       "each read or written once",
             "launches_per_inference": n, "flops_per_launch_avg": flops // n,
