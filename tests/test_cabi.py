@@ -62,3 +62,20 @@ def test_py_sum_matches_cpython_builtin():
         arr = (ctypes.c_double * max(1, n))(*[float(v) for v in vals])
         fl = (ctypes.c_int32 * max(1, n))(*flags)
         assert L.daris_py_sum(arr, fl, n) == float(sum(vals)), vals
+
+
+def test_conv_tile_width_rule():
+    """daris_conv_plan (host-only): 64-wide tiles when the 128-wide grid leaves
+    resident CTA slots (3 per planned SM) idle and the 64-wide grid fits in them;
+    128-wide otherwise (large batches keep their plans)."""
+    from paper_2504_08795_b200 import kernels as K
+
+    def bn(shape, cout, k, budget):
+        return K.conv_plan(K.conv_desc(shape, cout, k, k, 1, k // 2, sm_budget=budget)).block_n
+
+    # 7 M tiles x 4 = 28 < 3*23 and 56 <= 69 -> 64 wide
+    assert bn((1, 28, 28, 128), 512, 1, 23) == 64
+    # 28 x 2 = 56 < 69 but the 64-wide grid (112) would overflow 69 slots -> 128
+    assert bn((1, 56, 56, 64), 256, 1, 23) == 128
+    # batch 64 on the whole GPU: 256 tiles of 128 -> stays 128
+    assert bn((64, 14, 14, 256), 256, 3, 148) == 128
