@@ -79,3 +79,25 @@ def test_conv_tile_width_rule():
     assert bn((1, 56, 56, 64), 256, 1, 23) == 128
     # batch 64 on the whole GPU: 256 tiles of 128 -> stays 128
     assert bn((64, 14, 14, 256), 256, 3, 148) == 128
+
+
+def test_gpu_library_is_tcgen05_tma_sm100a():
+    """The built kernel library is sm_100a SASS that issues tcgen05 MMAs
+    (UTCHMMA) and TMA loads/stores (UTMALDG/UTMASTG), and the conv kernels keep
+    the 96-register cap that admits 3 resident CTAs per SM (cuobjdump, no GPU)."""
+    import re
+    import shutil
+    import subprocess
+    from pathlib import Path
+    import pytest
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not Path(cuobjdump).exists():
+        pytest.skip("cuobjdump not available")
+    lib = Path(__file__).resolve().parents[1] / "paper_2504_08795_b200" / "lib" / "libdaris_gpu.so"
+    sass = subprocess.run([cuobjdump, "-sass", str(lib)], capture_output=True, text=True, check=True).stdout
+    assert "sm_100a" in sass
+    for mnemonic in ("UTCHMMA", "UTMALDG", "UTMASTG"):
+        assert mnemonic in sass, mnemonic
+    res = subprocess.run([cuobjdump, "-res-usage", str(lib)], capture_output=True, text=True, check=True).stdout
+    regs = [int(r) for r in re.findall(r"conv_igemm_tc_kernel\S*:\s*\n\s*REG:(\d+)", res)]
+    assert regs and max(regs) <= 96, regs
