@@ -144,6 +144,19 @@ typedef struct daris_trace_entry {
   double duration;
 } daris_trace_entry;
 
+/* one task of a context's ctx_tasks list, for daris_eval_ledger */
+typedef struct daris_ledger_entry {
+  double util;           /* TimingTracker.utilization(task) */
+  int32_t hp;            /* task priority is HP */
+  int32_t active_jobs;   /* TaskState.active_jobs */
+} daris_ledger_entry;
+
+/* PriorityKey (scheduler.py:66-73) of one ready stage */
+typedef struct daris_ready_key {
+  double edf;
+  int32_t level, task, job, _pad;
+} daris_ready_key;
+
 typedef struct daris_handle daris_handle;
 
 int daris_create(const daris_gpu_config* gpu, const daris_task_spec* tasks, int32_t n_tasks,
@@ -211,6 +224,50 @@ int daris_water_fill(const int32_t* widths, int32_t n, double capacity, double* 
 int daris_allocate_rates(const daris_gpu_config* gpu, const int32_t* widths, const int32_t* ctx_ids,
                          int32_t n, double* out_alloc, double* out_rates, double* out_scale);
 double daris_py_sum(const double* values, const int32_t* is_int, int64_t n);
+
+/* Stateless decision kernels. The stateful handle above runs every decision
+ * through these same functions (csrc/core/decide.cpp); the object-level drop-in
+ * API (Scheduler / TimingTracker / make_job / next_completion / advance_progress
+ * over Python-owned TaskState, Job and ready lists, exactly as the reference's
+ * tests drive them) calls them directly. Each replaces one reference expression:
+ *   daris_eval_window_peak        ExecutionWindow.peak (timing.py:52-56)
+ *   daris_eval_stage_fallback     TimingTracker.stage_estimate, empty window (timing.py:84-86)
+ *   daris_eval_utilization        TimingTracker.utilization, uncached value (timing.py:102-107)
+ *   daris_eval_deadline_shares    TimingTracker.deadline_shares (timing.py:116-132)
+ *   daris_eval_virtual_deadlines  make_job's cumulative stage deadlines (model.py:211-227)
+ *   daris_eval_ledger             Scheduler.context_utilization (scheduler.py:157-171)
+ *   daris_eval_admission          Scheduler.admission_test (scheduler.py:179-200)
+ *   daris_eval_placement          Scheduler.populate_contexts (scheduler.py:131-153)
+ *   daris_eval_predicted_finish   Scheduler.predicted_finish (scheduler.py:202-213)
+ *   daris_eval_priority_level     Scheduler.priority_key level (scheduler.py:278-284)
+ *   daris_eval_pick               Scheduler.dispatch's min() (scheduler.py:289-296)
+ *   daris_eval_next_completion    gpu.next_completion (gpu.py:208-226)
+ *   daris_eval_advance            gpu.advance_progress, remaining[] updated in place (gpu.py:229-240)
+ * Messages of failing calls are readable with daris_eval_last_error (thread-local). */
+const char* daris_eval_last_error(void);
+int daris_eval_window_peak(const double* samples, int32_t n, double* out);
+int daris_eval_stage_fallback(double full_load, double nominal, double nominal_total, double* out);
+int daris_eval_utilization(int64_t completed_jobs, double full_load, double task_estimate, double period,
+                           double* out);
+int daris_eval_deadline_shares(const double* estimates, int32_t n, double deadline, int32_t task_id,
+                               double* out_shares);
+int daris_eval_virtual_deadlines(double release, double deadline, const double* shares, int32_t n,
+                                 double* out_abs_deadline, double* out);
+int daris_eval_ledger(const daris_ledger_entry* tasks, int32_t n, daris_ledger_t* out);
+int daris_eval_admission(const daris_ledger_t* ledger, double job_util, int32_t hp, int32_t n_streams,
+                         double* out_active, double* out_limit, int32_t* out_admitted);
+int daris_eval_placement(const double* util, const int32_t* hp, const int32_t* ids, int32_t n, int32_t n_contexts,
+                         int32_t insertion_order, int32_t* out_context, int32_t* out_order, double* out_totals);
+int daris_eval_predicted_finish(double t, const double* backlog_estimates, int64_t n, int32_t n_streams,
+                                double task_estimate, double* out);
+int daris_eval_priority_level(int32_t hp, int32_t is_last, int32_t predecessor_missed, int32_t no_last,
+                              int32_t no_prior, int32_t no_fixed, int32_t* out);
+int daris_eval_pick(const daris_ready_key* keys, int32_t n, int32_t* out_index);
+int daris_eval_next_completion(const double* remaining, const double* rates, const int64_t* job_ids,
+                               const int64_t* stage_indices, int32_t n, double now, int32_t* out_index,
+                               double* out_time);
+int daris_eval_advance(double* remaining, const double* rates, const int64_t* job_ids,
+                       const int64_t* stage_indices, int32_t n, double dt);
 
 #ifdef __cplusplus
 }

@@ -83,6 +83,15 @@ class ReportC(C.Structure):
                                          "missed_hp", "missed_lp")]
 
 
+class LedgerEntryC(C.Structure):
+    _fields_ = [("util", C.c_double), ("hp", C.c_int32), ("active_jobs", C.c_int32)]
+
+
+class ReadyKeyC(C.Structure):
+    _fields_ = [("edf", C.c_double), ("level", C.c_int32), ("task", C.c_int32), ("job", C.c_int32),
+                ("_pad", C.c_int32)]
+
+
 class TraceEntryC(C.Structure):
     _fields_ = [("task", C.c_int32), ("job", C.c_int32), ("stage", C.c_int32), ("_pad", C.c_int32),
                 ("duration", C.c_double)]
@@ -136,12 +145,28 @@ def lib() -> C.CDLL:
             "daris_allocate_rates": [P(GpuConfigC), P(i32), P(i32), i32, P(f64), P(f64), P(f64)],
             "daris_py_sum": [P(f64), P(i32), i64],
             "daris_destroy": [vp],
+            # stateless decision kernels (include/daris.h, csrc/core/decide.cpp)
+            "daris_eval_last_error": [],
+            "daris_eval_window_peak": [P(f64), i32, P(f64)],
+            "daris_eval_stage_fallback": [f64, f64, f64, P(f64)],
+            "daris_eval_utilization": [i64, f64, f64, f64, P(f64)],
+            "daris_eval_deadline_shares": [P(f64), i32, f64, i32, P(f64)],
+            "daris_eval_virtual_deadlines": [f64, f64, P(f64), i32, P(f64), P(f64)],
+            "daris_eval_ledger": [P(LedgerEntryC), i32, P(LedgerC)],
+            "daris_eval_admission": [P(LedgerC), f64, i32, i32, P(f64), P(f64), P(i32)],
+            "daris_eval_placement": [P(f64), P(i32), P(i32), i32, i32, i32, P(i32), P(i32), P(f64)],
+            "daris_eval_predicted_finish": [f64, P(f64), i64, i32, f64, P(f64)],
+            "daris_eval_priority_level": [i32, i32, i32, i32, i32, i32, P(i32)],
+            "daris_eval_pick": [P(ReadyKeyC), i32, P(i32)],
+            "daris_eval_next_completion": [P(f64), P(f64), P(i64), P(i64), i32, f64, P(i32), P(f64)],
+            "daris_eval_advance": [P(f64), P(f64), P(i64), P(i64), i32, f64],
         }
         for name, args in sig.items():
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = C.c_int
         L.daris_last_error.restype = C.c_char_p
+        L.daris_eval_last_error.restype = C.c_char_p
         L.daris_log_count.restype = C.c_int64
         L.daris_log_copy.restype = C.c_int64
         L.daris_audit_count.restype = C.c_int64
@@ -162,6 +187,10 @@ EXPORTED_SYMBOLS = (
     "daris_record_execution", "daris_note_job_complete", "daris_sim_run", "daris_trace_run",
     "daris_log_count", "daris_log_copy", "daris_audit_count", "daris_audit_copy", "daris_log_clear",
     "daris_water_fill", "daris_allocate_rates", "daris_py_sum",
+    "daris_eval_last_error", "daris_eval_window_peak", "daris_eval_stage_fallback", "daris_eval_utilization",
+    "daris_eval_deadline_shares", "daris_eval_virtual_deadlines", "daris_eval_ledger", "daris_eval_admission",
+    "daris_eval_placement", "daris_eval_predicted_finish", "daris_eval_priority_level", "daris_eval_pick",
+    "daris_eval_next_completion", "daris_eval_advance",
 )
 
 
@@ -367,3 +396,136 @@ def records_from_array(arr: np.ndarray) -> list[tuple]:
                     None if stages[i] < 0 else stages[i], None if ctxs[i] < 0 else ctxs[i],
                     None if streams[i] < 0 else streams[i], None if math.isnan(r) else r))
     return out
+
+
+# ----------------------------------------------------------------------------- stateless kernels
+# Thin typed wrappers over daris_eval_* (csrc/core/decide.cpp): the object-level
+# drop-in API keeps its state in Python objects, like the reference, and makes
+# every decision through these, the same functions the native handle uses.
+
+def _ev(code: int) -> None:
+    if code != 0:
+        raise_status(code, lib().daris_eval_last_error().decode())
+
+
+def _f64(vals) -> C.Array:
+    vals = list(vals)
+    return (C.c_double * max(1, len(vals)))(*vals)
+
+
+def ev_window_peak(values: Sequence[float]) -> float:
+    out = C.c_double()
+    _ev(lib().daris_eval_window_peak(_f64(values), len(values), C.byref(out)))
+    return out.value
+
+
+def ev_stage_fallback(full_load: float, nominal: float, nominal_total: float) -> float:
+    out = C.c_double()
+    _ev(lib().daris_eval_stage_fallback(float(full_load), float(nominal), float(nominal_total), C.byref(out)))
+    return out.value
+
+
+def ev_utilization(completed_jobs: int, full_load: float, task_estimate: float, period: float) -> float:
+    out = C.c_double()
+    _ev(lib().daris_eval_utilization(int(completed_jobs), float(full_load), float(task_estimate), float(period),
+                                     C.byref(out)))
+    return out.value
+
+
+def ev_task_estimate(stage_estimates: Sequence[float]) -> float:
+    """builtin sum() of the stage estimates (timing.py:88-90), CPython-exact."""
+    return lib().daris_py_sum(_f64(stage_estimates), None, len(stage_estimates))
+
+
+def ev_deadline_shares(estimates: Sequence[float], deadline: float, task_id: int) -> list[float]:
+    n = len(estimates)
+    out = (C.c_double * max(1, n))()
+    _ev(lib().daris_eval_deadline_shares(_f64(estimates), n, float(deadline), int(task_id), out))
+    return list(out)[:n]
+
+
+def ev_virtual_deadlines(release: float, deadline: float, shares: Sequence[float]) -> tuple[float, list[float]]:
+    n = len(shares)
+    out = (C.c_double * max(1, n))()
+    absd = C.c_double()
+    _ev(lib().daris_eval_virtual_deadlines(float(release), float(deadline), _f64(shares), n, C.byref(absd), out))
+    return absd.value, list(out)[:n]
+
+
+def ev_ledger(entries: Sequence[tuple[float, bool, int]]) -> LedgerC:
+    n = len(entries)
+    arr = (LedgerEntryC * max(1, n))(*[LedgerEntryC(float(u), int(bool(hp)), int(min(a, 2 ** 30)))
+                                       for u, hp, a in entries])
+    out = LedgerC()
+    _ev(lib().daris_eval_ledger(arr, n, C.byref(out)))
+    return out
+
+
+def ev_admission(ledger: LedgerC, job_util: float, hp: bool, n_streams: int) -> tuple[float, float, bool]:
+    active, limit, ok = C.c_double(), C.c_double(), C.c_int32()
+    _ev(lib().daris_eval_admission(C.byref(ledger), float(job_util), int(bool(hp)), int(n_streams),
+                                   C.byref(active), C.byref(limit), C.byref(ok)))
+    return active.value, limit.value, bool(ok.value)
+
+
+def ev_placement(utils: Sequence[float], hps: Sequence[bool], ids: Sequence[int], n_contexts: int,
+                 insertion: bool) -> tuple[list[int], list[int]]:
+    """Algorithm 1: (home context per input index, input indices in placement order)."""
+    n = len(utils)
+    ctx = (C.c_int32 * max(1, n))()
+    order = (C.c_int32 * max(1, n))()
+    totals = (C.c_double * max(1, n_contexts))()
+    _ev(lib().daris_eval_placement(_f64(utils), (C.c_int32 * max(1, n))(*[int(bool(h)) for h in hps]),
+                                   (C.c_int32 * max(1, n))(*[int(i) for i in ids]), n, int(n_contexts),
+                                   int(bool(insertion)), ctx, order, totals))
+    return list(ctx)[:n], list(order)[:n]
+
+
+def ev_predicted_finish(t: float, backlog: Sequence[float], n_streams: int, task_estimate: float) -> float:
+    out = C.c_double()
+    _ev(lib().daris_eval_predicted_finish(float(t), _f64(backlog), len(backlog), int(n_streams),
+                                          float(task_estimate), C.byref(out)))
+    return out.value
+
+
+def ev_priority_level(hp: bool, is_last: bool, predecessor_missed: bool, no_last: bool, no_prior: bool,
+                      no_fixed: bool) -> int:
+    out = C.c_int32()
+    _ev(lib().daris_eval_priority_level(int(bool(hp)), int(bool(is_last)), int(bool(predecessor_missed)),
+                                        int(bool(no_last)), int(bool(no_prior)), int(bool(no_fixed)),
+                                        C.byref(out)))
+    return out.value
+
+
+def ev_pick(keys: Sequence[tuple[int, float, int, int]]) -> int:
+    """Index of the minimal (level, edf, task, job) key, first minimum kept."""
+    n = len(keys)
+    arr = (ReadyKeyC * max(1, n))(*[ReadyKeyC(float(e), int(lv), int(t), int(j), 0) for lv, e, t, j in keys])
+    out = C.c_int32()
+    _ev(lib().daris_eval_pick(arr, n, C.byref(out)))
+    return out.value
+
+
+def ev_next_completion(remaining: Sequence[float], rates: Sequence[float], job_ids: Sequence[int],
+                       stage_indices: Sequence[int], now: float) -> tuple[int, float]:
+    n = len(remaining)
+    idx, t = C.c_int32(), C.c_double()
+    _ev(lib().daris_eval_next_completion(_f64(remaining), _f64(rates), (C.c_int64 * max(1, n))(*job_ids),
+                                         (C.c_int64 * max(1, n))(*stage_indices), n, float(now), C.byref(idx),
+                                         C.byref(t)))
+    return idx.value, t.value
+
+
+def ev_advance(remaining: list[float], rates: Sequence[float], job_ids: Sequence[int],
+               stage_indices: Sequence[int], dt: float) -> tuple[list[float], tuple[int, str] | None]:
+    """New remaining work; on overshoot raises after the stages before it were
+    advanced (the caller applies `remaining` element-wise, see gpu.advance_progress)."""
+    n = len(remaining)
+    rem = _f64(remaining)
+    code = lib().daris_eval_advance(rem, _f64(rates), (C.c_int64 * max(1, n))(*job_ids),
+                                    (C.c_int64 * max(1, n))(*stage_indices), n, float(dt))
+    out = list(rem)[:n]
+    if code != 0:
+        err = lib().daris_eval_last_error().decode()
+        return out, (code, err)
+    return out, None

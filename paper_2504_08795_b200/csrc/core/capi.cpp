@@ -321,3 +321,124 @@ double daris_py_sum(const double* values, const int32_t* is_int, int64_t n) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- stateless kernels
+namespace {
+thread_local std::string eval_error;
+template <class F>
+int eval_guard(F&& f) {
+  try {
+    f();
+    eval_error.clear();
+    return DARIS_OK;
+  } catch (const daris::Error& e) {
+    eval_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    eval_error = e.what();
+    return DARIS_E_INTERNAL;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* daris_eval_last_error(void) { return eval_error.c_str(); }
+
+int daris_eval_window_peak(const double* samples, int32_t n, double* out) {
+  return eval_guard([&] {
+    if (n < 1) throw daris::Error(DARIS_E_VALUE, "empty window has no peak");
+    *out = daris::window_peak(samples, n);
+  });
+}
+
+int daris_eval_stage_fallback(double full_load, double nominal, double nominal_total, double* out) {
+  return eval_guard([&] { *out = daris::stage_fallback(full_load, nominal, nominal_total); });
+}
+
+int daris_eval_utilization(int64_t completed_jobs, double full_load, double task_estimate, double period,
+                           double* out) {
+  return eval_guard([&] { *out = daris::utilization_of(completed_jobs, full_load, task_estimate, period); });
+}
+
+int daris_eval_deadline_shares(const double* estimates, int32_t n, double deadline, int32_t task_id,
+                               double* out_shares) {
+  return eval_guard([&] {
+    if (n < 1) throw daris::Error(DARIS_E_VALUE, "a task has at least one stage");
+    daris::deadline_split(estimates, n, deadline, out_shares, task_id);
+  });
+}
+
+int daris_eval_virtual_deadlines(double release, double deadline, const double* shares, int32_t n,
+                                 double* out_abs_deadline, double* out) {
+  return eval_guard([&] {
+    if (n < 1) throw daris::Error(DARIS_E_VALUE, "a task has at least one stage");
+    const double abs_dl = release + deadline;  // model.py:211
+    *out_abs_deadline = abs_dl;
+    daris::virtual_deadlines(release, abs_dl, shares, n, out);
+  });
+}
+
+int daris_eval_ledger(const daris_ledger_entry* tasks, int32_t n, daris_ledger_t* out) {
+  return eval_guard([&] { *out = daris::ledger_sum(tasks, n); });
+}
+
+int daris_eval_admission(const daris_ledger_t* ledger, double job_util, int32_t hp, int32_t n_streams,
+                         double* out_active, double* out_limit, int32_t* out_admitted) {
+  return eval_guard([&] {
+    bool ok;
+    daris::admission_eval(*ledger, job_util, hp != 0, n_streams, out_active, out_limit, &ok);
+    *out_admitted = ok ? 1 : 0;
+  });
+}
+
+int daris_eval_placement(const double* util, const int32_t* hp, const int32_t* ids, int32_t n, int32_t n_contexts,
+                         int32_t insertion_order, int32_t* out_context, int32_t* out_order, double* out_totals) {
+  return eval_guard([&] {
+    if (n_contexts < 1) throw daris::Error(DARIS_E_VALUE, "n_contexts must be >= 1");
+    daris::greedy_place(util, hp, ids, n, n_contexts, insertion_order != 0, out_context, out_totals, out_order);
+  });
+}
+
+int daris_eval_predicted_finish(double t, const double* backlog_estimates, int64_t n, int32_t n_streams,
+                                double task_estimate, double* out) {
+  return eval_guard([&] { *out = daris::predicted_finish_eval(t, backlog_estimates, n, n_streams, task_estimate); });
+}
+
+int daris_eval_priority_level(int32_t hp, int32_t is_last, int32_t predecessor_missed, int32_t no_last,
+                              int32_t no_prior, int32_t no_fixed, int32_t* out) {
+  return eval_guard([&] {
+    daris_options o{};
+    o.no_last = no_last;
+    o.no_prior = no_prior;
+    o.no_fixed = no_fixed;
+    *out = daris::priority_level(hp != 0, is_last != 0, predecessor_missed != 0, o);
+  });
+}
+
+int daris_eval_pick(const daris_ready_key* keys, int32_t n, int32_t* out_index) {
+  return eval_guard([&] {
+    if (n < 1) throw daris::Error(DARIS_E_VALUE, "empty ready list");
+    *out_index = daris::pick_ready(keys, n);
+  });
+}
+
+int daris_eval_next_completion(const double* remaining, const double* rates, const int64_t* job_ids,
+                               const int64_t* stage_indices, int32_t n, double now, int32_t* out_index,
+                               double* out_time) {
+  static_assert(sizeof(long long) == sizeof(int64_t), "int64 layout");
+  return eval_guard([&] {
+    *out_index = daris::next_completion_eval(remaining, rates, reinterpret_cast<const long long*>(job_ids),
+                                             reinterpret_cast<const long long*>(stage_indices), n, now, out_time);
+  });
+}
+
+int daris_eval_advance(double* remaining, const double* rates, const int64_t* job_ids,
+                       const int64_t* stage_indices, int32_t n, double dt) {
+  return eval_guard([&] {
+    daris::advance_eval(remaining, rates, reinterpret_cast<const long long*>(job_ids),
+                        reinterpret_cast<const long long*>(stage_indices), n, dt);
+  });
+}
+
+}  // extern "C"

@@ -161,8 +161,7 @@ double Dispatcher::stage_estimate(int tid, int j) const {  // timing.py:78-86
   const Window& w = rt_[i].win.at(j);
   if (!w.empty()) return w.peak();
   const TaskDef& t = tasks_[i];
-  const double share = t.nominal[j] / t.nominal_total;
-  return rt_[i].full_load * share;
+  return stage_fallback(rt_[i].full_load, t.nominal[j], t.nominal_total);
 }
 
 double Dispatcher::task_estimate(int tid) const {  // timing.py:88-90
@@ -176,9 +175,7 @@ double Dispatcher::utilization(int tid) {  // timing.py:92-108
   TaskRT& r = rt(tid);
   if (r.ucache_valid) return r.ucache;
   const TaskDef& t = task(tid);
-  double u;
-  if (r.completed == 0) u = r.full_load / t.period;
-  else u = task_estimate(tid) / t.period;
+  const double u = utilization_of(r.completed, r.full_load, r.completed == 0 ? 0.0 : task_estimate(tid), t.period);
   r.ucache = u;
   r.ucache_valid = true;
   return u;
@@ -195,55 +192,38 @@ std::vector<double> Dispatcher::deadline_shares(int tid) const {  // timing.py:1
   const size_t n = t.nominal.size();
   std::vector<double> est(n);
   for (size_t j = 0; j < n; ++j) est[j] = stage_estimate(tid, static_cast<int>(j));
-  const double total = py_sum(est);
-  if (total <= 0)
-    throw Error(DARIS_E_ZERO_TOTAL_ESTIMATE,
-                "task " + std::to_string(tid) + " has no positive execution estimate to split its deadline over");
-  std::vector<double> shares;
-  shares.reserve(n);
-  for (size_t j = 0; j + 1 < n; ++j) shares.push_back(est[j] / total * t.deadline);
-  const double rest = py_sum(shares);
-  shares.push_back(t.deadline - rest);
+  std::vector<double> shares(n);
+  deadline_split(est.data(), static_cast<int>(n), t.deadline, shares.data(), tid);
   return shares;
 }
 
 void Dispatcher::populate() {  // scheduler.py:131-153
-  std::vector<double> totals(gpu_.n_contexts, 0.0);
-  for (int cls = 0; cls < 2; ++cls) {
-    std::vector<int> group;
-    for (const TaskDef& t : tasks_)
-      if (t.hp == (cls == 0)) group.push_back(t.id);
-    if (!opts_.placement_insertion) {
-      std::vector<std::pair<double, int>> keyed;
-      for (int id : group) keyed.push_back({-utilization(id), id});
-      std::stable_sort(keyed.begin(), keyed.end());
-      for (size_t k = 0; k < group.size(); ++k) group[k] = keyed[k].second;
-    }
-    for (int id : group) {
-      int target = 0;
-      for (int c = 1; c < gpu_.n_contexts; ++c)
-        if (totals[c] < totals[target]) target = c;  // ties -> lowest id
-      rt(id).home = target + 1;
-      ctx_tasks_[target].push_back(id);
-      totals[target] += utilization(id);
-    }
+  const int n = static_cast<int>(tasks_.size());
+  std::vector<double> util(n), totals(gpu_.n_contexts);
+  std::vector<int32_t> hp(n), ids(n), home(n);
+  for (int i = 0; i < n; ++i) {
+    ids[i] = tasks_[i].id;
+    hp[i] = tasks_[i].hp ? 1 : 0;
+    util[i] = utilization(ids[i]);
+  }
+  std::vector<int32_t> order(n);
+  greedy_place(util.data(), hp.data(), ids.data(), n, gpu_.n_contexts, opts_.placement_insertion != 0,
+               home.data(), totals.data(), order.data());
+  for (int i : order) {  // ctx_tasks order = placement order (feeds the += ledgers)
+    rt_[i].home = home[i];
+    ctx_tasks_[home[i] - 1].push_back(ids[i]);
   }
 }
 
 daris_ledger_t Dispatcher::ledger(int ctx) {  // scheduler.py:157-171
-  double hp_total = 0.0, lp_total = 0.0, lp_active = 0.0, hp_active = 0.0;
-  for (int id : ctx_tasks_.at(ctx - 1)) {
-    const double u = utilization(id);
-    const TaskRT& r = rt(id);
-    if (task(id).hp) {
-      hp_total += u;
-      if (r.active > 0) hp_active += u;
-    } else {
-      lp_total += u;
-      if (r.active > 0) lp_active += u;
-    }
+  const auto& ids = ctx_tasks_.at(ctx - 1);
+  std::vector<daris_ledger_entry> e(ids.size());
+  for (size_t k = 0; k < ids.size(); ++k) {
+    e[k].util = utilization(ids[k]);
+    e[k].hp = task(ids[k]).hp ? 1 : 0;
+    e[k].active_jobs = static_cast<int32_t>(std::min<long long>(rt(ids[k]).active, 1 << 30));
   }
-  return {hp_total, lp_total, lp_active, hp_active};
+  return ledger_sum(e.data(), static_cast<int>(e.size()));
 }
 
 Audit Dispatcher::admission_test(const Job& job, int ctx, double t) {  // scheduler.py:179-200
@@ -251,22 +231,18 @@ Audit Dispatcher::admission_test(const Job& job, int ctx, double t) {  // schedu
   const double u = utilization(job.task);
   const bool hp = task(job.task).hp;
   double active, limit;
-  if (!hp) {
-    active = l.lp_active;
-    limit = gpu_.n_streams - l.hp_total;
-  } else {
-    active = l.hp_active + l.lp_active;
-    limit = static_cast<double>(gpu_.n_streams);
-  }
-  return {t, active, u, limit, job.id, job.task, hp ? DARIS_HP : DARIS_LP, ctx, active + u < limit};
+  bool ok;
+  admission_eval(l, u, hp, gpu_.n_streams, &active, &limit, &ok);
+  return {t, active, u, limit, job.id, job.task, hp ? DARIS_HP : DARIS_LP, ctx, ok};
 }
 
 double Dispatcher::predicted_finish(int tid, int ctx, double t) const {  // scheduler.py:202-213
-  double backlog = 0.0;
+  std::vector<double> backlog;
   for (const Job* live : live_.at(ctx - 1))
     for (const StageJob& st : live->stages)
-      if (st.state != DONE) backlog += stage_estimate(live->task, st.j);
-  return t + backlog / gpu_.n_streams + task_estimate(tid);
+      if (st.state != DONE) backlog.push_back(stage_estimate(live->task, st.j));
+  return predicted_finish_eval(t, backlog.data(), static_cast<long long>(backlog.size()), gpu_.n_streams,
+                               task_estimate(tid));
 }
 
 void Dispatcher::place(Job* job, int ctx) {  // scheduler.py:268-274
@@ -300,15 +276,10 @@ Job* Dispatcher::release(int tid, double t, int job_id, const double* stage_work
   job->batch = spec.batch;
   const int n = static_cast<int>(spec.nominal.size());
   job->stages.resize(n);
-  double acc = t;
+  std::vector<double> vdls(n);
+  virtual_deadlines(t, abs_dl, shares.data(), n, vdls.data());
   for (int j = 0; j < n; ++j) {
-    double vdl;
-    if (j == n - 1) {
-      vdl = abs_dl;
-    } else {
-      acc += shares[j];
-      vdl = acc;
-    }
+    const double vdl = vdls[j];
     StageJob& s = job->stages[j];
     s.job = job.get();
     s.j = j;
@@ -363,33 +334,20 @@ Job* Dispatcher::release(int tid, double t, int job_id, const double* stage_work
 
 int Dispatcher::level_key(const StageJob* st) const {  // scheduler.py:278-287
   const Job* job = st->job;
-  const bool is_last = (st->j == static_cast<int>(job->stages.size()) - 1) && !opts_.no_last;
-  const bool late = st->late_pred && !opts_.no_prior;
-  if (opts_.no_fixed) return 0;
-  return 4 * (task(job->task).hp ? 0 : 1) + 2 * (is_last ? 0 : 1) + (late ? 0 : 1);
+  const bool is_last = st->j == static_cast<int>(job->stages.size()) - 1;
+  return priority_level(task(job->task).hp, is_last, st->late_pred, opts_);
 }
 
 StageJob* Dispatcher::dispatch(int ctx, int stream, double t) {  // scheduler.py:289-296
   auto& q = ready_.at(ctx - 1);
   if (q.empty()) return nullptr;
-  size_t best = 0;
-  int bl = level_key(q[0]);
-  double be = opts_.edf_on_job_deadline ? q[0]->job->dl : q[0]->vdl;
-  for (size_t k = 1; k < q.size(); ++k) {
+  thread_local std::vector<daris_ready_key> keys;
+  keys.resize(q.size());
+  for (size_t k = 0; k < q.size(); ++k) {
     const StageJob* s = q[k];
-    const int l = level_key(s);
-    const double e = opts_.edf_on_job_deadline ? s->job->dl : s->vdl;
-    bool less;
-    if (l != bl) less = l < bl;
-    else if (e != be) less = e < be;
-    else if (s->job->task != q[best]->job->task) less = s->job->task < q[best]->job->task;
-    else less = s->job->id < q[best]->job->id;
-    if (less) {
-      best = k;
-      bl = l;
-      be = e;
-    }
+    keys[k] = {opts_.edf_on_job_deadline ? s->job->dl : s->vdl, level_key(s), s->job->task, s->job->id, 0};
   }
+  const size_t best = static_cast<size_t>(pick_ready(keys.data(), static_cast<int>(keys.size())));
   StageJob* st = q[best];
   q.erase(q.begin() + static_cast<long>(best));
   st->state = RUNNING;  // engine.py:445-449

@@ -3,6 +3,7 @@
 // reference's model.py / timing.py / scheduler.py; float arithmetic replicates
 // CPython 3.12 exactly (see PySum) so decisions are bit-identical.
 #pragma once
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <deque>
@@ -87,17 +88,8 @@ struct Window {
     if (count < cap) ++count;
   }
   bool empty() const { return count == 0; }
-  // max() over the samples oldest->newest (Python max keeps the first maximum)
-  double peak() const {
-    const int n = count;
-    const int start = (n < cap) ? 0 : head;
-    double best = buf[start];
-    for (int k = 1; k < n; ++k) {
-      double v = buf[(start + k) % cap];
-      if (v > best) best = v;
-    }
-    return best;
-  }
+  // max() over the samples oldest->newest (decide.cpp window_peak)
+  double peak() const;
 };
 
 enum StageSt : uint8_t { PENDING = 0, READY = 1, RUNNING = 2, DONE = 3 };
@@ -216,6 +208,27 @@ double allocate_rates(const daris_gpu_config& g, int per_ctx_sms, const std::vec
                       const std::vector<int>& ctx, std::vector<Alloc>& alloc, std::vector<double>& rates);
 
 double full_load_time(const Dispatcher& d, int task_id, int reps, const int32_t* draws);
+
+// --- stateless decision kernels (decide.cpp), shared by the Dispatcher and the
+// object-level drop-in API (daris_eval_* in the C ABI) ------------------------
+double window_peak(const double* v, int n);                                       // timing.py:52-56
+double stage_fallback(double full_load, double nominal, double nominal_total);     // timing.py:84-86
+double utilization_of(long long completed, double full_load, double task_est, double period);  // timing.py:102-107
+void deadline_split(const double* est, int n, double deadline, double* out, int task_id);      // timing.py:116-132
+void virtual_deadlines(double release, double abs_deadline, const double* shares, int n, double* out);  // model.py:216-227
+daris_ledger_t ledger_sum(const daris_ledger_entry* e, int n);                     // scheduler.py:157-171
+void admission_eval(const daris_ledger_t& l, double u, bool hp, int n_streams, double* active, double* limit,
+                    bool* admitted);                                               // scheduler.py:179-200
+void greedy_place(const double* util, const int32_t* hp, const int32_t* ids, int n, int n_ctx, bool insertion,
+                  int32_t* out_ctx, double* totals, int32_t* out_order);           // scheduler.py:131-153
+double predicted_finish_eval(double t, const double* backlog, long long n, int n_streams, double task_est);
+int priority_level(bool hp, bool is_last, bool late_pred, const daris_options& o);  // scheduler.py:278-284
+bool key_less(const daris_ready_key& a, const daris_ready_key& b);
+int pick_ready(const daris_ready_key* keys, int n);                                // scheduler.py:289-296
+int next_completion_eval(const double* rem, const double* rates, const long long* job, const long long* stage, int n,
+                         double now, double* t_out);                              // gpu.py:208-226
+void advance_eval(double* rem, const double* rates, const long long* job, const long long* stage, int n,
+                  double dt);                                                      // gpu.py:229-240
 
 struct RunResult {
   daris_report report;

@@ -97,43 +97,17 @@ double allocate_rates(const daris_gpu_config& g, int per_ctx_sms, const std::vec
   return scale;
 }
 
-// earliest finisher; ties on (job, stage) keys (gpu.py:208-226)
+// earliest finisher; ties on (job, stage) keys (gpu.py:208-226) — decide.cpp
 static int next_completion(const std::vector<double>& rem, const std::vector<long long>& k1,
                            const std::vector<long long>& k2, const std::vector<double>& rates, double now,
                            double* t_out) {
-  if (rem.empty()) throw Error(DARIS_E_NO_ACTIVE_STAGES, "no active stages to complete");
-  int best = -1;
-  double bt = 0;
-  for (size_t i = 0; i < rem.size(); ++i) {
-    const double r = rates[i];
-    if (r <= 0) throw Error(DARIS_E_VALUE, "active stage has a non-positive rate");
-    const double t = now + rem[i] / r;
-    bool less;
-    if (best < 0) less = true;
-    else if (t != bt) less = t < bt;
-    else if (k1[i] != k1[best]) less = k1[i] < k1[best];
-    else less = k2[i] < k2[best];
-    if (less) {
-      best = static_cast<int>(i);
-      bt = t;
-    }
-  }
-  *t_out = bt;
-  return best;
+  return next_completion_eval(rem.data(), rates.data(), k1.data(), k2.data(), static_cast<int>(rem.size()), now,
+                              t_out);
 }
 
 static void advance_progress(std::vector<double>& rem, const std::vector<double>& rates, double dt,
                              const std::vector<long long>& k1, const std::vector<long long>& k2) {  // gpu.py:229-240
-  if (dt < 0) throw Error(DARIS_E_VALUE, "dt must be >= 0");
-  for (size_t i = 0; i < rem.size(); ++i) {
-    const double left = rem[i] - rates[i] * dt;
-    if (left < -kEps) {
-      std::ostringstream m;
-      m << "stage (job " << k1[i] << ", stage " << k2[i] << ") overshoots completion";
-      throw Error(DARIS_E_OVERSHOOT, m.str());
-    }
-    rem[i] = std::max(0.0, left);
-  }
+  advance_eval(rem.data(), rates.data(), k1.data(), k2.data(), static_cast<int>(rem.size()), dt);
 }
 
 // One repetition of the busy-system measurement (timing.py:184-218).

@@ -1,9 +1,11 @@
 """GPU partition configuration and the parity rate model of the drop-in API.
 
-``GpuConfig`` / ``Policy`` / ``ceil_even`` / ``sm_per_context`` keep the
-reference's names and rules (stagesim/gpu.py:36-115). ``water_fill`` and
-``allocate_rates`` call the native rate model (the sim backend kept for
-bit-exact parity); on real hardware the executor replaces it entirely.
+``GpuConfig`` / ``Policy`` / ``ceil_even`` / ``sm_per_context`` /
+``ContextState`` / ``StreamState`` / ``build_contexts`` keep the reference's
+names and rules (stagesim/gpu.py:36-115). ``water_fill``, ``allocate_rates``,
+``next_completion`` and ``advance_progress`` call the native rate model (the
+sim backend kept for bit-exact parity, csrc/core/sim.cpp + decide.cpp); on
+real hardware the executor replaces it entirely.
 """
 
 from __future__ import annotations
@@ -15,7 +17,7 @@ from enum import Enum
 from typing import Sequence
 
 from . import _core
-from .errors import InvalidBatch, InvalidOversubscription
+from .errors import InvalidBatch, InvalidOversubscription, raise_status
 
 _EPS = 1e-9
 
@@ -73,6 +75,34 @@ def sm_per_context(config: GpuConfig) -> int:
     return out.value
 
 
+@dataclass
+class StreamState:
+    """One stream slot of a context; `occupant` is the stage running on it (gpu.py:89-93)."""
+
+    occupant: object | None = None
+
+
+@dataclass
+class ContextState:
+    """A context (SM partition) and its stream slots (gpu.py:96-108)."""
+
+    id: int                      # 1-based
+    sms: int                     # SMs granted (sm_per_context)
+    streams: list[StreamState]
+    util_ledger: object | None = None  # last ContextUtilization computed for it
+
+    def free_stream_index(self) -> int | None:
+        """Lowest free stream slot, None when all are occupied."""
+        return next((k for k, s in enumerate(self.streams) if s.occupant is None), None)
+
+
+def build_contexts(config: GpuConfig) -> list[ContextState]:
+    """N_c contexts of sm_per_context SMs with N_s empty stream slots each (gpu.py:111-115)."""
+    sms = sm_per_context(config)
+    return [ContextState(cid, sms, [StreamState() for _ in range(config.n_streams)])
+            for cid in range(1, config.n_contexts + 1)]
+
+
 def water_fill(widths: Sequence[float], capacity: float) -> tuple[list[float], float | None]:
     """Split `capacity` SMs over stages capped at their widths (gpu.py:118-152)."""
     n = len(widths)
@@ -118,6 +148,29 @@ def allocate_rates(active: Sequence[tuple], config: GpuConfig) -> RateAllocation
     for ctx in dict.fromkeys(ctx for _, ctx in active):
         levels[ctx] = water_fill([s.width for s, cc in active if cc == ctx], per)[1]
     return RateAllocation(list(alloc)[:n], list(rates)[:n], scale.value, levels)
+
+
+def next_completion(active: Sequence[tuple], allocation: RateAllocation, now: float):
+    """(index, stage, time) of the earliest finisher at the current rates, ties
+    on (job id, stage index) (gpu.py:208-226); native decide.cpp."""
+    stages = [s for s, _ in active]
+    idx, t = _core.ev_next_completion([s.remaining_work for s in stages], allocation.rates[:len(stages)],
+                                      [s.job_id for s in stages], [s.stage_index for s in stages], now)
+    return idx, stages[idx], t
+
+
+def advance_progress(active: Sequence[tuple], allocation: RateAllocation, dt: float) -> None:
+    """Integrate remaining work over `dt` at constant rates, in list order,
+    raising OvershootBeyondCompletion past the 1e-9 tolerance (gpu.py:229-240)."""
+    stages = [s for s, _ in active]
+    rem, err = _core.ev_advance([s.remaining_work for s in stages], allocation.rates[:len(stages)],
+                                [s.job_id for s in stages], [s.stage_index for s in stages], dt)
+    if err is not None and err[0] != 9:   # ValueError (dt < 0): nothing advanced
+        raise_status(*err)
+    for s, left in zip(stages, rem):
+        s.remaining_work = left
+    if err is not None:
+        raise_status(*err)
 
 
 @dataclass(frozen=True)

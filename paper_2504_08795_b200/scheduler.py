@@ -1,5 +1,5 @@
 """Scheduling core of the drop-in API: placement, admission, migration,
-priority dispatch and stage completion, executed by the native dispatcher.
+priority dispatch and stage completion, decided by the native decision kernels.
 
 Keeps the reference's public names (stagesim/scheduler.py:26-324):
 ``AblationFlags``, ``SchedulerMode``, ``PriorityKey``, ``ContextUtilization``,
@@ -94,17 +94,27 @@ class Placement:
 
 
 class Scheduler:
-    """Object-level view over one native dispatcher handle.
+    """Object-level scheduler over Python-owned state (scheduler.py:102-324).
 
-    Jobs are created natively at release (``admit_or_migrate``); the Job /
-    StageJob objects passed in are views that this class keeps in sync.
+    State lives where the reference keeps it — ``ctx_tasks`` / ``ready`` /
+    ``live_jobs`` per context, ``TaskState.current_context`` / ``active_jobs``,
+    the tracker's windows — so code that drives or inspects those objects
+    directly works unchanged. Each decision (ledgers, admission, Algorithm 1,
+    predicted finish, priority level, dispatch pick) is one native decision
+    kernel (csrc/core/decide.cpp) — the same functions the stateful dispatcher
+    behind the engine and the GPU executor runs, so both views decide alike
+    (tests/test_object_api.py drives them in lockstep).
+
+    ``stage_migration`` (extension, off by default as the reference has none):
+    a successor stage is queued in its task's current home context instead of
+    the job's placement, so a task migrated at release pulls its in-flight job
+    along (the native option of the same name, dispatcher.cpp ``complete``).
     """
 
     def __init__(self, tracker: TimingTracker, contexts: Sequence, config, *,
                  flags: AblationFlags = AblationFlags(), mode: SchedulerMode = SchedulerMode(),
                  placement_order: str = "descending_util", edf_on_job_deadline: bool = False,
                  stage_migration: bool = False):
-        from .model import spec_to_dict
         if placement_order not in ("descending_util", "insertion"):
             raise ValueError(f"unknown placement order {placement_order!r}")
         self.tracker = tracker
@@ -114,86 +124,141 @@ class Scheduler:
         self.mode = mode
         self.placement_order = placement_order
         self.edf_on_job_deadline = edf_on_job_deadline
-        states = list(tracker._states.values())
-        ws = states[0].window_size if states else 5
-        self._h = _core.Handle(config.native(), [spec_to_dict(st.task) for st in states],
-                               _core.options_struct(window_size=ws, no_last=flags.no_last,
-                                                    no_prior=flags.no_prior, no_fixed=flags.no_fixed,
-                                                    hpa=mode.hpa_enabled, placement_order=placement_order,
-                                                    edf_on_job_deadline=edf_on_job_deadline,
-                                                    stage_migration=stage_migration))
-        self._h.set_full_load([tracker._states[i].full_load_time for i in self._h.task_ids])
-        tracker._h = self._h          # one source of truth
-        self._jobs: dict[int, Job] = {}
+        self.stage_migration = stage_migration
+        ids = [c.id for c in self.contexts]
+        self.ctx_tasks: dict[int, list[int]] = {c: [] for c in ids}
+        self.ready: dict[int, list[StageJob]] = {c: [] for c in ids}
+        self.live_jobs: dict[int, list[Job]] = {c: [] for c in ids}
 
-    # --- placement ---
+    def _is_hp(self, task_id: int) -> bool:
+        return self.tracker.state(task_id).task.priority is Priority.HP
+
+    # --- placement (Algorithm 1) ---
     def populate_contexts(self, states: Sequence[TaskState]) -> None:
-        self._h.populate()
-        for st in states:
-            st.current_context = self._h.home_context(st.task.id)
+        """HP tasks first, then LP; within a class heaviest utilization first
+        (or insertion order); each to the context with the least total so far."""
+        states = list(states)
+        utils = [self.tracker.utilization(st.task.id) for st in states]
+        homes, order = _core.ev_placement(utils, [st.task.priority is Priority.HP for st in states],
+                                          [st.task.id for st in states], len(self.contexts),
+                                          self.placement_order == "insertion")
+        for i in order:
+            ctx_id = self.contexts[homes[i] - 1].id
+            states[i].current_context = ctx_id
+            self.ctx_tasks[ctx_id].append(states[i].task.id)
 
+    # --- Eq. 4-7 ledgers ---
     def context_utilization(self, ctx_id: int) -> ContextUtilization:
-        l = self._h.ledger(ctx_id)
-        return ContextUtilization(l.hp_total, l.lp_total, l.lp_active, l.hp_active)
+        entries = [(self.tracker.utilization(tid), self._is_hp(tid), self.tracker.state(tid).active_jobs)
+                   for tid in self.ctx_tasks[ctx_id]]
+        l = _core.ev_ledger(entries)
+        ledger = ContextUtilization(l.hp_total, l.lp_total, l.lp_active, l.hp_active)
+        self.contexts[ctx_id - 1].util_ledger = ledger
+        return ledger
 
     def context_utilizations(self) -> list[ContextUtilization]:
         return [self.context_utilization(c.id) for c in self.contexts]
 
-    # --- admission ---
+    # --- Eq. 10-11 admission ---
     def admission_test(self, job: Job, ctx_id: int, t: float) -> AdmissionDecision:
-        return AdmissionDecision.from_native(self._h.admission_test(job.task_id, job.job_id, ctx_id, t))
+        ledger = self.context_utilization(ctx_id)
+        u = self.tracker.utilization(job.task_id)
+        hp = self._is_hp(job.task_id)
+        lc = _core.LedgerC(ledger.hp_total, ledger.lp_total, ledger.lp_active, ledger.hp_active)
+        active, limit, ok = _core.ev_admission(lc, u, hp, self.config.n_streams)
+        return AdmissionDecision(t, job.job_id, job.task_id, Priority.HP if hp else Priority.LP, ctx_id,
+                                 active, u, limit, ok)
 
     def predicted_finish(self, job: Job, ctx_id: int, t: float) -> float:
-        return self._h.predicted_finish(job.task_id, ctx_id, t)
+        """t + (estimated work of live jobs' unfinished stages here) / N_s + the job's own estimate."""
+        backlog = [self.tracker.stage_estimate(live.task_id, sj.stage_index)
+                   for live in self.live_jobs[ctx_id] for sj in live.stage_jobs if sj.state is not StageState.DONE]
+        return _core.ev_predicted_finish(t, backlog, self.config.n_streams, self.tracker.task_estimate(job.task_id))
 
     def admit_or_migrate(self, job: Job, t: float) -> Placement:
-        n_before = len(self._h.audits())
-        work = [s.remaining_work for s in job.stage_jobs] or None
-        pl = self._h.release(job.task_id, t, job.job_id, work)
-        audits = [AdmissionDecision.from_native(a) for a in self._h.audits()[n_before:]]
+        """HP: home, tested only under HPA. LP: home if it passes, else the
+        passing context with the earliest predicted finish (sticky migration),
+        else rejected."""
         st = self.tracker.state(job.task_id)
-        if pl.context == 0:
-            return Placement(None, audits=audits)
-        job.placement = pl.context
-        st.active_jobs += 1
-        st.current_context = self._h.home_context(job.task_id)
-        if job.stage_jobs:
-            job.stage_jobs[0].state = StageState.READY
-        self._jobs[job.job_id] = job
-        return Placement(pl.context, migrated_from=pl.migrated_from or None, audits=audits)
+        home = st.current_context
+        audits: list[AdmissionDecision] = []
 
-    # --- dispatch ---
+        def passes(ctx_id: int) -> bool:
+            d = self.admission_test(job, ctx_id, t)
+            audits.append(d)
+            return d.admitted
+
+        if self._is_hp(job.task_id):
+            if self.mode.hpa_enabled and not passes(home):
+                return Placement(None, audits=audits)
+            self._place(job, home)
+            return Placement(home, audits=audits)
+        if passes(home):
+            self._place(job, home)
+            return Placement(home, audits=audits)
+        fits = [c.id for c in self.contexts if c.id != home and passes(c.id)]
+        if not fits:
+            return Placement(None, audits=audits)
+        finish = [self.predicted_finish(job, c, t) for c in fits]
+        target = fits[min(range(len(fits)), key=lambda k: (finish[k], fits[k]))]
+        self._migrate_task(job.task_id, home, target)
+        self._place(job, target)
+        return Placement(target, migrated_from=home, audits=audits)
+
+    def _migrate_task(self, task_id: int, old_ctx: int, new_ctx: int) -> None:
+        if self._is_hp(task_id):
+            raise AssertionError("high-priority tasks never migrate")
+        self.ctx_tasks[old_ctx].remove(task_id)
+        self.ctx_tasks[new_ctx].append(task_id)
+        self.tracker.state(task_id).current_context = new_ctx
+
+    def _place(self, job: Job, ctx_id: int) -> None:
+        job.placement = ctx_id
+        self.tracker.state(job.task_id).active_jobs += 1
+        self.live_jobs[ctx_id].append(job)
+        head = job.stage_jobs[0]
+        head.transition(StageState.READY)
+        self.ready[ctx_id].append(head)
+
+    # --- dispatch (8 fixed levels + EDF) ---
     def priority_key(self, stage: StageJob) -> PriorityKey:
-        hp = self.tracker.state(stage.task_id).task.priority is Priority.HP
-        is_last = stage.is_last and not self.flags.no_last
-        late = stage.predecessor_missed and not self.flags.no_prior
-        level = 0 if self.flags.no_fixed else 4 * (not hp) + 2 * (not is_last) + (not late)
+        f = self.flags
+        level = _core.ev_priority_level(self._is_hp(stage.task_id), stage.is_last, stage.predecessor_missed,
+                                        f.no_last, f.no_prior, f.no_fixed)
         edf = stage.job.absolute_deadline if self.edf_on_job_deadline else stage.virtual_abs_deadline
         return PriorityKey(level, edf, stage.task_id, stage.job_id)
 
-    def dispatch(self, ctx_id: int, t: float, stream: int = 0) -> StageJob | None:
-        ref = self._h.dispatch(ctx_id, stream, t)
-        if ref is None:
+    def dispatch(self, ctx_id: int, t: float) -> StageJob | None:
+        """Remove and return the context's highest-priority ready stage (no preemption)."""
+        queue = self.ready[ctx_id]
+        if not queue:
             return None
-        job = self._jobs[ref.job]
-        st = job.stage_jobs[ref.stage]
-        st.state = StageState.RUNNING
-        st.started_at, st.context, st.stream = ref.started_at, ref.context, ref.stream
-        st.virtual_abs_deadline = ref.virtual_deadline
-        return st
+        keys = [self.priority_key(s) for s in queue]
+        best = queue.pop(_core.ev_pick([(k.level, k.edf_key, k.task_id, k.job_id) for k in keys]))
+        return best
 
+    # --- completion ---
     def complete_stage(self, stage: StageJob, t: float) -> tuple[bool, bool]:
-        done, missed = self._h.complete(stage.job_id, stage.stage_index, t)
-        stage.state = StageState.DONE
+        """Record the observed time; promote the successor (late flag = t past
+        this stage's virtual deadline) or retire the job. Returns (job_done, missed)."""
+        self.tracker.record_execution(stage.task_id, stage.stage_index, t - stage.started_at)
+        stage.transition(StageState.DONE)
         job = stage.job
-        if not done:
+        if not stage.is_last:
             nxt = job.stage_jobs[stage.stage_index + 1]
             nxt.predecessor_missed = t > stage.virtual_abs_deadline
-            nxt.state = StageState.READY
+            nxt.transition(StageState.READY)
+            ctx = job.placement
+            if self.stage_migration:
+                home = self.tracker.state(job.task_id).current_context
+                if home != ctx:
+                    self.live_jobs[ctx].remove(job)
+                    self.live_jobs[home].append(job)
+                    job.placement = ctx = home
+            self.ready[ctx].append(nxt)
             return False, False
         job.completion_time = t
-        st = self.tracker.state(stage.task_id)
-        st.active_jobs -= 1
-        st.completed_jobs += 1
-        self._jobs.pop(job.job_id, None)
-        return True, missed
+        self.tracker.state(stage.task_id).active_jobs -= 1
+        self.tracker.note_job_complete(stage.task_id)
+        self.live_jobs[job.placement].remove(job)
+        return True, t > job.absolute_deadline
