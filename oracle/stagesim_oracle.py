@@ -249,12 +249,20 @@ class _Job:
 def simulate(tasks_in: list, gpu: dict, *, seed=0, duration=60.0, warmup_frac=0.1, ws=5, reps=10,
              no_staging=False, no_last=False, no_prior=False, no_fixed=False, hpa=False,
              phasing="random", placement_order="descending_util", edf_on_job_deadline=False,
-             overload_factor=None, phases_override=None, durations=None):
+             overload_factor=None, phases_override=None, durations=None, stage_migration=False):
     """Run the DARIS execution path and return (records, audits, report, extras).
 
     tasks_in: dicts {id, period, deadline, hp, stages: [(nominal, width)], batch, curve}.
     durations: optional trace {(task, job, stage): seconds} — trace-replay mode
     (SURVEY §7 step 1): every stage runs at rate 1 for its traced duration.
+    stage_migration: the build's zero-delay stage-level migration (north star (2),
+    PAPER.md:4; not in the reference, which re-homes a task only at release,
+    scheduler.py:215-266). Restated independently from its documented rule
+    (include/daris.h daris_options.stage_migration): when a
+    non-final stage completes, its successor is queued in the task's CURRENT
+    home context; if that differs from the job's placement, the job moves to
+    the end of the new context's live list (it counts towards that context's
+    predicted-finish backlog from then on) and its placement becomes the home.
     """
     label = f"{gpu['n_contexts']}x{gpu['n_streams']}_{gpu['oversubscription']:g}"
     tasks = [dict(t) for t in tasks_in]
@@ -466,6 +474,10 @@ def simulate(tasks_in: list, gpu: dict, *, seed=0, duration=60.0, warmup_frac=0.
             nxt = job.stages[st.j + 1]
             nxt.late_pred = t > st.vdl
             nxt.state = 1
+            if stage_migration and home[job.task] != job.place:
+                live[job.place].remove(job)
+                live[home[job.task]].append(job)
+                job.place = home[job.task]
             ready[job.place].append(nxt)
             return False, False
         job.done_at = t

@@ -100,16 +100,17 @@ def test_gpu_scenario_runs_and_replays(preset, rate):
                                                                           phases=res.phases)
     assert _cut(res.records, cfg.duration) == _cut(replay.records, cfg.duration)
     assert res.report.missed_hp == replay.report.missed_hp
-    # ... and through the oracle restatement of the reference scheduler
-    if not cfg.stage_migration:
-        otasks = [{"id": t.id, "period": t.period, "deadline": t.deadline, "hp": t.priority is S.Priority.HP,
-                   "stages": [(p.nominal_time, p.width) for p in t.stages], "batch": 1, "curve": None,
-                   "full_load": res.full_load[t.id]} for t in eff]
-        g = cfg.gpu
-        ogpu = {"total_sms": g.total_sms, "n_contexts": g.n_contexts, "n_streams": g.n_streams,
-                "oversubscription": g.oversubscription, "policy": g.policy.value, "kappa": 0.0}
-        recs, _, _, _ = O.simulate(otasks, ogpu, duration=cfg.duration, warmup_frac=cfg.warmup_frac,
-                                   durations=res.stage_durations(),
-                                   phases_override={t.id: ph for t, ph in zip(eff, res.phases)})
-        assert _cut(res.records, cfg.duration) == _cut(recs, cfg.duration)
+    # ... and through the oracle restatement of the reference scheduler (its
+    # independent stage-migration mode for the C3 migration run)
+    otasks = [{"id": t.id, "period": t.period, "deadline": t.deadline, "hp": t.priority is S.Priority.HP,
+               "stages": [(p.nominal_time, p.width) for p in t.stages], "batch": 1, "curve": None,
+               "full_load": res.full_load[t.id]} for t in eff]
+    g = cfg.gpu
+    ogpu = {"total_sms": g.total_sms, "n_contexts": g.n_contexts, "n_streams": g.n_streams,
+            "oversubscription": g.oversubscription, "policy": g.policy.value, "kappa": 0.0}
+    recs, _, _, _ = O.simulate(otasks, ogpu, duration=cfg.duration, warmup_frac=cfg.warmup_frac,
+                               durations=res.stage_durations(),
+                               phases_override={t.id: ph for t, ph in zip(eff, res.phases)},
+                               stage_migration=cfg.stage_migration)
+    assert _cut(res.records, cfg.duration) == _cut(recs, cfg.duration)
     sim.close()
