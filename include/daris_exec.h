@@ -59,7 +59,8 @@ typedef struct daris_exec_stats {
   int64_t graph_launches;   /* stage graphs launched in the run */
   int64_t copies_h2d, copies_d2h, copies_d2d;
   int64_t h2d_bytes, d2h_bytes;
-  int64_t slot_waits;       /* dispatches that had to wait for a buffer set */
+  int64_t slot_waits;       /* jobs that took over a buffer set whose previous job was still on
+                               the GPU (ordered behind its last stage by an event wait) */
   int64_t polls;
   double wall_seconds;      /* host wall time of the run incl. drain */
   double release_lag_max;   /* worst delay between a nominal release and its processing */
@@ -67,6 +68,9 @@ typedef struct daris_exec_stats {
   double progress_gap_max;  /* longest time with stages in flight and no completion observed */
   int64_t stalls;           /* GPU-wide stalls: progress gaps above the stall threshold */
   double first_stall_at;    /* executor time of the first stall (-1 if none) */
+  int64_t slot_deferred;    /* stage-0 launches held (stream kept) until a buffer set freed up:
+                               more live jobs of one task than it has buffer sets */
+  int64_t slot_backlog_max; /* most admitted jobs of one task waiting for a buffer set */
 } daris_exec_stats;
 
 typedef struct daris_exec daris_exec;
@@ -108,6 +112,9 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
  * shows ~1.7 ms whole-GPU pauses every few seconds (tools/freeze_probe.cu), so
  * runs can tell an environmental pause from a scheduling failure. */
 int daris_exec_set_stall_threshold(daris_exec* ex, double seconds);
+/* (start, length) in executor seconds of every stall of the last run that ended
+ * in a completion; returns the number of pairs (copies min(n, cap_pairs)) */
+int64_t daris_exec_stall_copy(const daris_exec* ex, double* buf, int64_t cap_pairs);
 
 int64_t daris_exec_trace_count(const daris_exec* ex);
 int64_t daris_exec_trace_copy(const daris_exec* ex, daris_stage_trace* buf, int64_t cap);
@@ -115,9 +122,13 @@ int64_t daris_exec_trace_copy(const daris_exec* ex, daris_stage_trace* buf, int6
 /* Full-load (AFET) calibration on the real GPU: every (context, stream) slot
  * loops jobs of the tasks in `slot_tasks` (n_contexts*n_streams entries, slot 0
  * is the target) for `seconds`; returns the mean job time of each task id seen
- * in slot 0 position rotations (out[i] for task id i+1, 0 if unseen). */
+ * in slot 0 position rotations (out[i] for task id i+1, 0 if unseen).
+ * task_hp (nullable, indexed by task id - 1): nonzero launches that task's
+ * stages on the high-priority streams, as daris_exec_run does for HP tasks, so
+ * the baseline is measured under the contention HP stages really see. */
 int daris_exec_busy_calibrate(daris_exec* ex, const int32_t* task_stage_counts, int32_t n_tasks,
-                              const int32_t* slot_tasks, double seconds, double* out_mean_job_time);
+                              const int32_t* slot_tasks, double seconds, double* out_mean_job_time,
+                              const int32_t* task_hp);
 
 const char* daris_exec_last_error(const daris_exec* ex);
 

@@ -23,6 +23,8 @@
 #include <string>
 #include <unordered_map>
 #include <vector>
+#include <deque>
+#include <functional>
 
 #include "../../../include/daris_exec.h"
 
@@ -78,6 +80,7 @@ struct Partition {
 
 struct Running {
   bool busy = false;
+  bool held = false;  // stage 0 dispatched onto this stream, launch held until its job gets a buffer set
   int task = 0, job = 0, stage = 0, slot = 0;
   double start = 0;
   int ev = -1;  // index of the stage's timing-event pair (DARIS_GPU_TIMING)
@@ -109,11 +112,14 @@ struct daris_exec {
   std::vector<Pool> pools;
   std::vector<cudaEvent_t> slot_free;  // per (task, slot)
   std::vector<cudaEvent_t> in_ready;   // per (task, slot): the job's input copy is done
-  std::vector<int> slot_owner;          // job id using the buffer set, 0 = free
+  std::vector<int> slot_owner;          // job id holding the buffer set, 0 = free
+  std::vector<char> slot_handoff;       // holder has launched its last stage: slot_free is recorded, the
+                                        // set may pass to the next job behind a GPU event wait
   std::vector<daris_stage_trace> trace;
   std::string err;
   int64_t graph_count = 0;
   double stall_threshold = 1e-3;
+  std::vector<double> stall_log;  // (start, length) pairs of the last run's GPU-wide stalls
   // DARIS_EXEC_FLAGS=1: stage completion as a stream memory write of a sequence
   // number into host-mapped memory (one word per (context, stream) slot), polled
   // with a plain load instead of cudaEventQuery
@@ -295,6 +301,7 @@ int daris_exec_create(const daris_exec_config* cfg, daris_exec** out, char* err,
   ex->dev_in.assign(ns, nullptr);
   ex->dev_out.assign(ns, nullptr);
   ex->slot_owner.assign(ns, 0);
+  ex->slot_handoff.assign(ns, 0);
   ex->slot_free.resize(ns);
   ex->in_ready.resize(ns);
   for (auto* v : {&ex->slot_free, &ex->in_ready})
@@ -420,6 +427,12 @@ int daris_exec_set_pool(daris_exec* ex, int32_t task, const void* pool, int32_t 
   return DARIS_OK;
 }
 
+int64_t daris_exec_stall_copy(const daris_exec* ex, double* buf, int64_t cap_pairs) {
+  const int64_t n = static_cast<int64_t>(ex->stall_log.size() / 2);
+  if (buf) std::memcpy(buf, ex->stall_log.data(), sizeof(double) * 2 * static_cast<size_t>(std::min(n, cap_pairs)));
+  return n;
+}
+
 int daris_exec_set_stall_threshold(daris_exec* ex, double seconds) {
   if (!(seconds > 0)) return fail(ex, "stall threshold must be positive");
   ex->stall_threshold = seconds;
@@ -517,8 +530,10 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
       }
   }
   ex->trace.clear();
+  ex->stall_log.clear();
   // every buffer set is idle between runs (each run ends with a device sync)
   std::fill(ex->slot_owner.begin(), ex->slot_owner.end(), 0);
+  std::fill(ex->slot_handoff.begin(), ex->slot_handoff.end(), 0);
   daris_exec_stats st{};
   Acc acc;
   acc.warmup = warmup;
@@ -610,18 +625,35 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
   staged_in.reserve(1024);
   const char* sie = std::getenv("DARIS_STAGE_INPUT");  // 0: copy at stage-0 dispatch on the stage's stream
   const bool input_at_admission = !(sie && sie[0] == '0');
-  auto stage_input = [&](int task, int job, int context) -> int {
+  // Buffer sets (activations, split-K workspace and counters, input / output)
+  // are owned by one job at a time, tracked here on the host. A set passes to
+  // the next job of its task only once the holder has LAUNCHED its last stage
+  // (slot_free recorded after it: the new job's first GPU work waits on that
+  // event) or has completed. A job admitted while every set of its task is
+  // held waits in a per-task FIFO with no input staged; if its stage 0 is
+  // dispatched first, the launch is held on the stream it was given until a
+  // set frees up (the stage's time includes the wait, as a busy stream would).
+  std::vector<std::deque<int>> slot_queue(n_tasks + 1);
+  std::unordered_map<int, int> job_ctx;       // job -> context it was admitted into (copy stream)
+  std::unordered_map<int, char> job_waits;    // job took over a set still in use on the GPU
+  std::deque<std::pair<int, int>> held;       // (context, stream) of held stage-0 launches, FIFO
+  job_ctx.reserve(1024);
+  job_waits.reserve(1024);
+  int n_held = 0;
+  auto acquire_slot = [&](int task) -> std::pair<int, bool> {  // (slot, needs GPU wait) or (-1, _)
+    for (int q = 0; q < c.slots_per_task; ++q)
+      if (ex->slot_owner[ex->sidx(task, q)] == 0) return {q, false};
+    for (int q = 0; q < c.slots_per_task; ++q)
+      if (ex->slot_handoff[ex->sidx(task, q)]) return {q, true};
+    return {-1, false};
+  };
+  auto stage_input = [&](int task, int job) -> int {
     if (!input_at_admission) return DARIS_OK;
     const auto& pool = ex->pools[task - 1];
     const size_t si = ex->sidx(task, job_slot[job]);
     if (!(pool.src && pool.n > 0 && ex->dev_in[si])) return DARIS_OK;
-    cudaStream_t cs = copy_streams[context - 1];
-    const int owner = ex->slot_owner[si];
-    if (owner != 0 && owner != job) {  // the buffer set's previous job may still be reading it
-      CUDA_TRY(ex, cudaStreamWaitEvent(cs, ex->slot_free[si], 0));
-      st.slot_waits++;
-    }
-    ex->slot_owner[si] = job;
+    cudaStream_t cs = copy_streams[job_ctx[job] - 1];
+    if (job_waits[job]) CUDA_TRY(ex, cudaStreamWaitEvent(cs, ex->slot_free[si], 0));
     const char* src = pool.src + static_cast<int64_t>(job_seq[job] % pool.n) * pool.in_bytes;
     CUDA_TRY(ex, cudaMemcpyAsync(ex->dev_in[si], src, static_cast<size_t>(pool.in_bytes),
                                  pool.on_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, cs));
@@ -635,21 +667,73 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
     }
     return DARIS_OK;
   };
-  auto launch = [&](const daris_stage_ref& r) -> int {
+  // give `job` buffer set `q`: claim it and stage the job's input
+  auto assign_slot = [&](int task, int job, std::pair<int, bool> got) -> int {
+    const size_t si = ex->sidx(task, got.first);
+    ex->slot_owner[si] = job;
+    ex->slot_handoff[si] = 0;
+    job_slot[job] = got.first;
+    job_waits[job] = got.second ? 1 : 0;
+    if (got.second) st.slot_waits++;
+    return stage_input(task, job);
+  };
+  std::function<int(const daris_stage_ref&)> launch;
+  std::vector<std::vector<daris_stage_ref>> held_ref(c.n_contexts, std::vector<daris_stage_ref>(c.n_streams));
+  // a set of `task` may have freed up: serve its FIFO, then any held stage-0 launches
+  auto serve_slot_queue = [&](int task) -> int {
+    auto& qd = slot_queue[task];
+    while (!qd.empty()) {
+      const auto got = acquire_slot(task);
+      if (got.first < 0) break;
+      const int job = qd.front();
+      qd.pop_front();
+      const int rc = assign_slot(task, job, got);
+      if (rc != DARIS_OK) return rc;
+    }
+    for (;;) {  // launch (FIFO) every held stage 0 whose job now has a set; launch may recurse
+      auto it = std::find_if(held.begin(), held.end(), [&](const std::pair<int, int>& cs) {
+        const daris_stage_ref& r = held_ref[cs.first - 1][cs.second];
+        auto js = job_slot.find(r.job);
+        return r.task == task && js != job_slot.end() && js->second >= 0;
+      });
+      if (it == held.end()) break;
+      const daris_stage_ref r = held_ref[it->first - 1][it->second];
+      run[it->first - 1][it->second].held = false;
+      held.erase(it);
+      n_held--;
+      const int rc = launch(r);
+      if (rc != DARIS_OK) return rc;
+    }
+    return DARIS_OK;
+  };
+  launch = [&](const daris_stage_ref& r) -> int {
     Partition& p = ex->parts[r.context - 1];
     const TaskInfo& t = info[r.task];
     cudaStream_t s = (t.prio == DARIS_HP ? p.streams_hi : p.streams)[r.stream];
+    Running& rr = run[r.context - 1][r.stream];
+    if (r.stage == 0 && job_slot[r.job] < 0) {  // no buffer set yet: hold the launch on this stream
+      rr.busy = true;
+      rr.held = true;
+      rr.task = r.task;
+      rr.job = r.job;
+      rr.stage = r.stage;
+      rr.slot = -1;
+      rr.start = r.started_at;
+      rr.ev = -1;
+      held_ref[r.context - 1][r.stream] = r;
+      held.push_back({r.context, r.stream});
+      n_held++;
+      st.slot_deferred++;
+      return DARIS_OK;
+    }
     const int slot = job_slot[r.job];
     const size_t si = ex->sidx(r.task, slot);
     if (r.stage == 0) {
       if (staged_in.count(r.job)) {
-        CUDA_TRY(ex, cudaStreamWaitEvent(s, ex->in_ready[si], 0));
+        CUDA_TRY(ex, cudaStreamWaitEvent(s, ex->in_ready[si], 0));  // orders behind slot_free too
         staged_in.erase(r.job);
       } else {
-        if (ex->slot_owner[si] != 0 && ex->slot_owner[si] != r.job) {
-          CUDA_TRY(ex, cudaStreamWaitEvent(s, ex->slot_free[si], 0));
-          st.slot_waits++;
-        }
+        if (job_waits[r.job]) CUDA_TRY(ex, cudaStreamWaitEvent(s, ex->slot_free[si], 0));
         const auto& pool = ex->pools[r.task - 1];
         if (!input_at_admission && pool.src && pool.n > 0 && ex->dev_in[si]) {
           const char* src = pool.src + static_cast<int64_t>(job_seq[r.job] % pool.n) * pool.in_bytes;
@@ -663,7 +747,6 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
           }
         }
       }
-      ex->slot_owner[si] = r.job;
     }
     cudaGraphExec_t g = ex->graphs[ex->gidx(r.task, r.stage, r.context, slot)];
     if (!g) return fail(ex, "no graph for dispatched stage", DARIS_E_INTERNAL);
@@ -676,6 +759,23 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
     CUDA_TRY(ex, cudaGraphLaunch(g, s));
     if (ev >= 0) CUDA_TRY(ex, cudaEventRecord(tev[ev + 1], s));
     st.graph_launches++;
+    if (use_flags) {
+      const size_t fi = static_cast<size_t>((r.context - 1) * c.n_streams + r.stream);
+      if (driver().writeValue32(reinterpret_cast<CUstream>(s), ex->flags_dev + fi * sizeof(uint32_t), ++flag_seq[fi],
+                                CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+        return fail(ex, "cuStreamWriteValue32 failed", DARIS_E_INTERNAL);
+    } else {
+      CUDA_TRY(ex, cudaEventRecord(p.done[r.stream], s));
+    }
+    rr.busy = true;
+    rr.held = false;
+    rr.task = r.task;
+    rr.job = r.job;
+    rr.stage = r.stage;
+    rr.slot = slot;
+    rr.start = r.started_at;
+    rr.ev = ev;
+    in_flight++;
     if (r.stage == t.n_stages - 1) {
       const auto& pool = ex->pools[r.task - 1];
       if (pool.host_out && pool.out_bytes > 0 && ex->dev_out[si]) {
@@ -685,24 +785,9 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
         st.d2h_bytes += pool.out_bytes;
       }
       CUDA_TRY(ex, cudaEventRecord(ex->slot_free[si], s));
+      ex->slot_handoff[si] = 1;  // the set may now pass on behind slot_free
+      if (!slot_queue[r.task].empty()) return serve_slot_queue(r.task);
     }
-    if (use_flags) {
-      const size_t fi = static_cast<size_t>((r.context - 1) * c.n_streams + r.stream);
-      if (driver().writeValue32(reinterpret_cast<CUstream>(s), ex->flags_dev + fi * sizeof(uint32_t), ++flag_seq[fi],
-                                CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
-        return fail(ex, "cuStreamWriteValue32 failed", DARIS_E_INTERNAL);
-    } else {
-      CUDA_TRY(ex, cudaEventRecord(p.done[r.stream], s));
-    }
-    Running& rr = run[r.context - 1][r.stream];
-    rr.busy = true;
-    rr.task = r.task;
-    rr.job = r.job;
-    rr.stage = r.stage;
-    rr.slot = slot;
-    rr.start = r.started_at;
-    rr.ev = ev;
-    in_flight++;
     return DARIS_OK;
   };
 
@@ -778,11 +863,18 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
         push_log(h, tr, DARIS_LOG_REJECT, tid, job_counter);
       } else {
         push_log(h, tr, DARIS_LOG_ADMIT, tid, job_counter, -1, pl.context);
-        job_slot[job_counter] = static_cast<int>(seq[tid] % c.slots_per_task);
         job_seq[job_counter] = static_cast<int>(seq[tid]);
         job_rel[job_counter] = tr;
-        status = stage_input(tid, job_counter, pl.context);
-        if (status != DARIS_OK) break;
+        job_ctx[job_counter] = pl.context;
+        job_slot[job_counter] = -1;
+        const auto got = slot_queue[tid].empty() ? acquire_slot(tid) : std::make_pair(-1, false);
+        if (got.first >= 0) {
+          status = assign_slot(tid, job_counter, got);
+          if (status != DARIS_OK) break;
+        } else {
+          slot_queue[tid].push_back(job_counter);
+          st.slot_backlog_max = std::max<int64_t>(st.slot_backlog_max, static_cast<int64_t>(slot_queue[tid].size()));
+        }
       }
       seq[tid] += 1;
       rel_idx[tid] += 1;
@@ -798,7 +890,7 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
     for (int k = 0; k < c.n_contexts; ++k)
       for (int s = 0; s < c.n_streams; ++s) {
         Running& rr = run[k][s];
-        if (!rr.busy) continue;
+        if (!rr.busy || rr.held) continue;
         st.polls++;
         cudaError_t q;
         if (use_flags) {
@@ -815,6 +907,10 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
         }
         if (q == cudaSuccess) {
           done.push_back({k + 1, s, rr.job, rr.stage});
+          if (in_stall) {
+            ex->stall_log.push_back(last_progress);
+            ex->stall_log.push_back(raw_now - last_progress);
+          }
           last_progress = raw_now;
           in_stall = false;
         }
@@ -856,7 +952,11 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
       in_flight--;
       if (job_done) {
         push_log(h, t, DARIS_LOG_JOB_COMPLETE, rr.task, rr.job, -1, d.ctx);
-        ex->slot_owner[ex->sidx(rr.task, rr.slot)] = 0;
+        const size_t si_done = ex->sidx(rr.task, rr.slot);
+        if (ex->slot_owner[si_done] == rr.job) {  // not yet handed to a later job
+          ex->slot_owner[si_done] = 0;
+          ex->slot_handoff[si_done] = 0;
+        }
         const double released = job_rel[rr.job];
         if (released >= acc.warmup) {
           const int hp = info[rr.task].prio == DARIS_HP ? 0 : 1;
@@ -868,12 +968,26 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
         job_slot.erase(rr.job);
         job_rel.erase(rr.job);
         job_seq.erase(rr.job);
+        job_ctx.erase(rr.job);
+        job_waits.erase(rr.job);
+        if (!slot_queue[rr.task].empty()) {
+          status = serve_slot_queue(rr.task);
+          if (status != DARIS_OK) break;
+        }
       }
       status = refill(t);
       if (status != DARIS_OK) break;
       progressed = true;
     }
     if (status != DARIS_OK) break;
+    if (in_flight == 0 && n_held > 0 && now <= duration) {
+      // held stage-0 launches occupy streams while the jobs holding their task's
+      // buffer sets have nothing on the GPU: none of them can ever progress
+      status = fail(ex, "buffer sets exhausted: " + std::to_string(n_held) +
+                            " stage-0 launches wait for a buffer set while no stage is in flight "
+                            "(more live jobs of a task than its buffer slots; raise slots)", DARIS_E_INTERNAL);
+      break;
+    }
     if (heap.empty() && in_flight == 0) {
       if (now > duration) break;
       int32_t ready = 0;
@@ -931,7 +1045,8 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
 }
 
 int daris_exec_busy_calibrate(daris_exec* ex, const int32_t* task_stage_counts, int32_t n_tasks,
-                              const int32_t* slot_tasks, double seconds, double* out_mean_job_time) {
+                              const int32_t* slot_tasks, double seconds, double* out_mean_job_time,
+                              const int32_t* task_hp) {
   using clock = std::chrono::steady_clock;
   const daris_exec_config& c = ex->cfg;
   const int n_slots = c.n_contexts * c.n_streams;
@@ -958,8 +1073,10 @@ int daris_exec_busy_calibrate(daris_exec* ex, const int32_t* task_stage_counts, 
     Partition& p = ex->parts[l.ctx - 1];
     cudaGraphExec_t g = ex->graphs[ex->gidx(l.task, l.stage, l.ctx, l.slot)];
     if (!g) return fail(ex, "calibration needs graphs for every task in every context");
-    CUDA_TRY(ex, cudaGraphLaunch(g, p.streams[l.stream]));
-    CUDA_TRY(ex, cudaEventRecord(p.done[l.stream], p.streams[l.stream]));
+    // the stream class daris_exec_run launches this task's stages on (HP: high priority)
+    cudaStream_t strm = (task_hp && task_hp[l.task - 1] ? p.streams_hi : p.streams)[l.stream];
+    CUDA_TRY(ex, cudaGraphLaunch(g, strm));
+    CUDA_TRY(ex, cudaEventRecord(p.done[l.stream], strm));
     return DARIS_OK;
   };
   for (auto& l : loops) {

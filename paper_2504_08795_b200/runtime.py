@@ -57,7 +57,8 @@ class ExecStatsC(C.Structure):
                 ("copies_d2d", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("slot_waits", C.c_int64), ("polls", C.c_int64), ("wall_seconds", C.c_double),
                 ("release_lag_max", C.c_double), ("loop_gap_max", C.c_double),
-                ("progress_gap_max", C.c_double), ("stalls", C.c_int64), ("first_stall_at", C.c_double)]
+                ("progress_gap_max", C.c_double), ("stalls", C.c_int64), ("first_stall_at", C.c_double),
+                ("slot_deferred", C.c_int64), ("slot_backlog_max", C.c_int64)]
 
 
 _exec_lib = None
@@ -79,7 +80,7 @@ def exec_lib() -> C.CDLL:
             "daris_exec_set_io": [vp, i32, i32, vp, vp],
             "daris_exec_set_pool": [vp, i32, vp, i32, i32, i64, vp, i64],
             "daris_exec_run": [vp, vp, f64, f64, P(f64), i32, P(_core.ReportC), P(ExecStatsC)],
-            "daris_exec_busy_calibrate": [vp, P(i32), i32, P(i32), f64, P(f64)],
+            "daris_exec_busy_calibrate": [vp, P(i32), i32, P(i32), f64, P(f64), P(i32)],
             "daris_exec_set_stall_threshold": [vp, f64],
             "daris_exec_time_graph": [vp, i32, i32, i32, i32, i32, P(f64)],
         }
@@ -95,6 +96,8 @@ def exec_lib() -> C.CDLL:
         L.daris_exec_trace_count.restype = C.c_int64
         L.daris_exec_trace_copy.argtypes = [vp, P(StageTraceC), i64]
         L.daris_exec_trace_copy.restype = C.c_int64
+        L.daris_exec_stall_copy.argtypes = [vp, P(f64), i64]
+        L.daris_exec_stall_copy.restype = C.c_int64
         L.daris_exec_quantum.argtypes = []
         L.daris_exec_quantum.restype = C.c_double
         _exec_lib = L
@@ -194,16 +197,26 @@ class Executor:
         self._gpu_times = [(a.gpu_start, a.gpu_end) for a in list(arr)[:n]]
         return [(a.task, a.job, a.stage, a.context, a.stream, a.slot, a.start, a.end) for a in list(arr)[:n]]
 
+    def stall_log(self) -> list[tuple[float, float]]:
+        """(start, length) of each GPU-wide stall of the last run (executor seconds)."""
+        L = exec_lib()
+        n = L.daris_exec_stall_copy(self._h, None, 0)
+        buf = (C.c_double * max(2, 2 * n))()
+        L.daris_exec_stall_copy(self._h, buf, n)
+        return [(buf[2 * i], buf[2 * i + 1]) for i in range(n)]
+
     def trace_gpu(self) -> list[tuple[float, float]]:
         """Device-side (start, end) of each traced stage, aligned with trace()
         (NaN unless the run had DARIS_GPU_TIMING set)."""
         return getattr(self, "_gpu_times", [])
 
-    def busy_calibrate(self, stage_counts: Sequence[int], slot_tasks: Sequence[int], seconds: float) -> float:
+    def busy_calibrate(self, stage_counts: Sequence[int], slot_tasks: Sequence[int], seconds: float,
+                       task_hp: Sequence[bool] | None = None) -> float:
         sc = (C.c_int32 * len(stage_counts))(*stage_counts)
         st = (C.c_int32 * len(slot_tasks))(*slot_tasks)
+        hp = (C.c_int32 * len(stage_counts))(*[int(bool(x)) for x in task_hp]) if task_hp is not None else None
         out = C.c_double()
-        self._c(exec_lib().daris_exec_busy_calibrate(self._h, sc, len(stage_counts), st, seconds, C.byref(out)),
+        self._c(exec_lib().daris_exec_busy_calibrate(self._h, sc, len(stage_counts), st, seconds, C.byref(out), hp),
                 "busy_calibrate")
         return out.value
 
@@ -245,6 +258,65 @@ class RunResult:
     periods: dict
     stage_nominal: dict
     partitions: list
+    log: np.ndarray | None = None        # the raw native event log (_core.LOG_DTYPE)
+    stalls: list = field(default_factory=list)  # (start, length) of GPU-wide stalls
+    batch: dict = field(default_factory=dict)   # images per job, by task id
+
+    def windows(self, warmup: float, step: float, n_steps: int) -> list[dict]:
+        return window_stats(self.log, self.periods, {t.id for t in self.tasks if t.priority is Priority.HP},
+                            warmup, step, n_steps, self.stalls, self.batch)
+
+
+def window_stats(log: np.ndarray, periods: dict[int, float], hp_ids: set[int], warmup: float, step: float,
+                 n_steps: int, stalls=(), batch: dict[int, int] | None = None) -> list[dict]:
+    """Per-window accounting of a run's event log. Window k holds the jobs
+    RELEASED in [warmup + k*step, warmup + (k+1)*step). A job misses when it
+    completes after release + D (D = T), or when it was admitted, has not
+    completed, and its deadline release + D has passed by the end of the log
+    (the run's horizon) — a backlog cannot hide misses. LP loss counts misses
+    and admission rejections over LP releases. `stalls` are the executor's
+    GPU-wide stalls; each window notes how many began inside the time its
+    jobs were live (release to deadline)."""
+    kind, t, task, job = log["kind"], log["time"], log["task"], log["job"]
+    horizon = float(t[kind == 6][0]) if (kind == 6).any() else float(t.max())
+    n = int(job.max()) + 1 if len(job) else 1
+    rel_t = np.full(n, np.nan)
+    rel_task = np.zeros(n, dtype=np.int64)
+    done_t = np.full(n, np.nan)
+    rejected = np.zeros(n, dtype=bool)
+    m = kind == 0
+    rel_t[job[m]] = t[m]
+    rel_task[job[m]] = task[m]
+    rejected[job[kind == 2]] = True
+    m = kind == 5
+    done_t[job[m]] = t[m]
+    ids = np.nonzero(~np.isnan(rel_t))[0]
+    per = np.array([periods[int(k)] for k in rel_task[ids]])
+    dl = rel_t[ids] + per
+    finished = ~np.isnan(done_t[ids])
+    missed = ~rejected[ids] & ((finished & (done_t[ids] > dl)) | (~finished & (dl <= horizon)))
+    is_hp = np.isin(rel_task[ids], list(hp_ids))
+    imgs = np.array([(batch or {}).get(int(k), 1) for k in rel_task[ids]])
+    win = np.floor((rel_t[ids] - warmup) / step).astype(np.int64)
+    st_start = np.array([a for a, _ in stalls]) if len(stalls) else np.zeros(0)
+    out = []
+    for k in range(n_steps):
+        sel = win == k
+        hp, lp = sel & is_hp, sel & ~is_hp
+        lo, hi = warmup + k * step, warmup + (k + 1) * step
+        rel_lp = int(lp.sum())
+        lost_lp = int((lp & (missed | rejected[ids])).sum())
+        out.append({"released_hp": int(hp.sum()), "released_lp": rel_lp, "missed_hp": int((hp & missed).sum()),
+                    "missed_lp": int((lp & missed).sum()), "rejected_lp": int((lp & rejected[ids]).sum()),
+                    "lp_loss": lost_lp / rel_lp if rel_lp else 0.0,
+                    "completed_images": int(imgs[sel & finished & (done_t[ids] <= horizon)].sum()),
+                    "stalls": int(((st_start >= lo) & (st_start < hi + max(periods.values()))).sum())})
+    return out
+
+
+def window_ok(w: dict) -> bool:
+    """HP miss = 0 and LP loss (misses + rejections) < 2 % in one window."""
+    return w["missed_hp"] == 0 and w["lp_loss"] < 0.02 and w["released_hp"] + w["released_lp"] > 0
 
 
 class DarisRuntime:
@@ -437,7 +509,8 @@ class DarisRuntime:
                     c = rng.choice(ids)
                     if slot_tasks.count(c) < self.exec.slots:
                         slot_tasks.append(c)
-                by_model[t.key] = quantize(max(self.exec.busy_calibrate(counts, slot_tasks, seconds),
+                hp = [x.priority is Priority.HP for x in self.tasks]
+                by_model[t.key] = quantize(max(self.exec.busy_calibrate(counts, slot_tasks, seconds, hp),
                                                  2 * QUANTUM))
             out[t.id] = by_model[t.key]
         self.afet = out
@@ -480,12 +553,13 @@ class DarisRuntime:
                                                 f"{self.gpu.oversubscription:g}", config=self.gpu,
                                     seed=self.seed)
         stats = {f: getattr(st, f) for f, _ in ExecStatsC._fields_}
-        records = _core.records_from_array(h.log_array())
+        log = h.log_array()
+        records = _core.records_from_array(log)
         from .scheduler import AdmissionDecision
         admissions = [AdmissionDecision.from_native(a) for a in h.audits()]
         return RunResult(report, stats, self.exec.trace(), records, admissions, full_load, phases,
                          self.specs(), {t.id: t.period for t in self.tasks}, self.stage_nominal,
-                         self.exec.partitions)
+                         self.exec.partitions, log, self.exec.stall_log(), {t.id: t.batch for t in self.tasks})
 
     def close(self) -> None:
         self.exec.close()

@@ -6,6 +6,7 @@ import pytest
 import torch
 
 from oracle import stagesim_oracle as O
+from paper_2504_08795_b200 import nets
 from paper_2504_08795_b200.gpu import GpuConfig, Policy
 from paper_2504_08795_b200.model import Priority
 from paper_2504_08795_b200.runtime import DarisRuntime, TaskDef, quantize
@@ -100,4 +101,46 @@ def test_batched_jobs_count_images_and_replay():
     recs, _, _, _ = O.simulate(otasks, ogpu, duration=0.5, warmup_frac=0.1, durations=durations,
                                phases_override={s.id: ph for s, ph in zip(res.tasks, res.phases)})
     assert _decisions(res.records, 0.5) == _decisions(recs, 0.5)
+    rt.close()
+
+
+def test_buffer_sets_never_shared_under_backlog():
+    """More live jobs of one task than it has buffer sets (an HP task released
+    far faster than it completes; HP jobs are never admission-tested): a job
+    takes over a set only after the holder launched its last stage (ordered
+    behind it on the GPU), later jobs wait in a FIFO and hold their stage-0
+    launch. Every buffer set's final logits must be those of the last job that
+    used it, computed from that job's own input image — any overlap of two jobs
+    on one set (activations, split-K scratch / counters) would corrupt them —
+    and a normal run afterwards must still be exact."""
+    gpu = GpuConfig(148, 1, 3, 1.0, Policy.STR)
+    tasks = [TaskDef(1, "resnet50", Priority.HP, 20000.0, 4)]
+    rt = DarisRuntime(tasks, gpu, slots=2, phasing="zero")
+    rt.capture_all()
+    rt.afet = {1: 1e-3}
+    res = rt.run(duration=0.05, warmup=0.0, full_load=rt.afet)
+    st = res.stats
+    assert st["slot_deferred"] > 0 and st["slot_backlog_max"] >= 2, st
+    assert res.report.completed_hp > 10
+    net = rt.net_of(rt.tasks[0])
+    pool = rt.pools[1]
+    ref_tb = nets.allocate_buffers(net, rt.plan_of(rt.tasks[0]))
+
+    def logits(img_index):
+        out = nets.forward(net, ref_tb, pool[img_index:img_index + 1], stream=None,
+                           sm_budget=rt.plan_of(rt.tasks[0])).float().cpu().clone()
+        torch.cuda.synchronize()
+        return out
+
+    last = {}
+    n_st = net.n_stages
+    for t in res.trace:   # (task, job, stage, ctx, stream, slot, start, end, ...)
+        if t[2] == n_st - 1 and (t[5] not in last or t[7] >= last[t[5]][1]):
+            last[t[5]] = (t[1], t[7])
+    assert len(last) == 2
+    for slot, (job, _) in last.items():
+        got = rt.buffers[(1, slot)].output.float().cpu()
+        want = logits((job - 1) % rt.pool_size)   # one task, no rejections: job j used image j-1
+        cos = torch.nn.functional.cosine_similarity(got.flatten(), want.flatten(), dim=0).item()
+        assert cos > 0.9999, (slot, job, cos)
     rt.close()
