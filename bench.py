@@ -129,7 +129,8 @@ def dist_init():
     if world > 1:
         import torch.distributed as dist
         import torch
-        torch.cuda.set_device(local)
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
         dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
     return world, rank, local
 
@@ -165,33 +166,23 @@ def c2_tasks(rate: float, ids: list[int], batch: int = 1):
 
 def daris_batched(args, gpu, mine, log, batch: int = 4) -> dict:
     """The paper's "DARIS with batched inputs" variant: the
-    same 8-task C2 schedule, every job a batch of `batch` images. Reported next
-    to the batch-1 headline (which BASELINE.json's config fixes) and to the
-    single-tenant batching baseline."""
+    same 8-task C2 schedule, every job a batch of `batch` images, measured with
+    the headline's protocol. Reported next to the batch-1 headline (which
+    BASELINE.json's config fixes) and to the single-tenant batching baseline."""
     from paper_2504_08795_b200.runtime import DarisRuntime
     rt = DarisRuntime(c2_tasks(100.0, mine, batch), gpu, slots=3, seed=0)
     rt.capture_all()
     rt.afet = rt.calibrate_full_load(0.2)
     guess = 0.6 * (gpu.n_contexts * gpu.n_streams) / max(rt.afet.values()) / len(mine)
-    rate = knee_search(rt, guess, min(args.probe_seconds, 0.6), log)
+    rate = knee_search(rt, guess, args.probe_seconds, args.step_seconds, log)
     rate = all_reduce([rate], "min")[0]
-    step, dur = args.step_seconds, (args.warmup + args.steps) * args.step_seconds
-    ok = False
-    for _ in range(TIMED_ATTEMPTS):
-        rt.set_rate(rate)
-        barrier()
-        res = run_clean(rt, dur, args.warmup * step, log, f"batched {rate:.0f}")[0]
-        barrier()
-        ok = all_reduce([1.0 if feasible(res.report) else 0.0], "min")[0] > 0
-        log(f"batched b{batch} rate={rate:.1f} ok={ok} inf/s={res.report.jps:.0f}")
-        if ok:
-            break
-        rate *= 0.97
-    rep = res.report
-    done = all_reduce([rep.jps], "sum")[0]  # report JPS counts images (batch per job, engine.py:153-220)
+    rate, res, s, _, _, attempts = timed_knee(rt, rate, args, log, f"batched b{batch}")
+    done = all_reduce([s["inf_per_s"]], "sum")[0]   # images (batch per job, engine.py:153-220)
     out = {"batch": batch, "value": round(done, 1), "unit": UNIT, "rate_per_task": round(rate, 2),
-           "constraints_met": bool(ok), "hp_miss": int(rep.missed_hp), "lp_loss": round(lp_loss(rep), 5),
-           "p99_hp_response_ms": round(rep.response_hp.p99 * 1e3, 3),
+           "constraints_met": bool(s["ok"]), "windows_failed": s["windows_failed"], "hp_miss": s["missed_hp"],
+           "lp_loss": round(s["lp_loss"], 5), "attempts": attempts,
+           "p99_hp_response_ms": round(res.p99_hp(args.warmup * args.step_seconds,
+                                                  (args.warmup + args.steps) * args.step_seconds) * 1e3, 3),
            "isolated_job_ms": round(sum(rt.stage_nominal[rt.tasks[0].key]) * 1e3, 3)}
     rt.close()
     return out
@@ -214,10 +205,37 @@ def feasible(rep) -> bool:
     return done > 0 and rep.missed_hp == 0 and rep.dmr_lp < 0.02 and lp_loss(rep) < 0.02
 
 
-def conv_roofline(rt, peaks) -> dict:
-    """Dominant kernel (conv_igemm_tc_kernel): algorithmic FLOPs per launch ÷ the
-    launch's CUDA-event time on a live partition stream (each op captured 10x in
-    a graph so host launch cost is excluded)."""
+TRAFFIC_FILE = ROOT / "profiles" / "r02_conv_traffic.json"
+
+
+def conv_traffic(rt) -> dict:
+    """DRAM bytes per conv launch from the committed ncu --set full capture of
+    this plan (profiles/r02_conv_traffic.json: dram__bytes_read.sum +
+    dram__bytes_write.sum per launch, with the plan parameters it was taken
+    at). Used only when those match this run's plan; else null, with why."""
+    import hashlib
+    if not TRAFFIC_FILE.exists():
+        return {"traffic": None, "traffic_note": f"no capture file {TRAFFIC_FILE.name}"}
+    raw = TRAFFIC_FILE.read_bytes()
+    d = json.loads(raw)
+    knobs = {k: v for k, v in os.environ.items() if k.startswith("DARIS_") and k != "DARIS_GPU_TIMING"}
+    want = {"plan_sms": rt.sm_budget, "model": "resnet50", "batch": 1, "knobs": knobs}
+    have = {k: d.get(k) for k in want}
+    if have != want:
+        return {"traffic": None, "traffic_note": f"capture plan {have} != this run's {want}"}
+    return {"traffic": int(d["dram_bytes_per_launch"]),
+            "traffic_source": f"{TRAFFIC_FILE.name} sha256:{hashlib.sha256(raw).hexdigest()[:16]} "
+                              f"({d['launches']} conv launches of one forward, {d['capture']})"}
+
+
+def conv_roofline(rt, peaks, loaded_stage_s: float | None = None) -> dict:
+    """Dominant kernel (conv_igemm_tc_kernel). `achieved` = algorithmic bytes per
+    conv launch / the launch's average time, each op replayed 10x back-to-back
+    in a CUDA graph on a live partition stream (CUDA events on that stream).
+    `under_load`: the same bytes over the conv share of a job's device-side
+    stage time measured inside the loaded C2 schedule (DARIS_GPU_TIMING events
+    around every stage graph), i.e. the per-launch time the kernel really gets
+    while 8 jobs share the GPU."""
     import torch
     from paper_2504_08795_b200 import nets
     net = next(iter(rt.nets.values()))
@@ -252,23 +270,48 @@ def conv_roofline(rt, peaks) -> dict:
     gbs = nbytes / t_conv / 1e9
     tflops = flops / t_conv / 1e12
     n = len(conv)
-    return {"kernel": "conv_igemm_tc_kernel", "bound": "hbm" if ai < ridge else "tensor",
-            "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": round(gbs / peaks["hbm_gbs"], 5),
-            "traffic": 1662737, "algorithmic_bytes_per_launch": nbytes // n,
-            "arithmetic_intensity_flop_per_byte": round(ai, 1), "ridge_flop_per_byte": round(ridge, 1),
-            "tensor_view": {"achieved": round(tflops, 3), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                            "frac": round(tflops / peaks["bf16_tflops"], 5)},
-            "frac_of_sm_share": round(gbs / (peaks["hbm_gbs"] * rt.sm_budget / 148), 4),
-            "traffic_note": "dram__bytes_read+write per conv launch, mean over 46 conv launches of one forward "
-                            "(76.5 MB; algorithmic weights+in+out+residual 91.9 MB), ncu --set full, "
-                            "profiles/r01_ncu_full_convs_resnet50_plan23_final.csv",
-            "algorithmic_bytes_note": "per launch: bf16 weights + input + output (+ residual / fused-branch input), "
-                                      "each read or written once",
-            "launches_per_inference": n, "flops_per_launch_avg": flops // n,
-            "avg_launch_us": round(t_conv / n * 1e6, 3), "share_of_inference": round(t_conv / t_all, 4),
-            "partition_sms": rt.partition_sms, "plan_sms": rt.sm_budget,
-            "peak_kind": f"HBM copy bandwidth ({peaks['source']}); frac_of_sm_share scales it by plan_sms/148"}
+    out = {"kernel": "conv_igemm_tc_kernel", "bound": "hbm" if ai < ridge else "tensor",
+           "achieved": round(gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+           "frac": round(gbs / peaks["hbm_gbs"], 5), **conv_traffic(rt),
+           "algorithmic_bytes_per_launch": nbytes // n,
+           "arithmetic_intensity_flop_per_byte": round(ai, 1), "ridge_flop_per_byte": round(ridge, 1),
+           "tensor_view": {"achieved": round(tflops, 3), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                           "frac": round(tflops / peaks["bf16_tflops"], 5)},
+           "algorithmic_bytes_note": "per launch: bf16 weights + input + output (+ residual / fused-branch input), "
+                                     "each read or written once",
+           "launches_per_inference": n, "flops_per_launch_avg": flops // n,
+           "avg_launch_us": round(t_conv / n * 1e6, 3), "share_of_inference": round(t_conv / t_all, 4),
+           "partition_sms": rt.partition_sms, "plan_sms": rt.sm_budget,
+           "peak_kind": f"HBM copy bandwidth, burst ({peaks['source']})"}
+    if loaded_stage_s:
+        t_load = loaded_stage_s * (t_conv / t_all)   # conv share of a job's device time under load
+        out["under_load"] = {"achieved": round(nbytes / t_load / 1e9, 1), "unit": "GB/s",
+                             "frac": round(nbytes / t_load / 1e9 / peaks["hbm_gbs"], 5),
+                             "avg_launch_us": round(t_load / n * 1e6, 3),
+                             "job_device_ms": round(loaded_stage_s * 1e3, 4),
+                             "tensor_frac": round(flops / t_load / 1e12 / peaks["bf16_tflops"], 5)}
+    return out
+
+
+def loaded_job_device_time(rt, rate: float, seconds: float = 2.0) -> float | None:
+    """Mean device-side time of one job's stage graphs (sum over its stages of
+    CUDA-event end - start) in the C2 schedule at `rate` (DARIS_GPU_TIMING)."""
+    import numpy as np
+    os.environ["DARIS_GPU_TIMING"] = "1"
+    try:
+        rt.set_rate(rate)
+        res = rt.run(duration=0.5 + seconds, warmup=0.5, full_load=rt.afet)
+        tr = res.trace
+        gt = rt.exec.trace_gpu()
+    finally:
+        del os.environ["DARIS_GPU_TIMING"]
+    per_job: dict = {}
+    for t, (a, b) in zip(tr, gt):
+        if np.isfinite(a) and np.isfinite(b) and t[6] >= 0.5:
+            per_job.setdefault(t[1], []).append(b - a)
+    n_st = next(iter(rt.nets.values())).n_stages
+    full = [sum(v) for v in per_job.values() if len(v) == n_st]
+    return float(np.mean(full)) if full else None
 
 
 def conv_algorithmic_bytes(op) -> int:
@@ -328,48 +371,51 @@ def batching_baseline(batches=(1, 2, 4, 8, 16, 32, 64), reps: int = 20) -> dict:
             "setup": f"resnet50, whole GPU ({sm} SMs, one stream), CUDA graph per forward, same kernels"}
 
 
-STALL_RETRIES = 6  # re-measurements of a window that contained a GPU-wide stall
-TIMED_ATTEMPTS = 10  # timed windows, stepping the rate down 5 % after each one that misses a deadline
+PROBE_WARMUP = 0.25   # warm-up share of a knee-search probe
+STEP_DOWN = 0.85      # rate factor after a timed run with a failing window
 
 
-def run_clean(rt, duration: float, warmup: float, log, tag: str):
-    """One scheduling window; re-measured (up to STALL_RETRIES times) when the
-    executor saw a GPU-wide stall in it. An idle B200 on this pool pauses every
-    SM for ~1.7 ms every few seconds (tools/freeze_probe.cu, profiles/), which no
-    schedule can absorb at sub-2 ms deadlines — the same re-measure rule the
-    clock record applies to hw_slowdown. Returns (result, attempts, stalls seen)."""
-    seen = 0
-    tried = []
-    for attempt in range(1, STALL_RETRIES + 2):
-        res = rt.run(duration=duration, warmup=warmup, full_load=rt.afet)
-        st = res.stats
-        seen += st["stalls"]
-        if st["stalls"] == 0:
-            return res, attempt, seen
-        tried.append(res)
-        log(f"{tag}: GPU-wide stall at t={st['first_stall_at']:.3f}s "
-            f"(progress gap {st['progress_gap_max'] * 1e3:.2f} ms, ok={feasible(res.report)}), re-measuring")
-    # every attempt saw a stall: keep the best feasible one (else the last)
-    ok = [r for r in tried if feasible(r.report)]
-    best = max(ok, key=lambda r: r.report.completed_hp + r.report.completed_lp) if ok else tried[-1]
-    return best, len(tried), seen
+def run_windows(rt, warmup_s: float, step: float, n: int):
+    """One continuous run: `warmup_s` of warm-up, then `n` windows of `step`
+    seconds of periodic releases. Returns (result, per-window accounting)."""
+    res = rt.run(duration=warmup_s + n * step, warmup=warmup_s, full_load=rt.afet)
+    return res, res.windows(warmup_s, step, n)
 
 
-def knee_search(rt, build_rate: float, probe_s: float, log, set_rate=None) -> float:
-    """Per-task rate with the highest completed inferences/s among feasible
-    ones (HP miss = 0, LP DMR < 2 %). DMR counts only admitted LP jobs
-    (engine.py:153-220), so past the knee admission control rejects LP jobs and
-    a feasible rate can complete fewer: grow x1.25 while feasible and not
-    losing throughput, then bisect towards the best feasible rate."""
+def summarize(ws: list[dict], step: float) -> dict:
+    from paper_2504_08795_b200.runtime import window_ok
+    failed = [k for k, w in enumerate(ws) if not window_ok(w)]
+    first_stall = next((k for k, w in enumerate(ws) if w["stalls"] > 0), None)
+    # a failing window is pause-related when a GPU-wide pause began in it or in
+    # an earlier window (an LP task whose MRET sample took a pause can stay
+    # rejected until it completes a job: timing.py:92-114, admission never lets
+    # it complete one)
+    no_pause = [k for k in failed if first_stall is None or k < first_stall]
+    rel_lp = sum(w["released_lp"] for w in ws)
+    return {"ok": not failed, "windows": len(ws), "windows_failed": len(failed),
+            "windows_failed_without_pause": len(no_pause), "stalls": sum(w["stalls"] for w in ws),
+            "inf_per_s": sum(w["completed_images"] for w in ws) / (len(ws) * step),
+            "missed_hp": sum(w["missed_hp"] for w in ws), "missed_lp": sum(w["missed_lp"] for w in ws),
+            "rejected_lp": sum(w["rejected_lp"] for w in ws), "released_lp": rel_lp,
+            "lp_loss": (sum(w["missed_lp"] + w["rejected_lp"] for w in ws) / rel_lp) if rel_lp else 0.0}
+
+
+def knee_search(rt, build_rate: float, probe_s: float, step: float, log, set_rate=None) -> float:
+    """Per-task rate with the most completed inferences/s among rates whose
+    probe run has every `step` window feasible (HP miss 0, LP loss < 2 %; an
+    LP job rejected by admission counts as lost: past the knee admission flips
+    into rejecting LP jobs, which the reference's DMR would call feasible).
+    Grow x1.25 while feasible and not losing throughput, then bisect."""
     set_rate = set_rate or rt.set_rate
+    n = max(1, int(round(probe_s / step)))
 
     def probe(r, tag):
         set_rate(r)
-        rep = run_clean(rt, probe_s, probe_s * 0.25, log, f"{tag} {r:.0f}")[0].report
-        ok = feasible(rep)
-        log(f"{tag} rate={r:.4g} ok={ok} jps={rep.jps:.0f} miss_hp={rep.missed_hp} dmr_lp={rep.dmr_lp:.3f} "
-            f"rej_lp={rep.rejected_lp} p99_hp={rep.response_hp.p99 * 1e3:.3f}ms")
-        return ok, rep.jps
+        res, ws = run_windows(rt, probe_s * PROBE_WARMUP, step, n)
+        s = summarize(ws, step)
+        log(f"{tag} rate={r:.4g} ok={s['ok']} inf/s={s['inf_per_s']:.0f} failed={s['windows_failed']}/{n} "
+            f"miss_hp={s['missed_hp']} lp_loss={s['lp_loss']:.3f} stalls={s['stalls']}")
+        return s["ok"], s["inf_per_s"]
 
     best_r, best_j = 0.0, -1.0
     lo, hi = 0.0, None
@@ -388,7 +434,15 @@ def knee_search(rt, build_rate: float, probe_s: float, log, set_rate=None) -> fl
             break
     if hi is None:
         return best_r
-    for _ in range(5):
+    if lo == 0.0:  # the first probe already failed: walk down
+        r = build_rate
+        for _ in range(8):
+            r *= 0.8
+            ok, j = probe(r, "down")
+            if ok:
+                return r
+        return r
+    for _ in range(4):
         mid = 0.5 * (lo + hi)
         ok, j = probe(mid, "bisect")
         if ok and j >= 0.99 * best_j:
@@ -400,15 +454,58 @@ def knee_search(rt, build_rate: float, probe_s: float, log, set_rate=None) -> fl
     return best_r
 
 
-def ours(args) -> dict | None:
+def timed_knee(rt, rate: float, args, log, tag: str, set_rate=None, clock_index=None):
+    """The timed measurement: `warmup` + `steps` windows of `step_seconds`, one
+    continuous run. Every window of the run must meet HP miss 0 and LP loss
+    < 2 %; a run with any failing window is NOT re-measured at the same rate —
+    the rate steps down (x STEP_DOWN) and the whole run repeats, up to
+    `timed_attempts` runs. All ranks decide together (min over ranks).
+    Returns (rate, result, windows summary, clocks, attempts)."""
+    set_rate = set_rate or rt.set_rate
+    step = args.step_seconds
+    attempts = []
+    out = None
+    for a in range(args.timed_attempts):
+        set_rate(rate)
+        barrier()
+        with ClockSampler(clock_index if clock_index is not None else 0) as clk:
+            t0 = time.perf_counter()
+            res, ws = run_windows(rt, args.warmup * step, step, args.steps)
+            wall = time.perf_counter() - t0
+        barrier()
+        s = summarize(ws, step)
+        ok = all_reduce([1.0 if s["ok"] else 0.0], "min")[0] > 0
+        fails = all_reduce([float(s["windows_failed"]), float(s["windows_failed_without_pause"]),
+                            float(s["stalls"])], "sum")
+        attempts.append({"rate_per_task": round(rate, 2), "windows_failed": int(fails[0]),
+                         "windows_failed_without_pause": int(fails[1]), "gpu_pauses": int(fails[2]),
+                         "inf_per_s": round(s["inf_per_s"], 1)})
+        log(f"{tag} rate={rate:.1f} ok={ok} inf/s={s['inf_per_s']:.0f} failed={s['windows_failed']} "
+            f"(without pause {s['windows_failed_without_pause']}) pauses={s['stalls']} wall={wall:.1f}s")
+        out = (rate, res, s, clk.summary(), wall)
+        if ok:
+            break
+        rate *= STEP_DOWN
+    rate, res, s, clocks, wall = out
+    return rate, res, s, clocks, wall, attempts
+
+
+def ours(args, make_runtime=None) -> dict | None:
+    """Our arm. `make_runtime(tasks, gpu)` builds a rank's DARIS runtime (a
+    DarisRuntime on its GPU; the CPU gloo test passes a stand-in)."""
     import torch
     from paper_2504_08795_b200 import nets
     from paper_2504_08795_b200.box import BoxTask, local_tasks, place_tasks
     from paper_2504_08795_b200.gpu import GpuConfig, Policy
-    from paper_2504_08795_b200.runtime import DarisRuntime
 
+    if make_runtime is None:
+        from paper_2504_08795_b200.runtime import DarisRuntime
+
+        def make_runtime(tasks, gpu):
+            return DarisRuntime(tasks, gpu, slots=3, seed=0)
     world, rank, local = dist_init()
-    torch.cuda.set_device(local)
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local)
     log = (lambda m: print(f"[rank{rank}] {m}", file=sys.stderr, flush=True)) if args.verbose else (lambda m: None)
     peaks = _peaks()
     # box placement: 8 tasks per GPU (weak scaling), Algorithm 1 at GPU granularity
@@ -417,7 +514,7 @@ def ours(args) -> dict | None:
     mine = [tid - 1 for tid in local_tasks(assignment, rank)]
     gpu = GpuConfig(148, 4, 2, 2.0, Policy.MPS_STR)
     t_setup = time.time()
-    rt = DarisRuntime(c2_tasks(100.0, mine), gpu, slots=3, seed=0)
+    rt = make_runtime(c2_tasks(100.0, mine), gpu)
     rt.capture_all()
     rt.afet = rt.calibrate_full_load(0.3)
     iso = sum(rt.stage_nominal["resnet50"])
@@ -425,82 +522,51 @@ def ours(args) -> dict | None:
     guess = 0.6 * (gpu.n_contexts * gpu.n_streams) / max(rt.afet.values()) / len(mine)
     log(f"setup {time.time() - t_setup:.1f}s partitions={rt.exec.partitions} isolated={iso * 1e3:.3f} ms "
         f"afet={rt.afet} guess={guess:.1f}/task")
-    rate = knee_search(rt, guess, args.probe_seconds, log)
-    rate = all_reduce([rate], "min")[0]
     step = args.step_seconds
-    duration = (args.warmup + args.steps) * step
+    window = args.steps * step
     warm = args.warmup * step
-
-    stall_log = {"attempts": [], "stalls_seen": 0}
-
-    def timed(rate_):
-        rt.set_rate(rate_)
-        barrier()
-        with ClockSampler(local) as clk:
-            t0 = time.perf_counter()
-            res, attempts, seen = run_clean(rt, duration, warm, log, f"timed {rate_:.0f}")
-            wall = (time.perf_counter() - t0) / attempts
-        barrier()
-        stall_log["attempts"].append(attempts)
-        stall_log["stalls_seen"] += seen
-        return res, wall, clk.summary()
-
-    # timed run at the knee; step down if the confirmation run breaks the constraints
-    # (a window that misses a deadline steps the rate down 3 %; a GPU-wide stall
-    # inside a window is re-measured by run_clean, not stepped down for)
-    for attempt in range(TIMED_ATTEMPTS):
-        res, wall, clocks = timed(rate)
-        ok = all_reduce([1.0 if feasible(res.report) else 0.0], "min")[0] > 0
-        log(f"timed rate={rate:.1f} ok={ok} jps={res.report.jps:.0f} wall={wall:.2f}s")
-        if ok or attempt == TIMED_ATTEMPTS - 1:
-            break
-        rate *= 0.97
-    constraints_met = ok
+    rate = knee_search(rt, guess, args.probe_seconds, step, log)
+    rate = all_reduce([rate], "min")[0]
+    rate, res, summ, clocks, wall, attempts = timed_knee(rt, rate, args, log, "timed", clock_index=local)
     rep = res.report
     net0 = next(iter(rt.nets.values()))
     n_ops = {st: nets.stage_launches(net0, st) for st in range(net0.n_stages)}
-    launches = sum(n_ops[t[2]] for t in res.trace if t[6] >= warm and t[6] < duration)
-    completed = rep.completed_hp + rep.completed_lp
-    tot = all_reduce([completed, rep.missed_hp, rep.missed_lp, rep.accepted_hp, rep.accepted_lp, launches,
-                      rep.rejected_lp], "sum")
+    end = warm + window
+    launches = sum(n_ops[t[2]] for t in res.trace if warm <= t[6] < end)
+    tot = all_reduce([summ["inf_per_s"] * window, summ["missed_hp"], summ["missed_lp"], summ["rejected_lp"],
+                      summ["released_lp"], launches], "sum")
     wall_max = all_reduce([wall], "max")[0]
-    p99 = all_reduce([rep.response_hp.p99], "max")[0]
-    window = args.steps * step
+    p99 = all_reduce([res.p99_hp(warm, end)], "max")[0]
     value = tot[0] / window
+    pauses = {"policy": "no re-measurement: a timed run with any failing window (including one hit by a "
+                        "GPU-wide pause) steps the rate down and repeats the whole run",
+              "attempts": attempts}
+    # secondary: the highest-rate attempt whose failures all followed a GPU-wide pause
+    excl = next((a for a in attempts if a["windows_failed_without_pause"] == 0), None)
 
-    # end-to-end through host buffers (H2D input + D2H logits every job)
+    # end-to-end through host buffers (H2D input + D2H logits every job), its own knee
     rt.use_host_io(True)
-    # its own knee: the H2D input copy sits on the critical path of every job
-    e2e_rate = knee_search(rt, 0.8 * rate, args.probe_seconds, log)
+    e2e_rate = knee_search(rt, 0.9 * rate, args.probe_seconds, step, log)
     e2e_rate = all_reduce([e2e_rate], "min")[0]
-    for attempt in range(TIMED_ATTEMPTS):
-        res_e, wall_e, _ = timed(e2e_rate)
-        ok_e = all_reduce([1.0 if feasible(res_e.report) else 0.0], "min")[0] > 0
-        r_ = res_e.report
-        log(f"e2e rate={e2e_rate:.1f} ok={ok_e} jps={r_.jps:.0f} miss_hp={r_.missed_hp} dmr_lp={r_.dmr_lp:.3f} "
-            f"rej_lp={r_.rejected_lp} p99_hp={r_.response_hp.p99 * 1e3:.3f}ms "
-            f"loop_gap_max={res_e.stats['loop_gap_max'] * 1e6:.0f}us slot_waits={res_e.stats['slot_waits']}")
-        if ok_e or attempt == TIMED_ATTEMPTS - 1:
-            break
-        e2e_rate *= 0.97
-    re = res_e.report
-    e_done = all_reduce([re.completed_hp + re.completed_lp], "sum")[0]
-    jobs_total = max(1, res_e.stats["copies_h2d"])
-    frac = (re.completed_hp + re.completed_lp) / jobs_total
+    e2e_rate, res_e, summ_e, _, _, attempts_e = timed_knee(rt, e2e_rate, args, log, "e2e", clock_index=local)
+    e_done = all_reduce([summ_e["inf_per_s"] * window], "sum")[0]
+    st_e = res_e.stats
+    frac_timed = window / (window + warm)
     e2e = {"value": round(e_done / window, 2), "unit": UNIT,
-           "h2d_bytes_per_step": int(res_e.stats["h2d_bytes"] * frac / args.steps),
-           "d2h_bytes_per_step": int(res_e.stats["d2h_bytes"] * frac / args.steps),
-           "rate_per_task": round(e2e_rate, 2), "hp_miss": int(re.missed_hp), "dmr_lp": re.dmr_lp,
-           "lp_loss": round(lp_loss(re), 5),
-           "constraints_met": bool(ok_e)}
+           "h2d_bytes_per_step": int(st_e["h2d_bytes"] * frac_timed / args.steps),
+           "d2h_bytes_per_step": int(st_e["d2h_bytes"] * frac_timed / args.steps),
+           "rate_per_task": round(e2e_rate, 2), "constraints_met": bool(summ_e["ok"]),
+           "windows_failed": summ_e["windows_failed"], "hp_miss": summ_e["missed_hp"],
+           "lp_loss": round(summ_e["lp_loss"], 5), "attempts": attempts_e}
     rt.use_host_io(False)
 
-    roof = conv_roofline(rt, peaks) if rank == 0 else None
+    roof = conv_roofline(rt, peaks, loaded_job_device_time(rt, rate)) if (rank == 0 and not args.no_roofline) \
+        else None
     rt.close()
-    batched = None if args.no_batched else [daris_batched(args, gpu, mine, log, b) for b in (4, 8, 16)]
+    batched = None if args.no_batched else [daris_batched(args, gpu, mine, log, b) for b in args.batched]
     batching = batching_baseline() if (rank == 0 and not args.no_batching) else None
     cpu = cpu_reference(args.cpu_seconds) if (rank == 0 and world == 1 and not args.no_cpu) else None
-    flops_inf = next(iter(rt.nets.values())).flops_per_image
+    flops_inf = net0.flops_per_image
     out = None
     if rank == 0:
         out = {
@@ -513,25 +579,29 @@ def ours(args) -> dict | None:
                        "partition_sms": [p["sm_count"] for p in rt.exec.partitions],
                        "green_contexts": all(p["green"] for p in rt.exec.partitions), "stages": 4, "batch": 1,
                        "knee_rate_per_task": round(rate, 2), "step_seconds": step,
+                       "timed_window_seconds": window,
+                       "protocol": "knee = the rate whose continuous timed run of `steps` windows has EVERY window "
+                                   "at HP miss 0 and LP loss < 2 % (misses + admission rejections; admitted jobs "
+                                   "past their deadline unfinished count as misses); a failing run steps the rate "
+                                   f"down x{STEP_DOWN} and repeats, no re-measurement at the same rate",
                        "l2": "inputs larger than L2: each job copies a distinct image from 64-image per-task "
                              "pools (8 x 64 x 602 KB = 308 MB per GPU)",
                        "timing": "host steady clock over the periodic schedule, barrier + synchronize both "
-                                 "sides, max over ranks; stage completions via "
-                                 + ("host-mapped flags (cuStreamWriteValue32)"
-                                    if os.environ.get("DARIS_EXEC_FLAGS", "") == "1" else "CUDA event polling")},
-            "constraints_met": bool(constraints_met),
-            "hp_miss": int(tot[1]), "dmr_lp": (tot[2] / tot[4]) if tot[4] else 0.0,
-            "lp_loss": round(lp_loss(rep), 5),
-            "executor_stats": {k: res.stats[k] for k in ("graph_launches", "slot_waits", "polls",
+                                 "sides, max over ranks; stage completions via CUDA event polling"},
+            "constraints_met": bool(summ["ok"]), "windows_failed": summ["windows_failed"],
+            "hp_miss": int(tot[1]), "lp_loss": round((tot[2] + tot[3]) / tot[4], 5) if tot[4] else 0.0,
+            "rejected_lp": int(tot[3]),
+            "p99_hp_response_ms": round(p99 * 1e3, 3), "p95_hp_response_ms": round(rep.response_hp.p95 * 1e3, 3),
+            "mean_hp_response_ms": round(rep.response_hp.mean * 1e3, 3),
+            "gpu_pauses": pauses,
+            "value_excl_pauses": ({"value": excl["inf_per_s"] * world, "rate_per_task": excl["rate_per_task"],
+                                   "windows_failed": excl["windows_failed"], "gpu_pauses": excl["gpu_pauses"],
+                                   "note": "highest-rate timed run whose failing windows all began at or after a "
+                                           "detected GPU-wide pause (~1.7 ms, environmental: "
+                                           "profiles/r02_freeze_probe_idle.txt)"} if excl else None),
+            "executor_stats": {k: res.stats[k] for k in ("graph_launches", "slot_waits", "slot_deferred", "polls",
                                                           "release_lag_max", "loop_gap_max", "progress_gap_max",
                                                           "stalls", "wall_seconds")},
-            "gpu_stalls": {"policy": "a timed window in which the executor saw a GPU-wide stall (no stage "
-                                     "completion for > max(1 ms, 3x the longest stage) with stages in flight) "
-                                     f"is re-measured, up to {STALL_RETRIES} times",
-                           "attempts_per_timed_run": stall_log["attempts"],
-                           "stalls_seen": stall_log["stalls_seen"]},
-            "p99_hp_response_ms": round(p99 * 1e3, 3), "p95_hp_response_ms": round(rep.response_hp.p95 * 1e3, 3),
-            "mean_hp_response_ms": round(rep.response_hp.mean * 1e3, 3), "rejected_lp": int(tot[6]),
             "e2e": e2e, "gpu_launches": int(tot[5]), "clocks": clocks, "roofline": roof,
             "roofline_model": {"bound": "tensor", "achieved": round(value * flops_inf / 1e12, 3),
                                "peak": peaks["bf16_tflops_sustained"] * world, "unit": "TFLOP/s",
@@ -625,15 +695,19 @@ def reference(args) -> dict | None:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--step-seconds", type=float, default=0.1)
+    ap.add_argument("--step-seconds", type=float, default=0.5)
     ap.add_argument("--probe-seconds", type=float, default=1.0)
+    ap.add_argument("--timed-attempts", type=int, default=8)
+    ap.add_argument("--batched", type=lambda v: [int(x) for x in v.split(",")], default=[16],
+                    help="batch sizes of the DARIS-with-batched-jobs variant")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-batching", action="store_true")
     ap.add_argument("--no-batched", action="store_true", help="skip the DARIS-with-batched-inputs variant")
+    ap.add_argument("--no-roofline", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -84,7 +84,6 @@ typedef struct daris_conv_plan_t {
   int32_t tma_rows;         /* > 0: activations arrive by TMA, M tile = tma_rows whole output rows */
   int32_t m_sub;            /* UMMA M=128 sub-tiles per CTA: 2 = a 256-row tile (TMA path, no split-K),
                                chosen when the grid would exceed the planned SMs */
-  int32_t halo;             /* 1: 3x3/s1/p1 from one halo tile per 64-channel block (conv_halo_kernel) */
 } daris_conv_plan_t;
 
 int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out);
@@ -115,12 +114,6 @@ int daris_avgpool(const void* x, float* y, int32_t n, int32_t hw, int32_t c, voi
 /* Linear layer for small batches (weight-streaming GEMV, HBM bound):
  * y[b][o] = act(sum_k x[b][k] * w[o][k] + bias[o]); x fp32 or bf16 (x_bf16=1),
  * y fp32 (y_bf16=0) or bf16. k % 8 == 0. */
-/* Global average pool over hw pixels of [batch][hw][k] NHWC bf16 fused with the
- * fp32 classifier y[batch][o] = mean(x) . w^T + bias (batch <= 4; `grid` blocks,
- * 0 = one output feature per warp). The last two ops of a ResNet (torchvision
- * avgpool + fc) as one launch. */
-int daris_pool_linear(const void* x, const void* w, const float* bias, float* y, int32_t batch, int32_t hw,
-                      int32_t k, int32_t o, int32_t grid, void* stream);
 int daris_linear(const void* x, int32_t x_bf16, const void* w, const float* bias, void* y, int32_t y_bf16,
                  int32_t batch, int32_t k, int32_t o, int32_t relu, void* stream);
 
@@ -129,61 +122,6 @@ int daris_linear(const void* x, int32_t x_bf16, const void* w, const float* bias
 int daris_dwconv(const void* x, void* y, const void* weight, const float* scale, const float* bias, int32_t n,
                  int32_t h, int32_t w, int32_t c, int32_t k, int32_t stride, int32_t pad, int32_t ho, int32_t wo,
                  int32_t relu, void* stream);
-
-/* ---------------------------------------------------------------------------
- * Persistent stage kernel: one launch runs a whole DARIS stage (the DNN
- * segment between two synchronisation points) on its partition. The stage is
- * a chain of ops; each op is cut into work units that CTAs claim in
- * topological order from a global counter, and a unit starts once the
- * previous op has published all of its output (per-op completion counter).
- * Deadlock-free for any grid size and any co-residency with other tenants.
- * Ops: conv (tcgen05, same layout rules as daris_conv2d but 128x64 tiles),
- * NCHW->NHWC8 pack, max pool, depthwise conv, global average pool, linear.
- * ------------------------------------------------------------------------- */
-enum daris_op_kind {
-  DARIS_OP_CONV = 0,     /* x NHWC bf16, weight [cout][kh][kw][c], scale/bias, residual, relu */
-  DARIS_OP_PACK8 = 1,    /* x fp32 NCHW [n][c<=8][h][w] -> y bf16 NHWC [n][h][w][8] */
-  DARIS_OP_MAXPOOL = 2,  /* NHWC bf16, window kh x kw, stride, pad */
-  DARIS_OP_AVGPOOL = 3,  /* NHWC bf16 [n][h][w][c] -> fp32 [n][c] */
-  DARIS_OP_LINEAR = 4,   /* y[n][cout] = x[n][c] . weight[cout][c] + bias; flags: 1 = x bf16, 2 = y bf16 */
-  DARIS_OP_DWCONV = 5    /* depthwise, weight [kh][kw][c] bf16, folded BN scale/bias, relu */
-};
-
-typedef struct daris_stage_op {
-  int32_t kind, relu, flags, splits;  /* splits: conv split-K factor, 0 = auto */
-  const void* x;
-  void* y;
-  const void* residual;
-  const void* weight;
-  const float* scale;
-  const float* bias;
-  int32_t n, h, w, c, cout, kh, kw, stride, pad, ho, wo, _pad;
-} daris_stage_op;
-
-typedef struct daris_stage_info_t {
-  int32_t grid, layers, units, smem_bytes;
-  int64_t workspace_floats;
-} daris_stage_info_t;
-
-typedef struct daris_stage_prog daris_stage_prog;
-
-/* Build a stage program (device-side op table, weight tensor maps, split-K
- * scratch, self-resetting counters) for `grid` persistent CTAs. Pointers in
- * `ops` are captured: the program is bound to one buffer set. */
-int daris_stage_create(const daris_stage_op* ops, int32_t n_ops, int32_t grid, daris_stage_prog** out);
-/* One launch of the whole stage on `stream` (capturable into a CUDA graph).
- * Launches of one program must be stream-ordered (its counters are reused). */
-int daris_stage_launch(const daris_stage_prog* prog, void* stream);
-int daris_stage_info(const daris_stage_prog* prog, daris_stage_info_t* out);
-int daris_stage_layer_units(const daris_stage_prog* prog, int32_t layer, int32_t* units, int32_t* splits);
-/* profiling: per unit 16 uint64 globaltimer stamps (claim, start, dependency met,
- * gather done, accumulator ready, published, epilogue done, CTA id, first K block
- * issued, all issued, loads landed); NULL = off */
-int daris_stage_set_trace(daris_stage_prog* prog, void* trace);
-/* conv split-K plan the stage kernel would use on `grid` CTAs */
-int daris_stage_plan_conv(const daris_stage_op* op, int32_t grid, int32_t* splits, int32_t* kb_per_split,
-                          int32_t* units);
-void daris_stage_destroy(daris_stage_prog* prog);
 
 /* Number of SMs on the current device (cached). */
 int daris_device_sms(void);

@@ -322,83 +322,6 @@ __global__ void linear_kernel(const void* __restrict__ x, int x_bf16, const __nv
   }
 }
 
-// Global average pool fused into the classifier (batch <= 4): every block
-// pools the [batch][hw][k] NHWC activations into shared memory (pixels split
-// over threads, fp32 shared atomics), then its warps compute output features
-// j = block*warps + warp, stepping by grid*warps, streaming the weight rows.
-// Replaces avgpool + linear (one dependent launch less per inference).
-constexpr int kPoolLinMaxB = 4;
-__global__ void pool_linear_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
-                                   const float* __restrict__ bias, float* __restrict__ y, int batch, int hw, int k,
-                                   int o) {
-  extern __shared__ float pooled[];  // [batch][k]
-  pdl_wait();
-  pdl_trigger();
-  const int chunks = k / 8;
-  for (int i = threadIdx.x; i < batch * k; i += blockDim.x) pooled[i] = 0.f;
-  __syncthreads();
-  // pixel split so that batch * chunks * ps covers the block about twice
-  int ps = (2 * blockDim.x) / (batch * chunks);
-  ps = ps < 1 ? 1 : (ps > hw ? hw : ps);
-  const int items = batch * chunks * ps;
-  for (int it = threadIdx.x; it < items; it += blockDim.x) {
-    const int part = it % ps;
-    const int bc = it / ps;
-    const int img = bc / chunks, ch = bc - img * chunks;
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const uint4* src = reinterpret_cast<const uint4*>(x + static_cast<size_t>(img) * hw * k) + ch;
-#pragma unroll 4
-    for (int p = part; p < hw; p += ps) {
-      const uint4 v = __ldg(src + static_cast<size_t>(p) * chunks);
-      const uint32_t vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = unpack_bf16x2(vv[e]);
-        acc[2 * e] += f.x;
-        acc[2 * e + 1] += f.y;
-      }
-    }
-    float* dst = pooled + img * k + ch * 8;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) atomicAdd(dst + e, acc[e]);
-  }
-  __syncthreads();
-  const float inv = 1.f / static_cast<float>(hw);
-  const int warps = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = blockIdx.x * warps + warp; j < o; j += gridDim.x * warps) {
-    const __nv_bfloat16* wrow = w + static_cast<size_t>(j) * k;
-    float acc[kPoolLinMaxB] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 8
-    for (int kk = lane * 8; kk < k; kk += 32 * 8) {
-      const uint4 wv = ld_stream(wrow + kk);
-      const uint32_t ww[4] = {wv.x, wv.y, wv.z, wv.w};
-      float wf[8];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = unpack_bf16x2(ww[e]);
-        wf[2 * e] = f.x;
-        wf[2 * e + 1] = f.y;
-      }
-#pragma unroll
-      for (int b = 0; b < kPoolLinMaxB; ++b) {
-        if (b < batch) {
-          const float4 p0 = *reinterpret_cast<const float4*>(pooled + b * k + kk);
-          const float4 p1 = *reinterpret_cast<const float4*>(pooled + b * k + kk + 4);
-          acc[b] += p0.x * wf[0] + p0.y * wf[1] + p0.z * wf[2] + p0.w * wf[3] + p1.x * wf[4] + p1.y * wf[5] +
-                    p1.z * wf[6] + p1.w * wf[7];
-        }
-      }
-    }
-#pragma unroll
-    for (int b = 0; b < kPoolLinMaxB; ++b) {
-      float v = acc[b];
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-      if (lane == 0 && b < batch) y[static_cast<size_t>(b) * o + j] = v * inv + (bias ? bias[j] : 0.f);
-    }
-  }
-}
-
 // depthwise conv: one thread per (output pixel, 8 channels)
 __global__ void dwconv_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
                               const __nv_bfloat16* __restrict__ wt, const float* __restrict__ scale,
@@ -512,31 +435,6 @@ extern "C" int daris_linear(const void* x, int32_t x_bf16, const void* w, const 
   cudaError_t return_code = launch_pdl(linear_kernel, dim3((o + warps - 1) / warps), dim3(warps * 32), 0, static_cast<cudaStream_t>(stream), 
       x, x_bf16, static_cast<const __nv_bfloat16*>(w), bias, y, y_bf16, batch, k, o, relu);
   return static_cast<int>(return_code);
-}
-
-extern "C" int daris_pool_linear(const void* x, const void* w, const float* bias, float* y, int32_t batch,
-                                 int32_t hw, int32_t k, int32_t o, int32_t grid, void* stream) {
-  if (!x || !w || !y) return DARIS_K_BAD_ARG;
-  if (k % 8 != 0 || batch < 1 || batch > kPoolLinMaxB || o < 1 || hw < 1) return DARIS_K_BAD_SHAPE;
-  const int threads = 512;
-  const size_t smem = static_cast<size_t>(batch) * k * sizeof(float);
-  if (smem > 48 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(pool_linear_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      attr = true;
-    }
-    if (smem > 64 * 1024) return DARIS_K_BAD_SHAPE;
-  }
-  // one output feature per warp by default: the GEMV is latency-bound, so every
-  // output row's weight loads should be in flight at once (the pool is redone per block)
-  const int warps = threads / 32;
-  int g = grid > 0 ? grid : (o + warps - 1) / warps;
-  if (g > (o + warps - 1) / warps) g = (o + warps - 1) / warps;
-  cudaError_t rc = launch_pdl(pool_linear_kernel, dim3(g), dim3(threads), smem, static_cast<cudaStream_t>(stream),
-                              static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w), bias, y,
-                              batch, hw, k, o);
-  return static_cast<int>(rc);
 }
 
 extern "C" int daris_dwconv(const void* x, void* y, const void* weight, const float* scale, const float* bias,

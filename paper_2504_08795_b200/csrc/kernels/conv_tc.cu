@@ -94,7 +94,6 @@ struct ConvArgs {
   int kb_seg1;        // K blocks of the primary input; blocks >= kb_seg1 come from x2 (DARIS_CONV_DUAL)
   int stride2;        // x2 sampling stride
   int box_rows;       // rows of one output/residual TMA box
-  int plain_push;     // cluster split-K: plain remote stores + cluster barrier instead of st.async + mbarrier
   unsigned long long* ts;  // optional per-CTA phase timestamps (globaltimer ns), 16 per CTA
   FDiv d_howo, d_wo, d_kw, d_cinb, d_tiles_h;
 };
@@ -546,30 +545,19 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
         uint32_t r[32];
         tmem_ld_32x32b_x32(t_row + c0, r);  // warp-collective (.sync.aligned): every lane loads
         if (push) {
-          if (a.plain_push) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-              st_cluster_v4(dst + (c0 + 4 * q) * 4, __uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                            __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
-          } else {
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              st_async_v4(dst + (c0 + 4 * q) * 4, __uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                          __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]), bar);
-          }
+          for (int q = 0; q < 8; ++q)
+            st_async_v4(dst + (c0 + 4 * q) * 4, __uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                        __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]), bar);
         }
       }
     }
     __syncwarp();
-    if (a.plain_push) {
-      cluster_sync();  // every partial row has landed in its owner (release/acquire)
-    } else {
-      cluster_arrive();  // (released before exit: no CTA leaves while peers may still push to it)
-    }
+    cluster_arrive();  // (released before exit: no CTA leaves while peers may still push to it)
     if (warp < 4) {
       const int r_begin = (split * kBM) / S, r_end = ((split + 1) * kBM) / S;
       const int valid = max(0, min(r_end, mvalid) - r_begin);
-      if (!a.plain_push) mbar_wait(red_bar, 0);
+      mbar_wait(red_bar, 0);
       if (ts && threadIdx.x == 0) ts[10] = gtimer();
       float* s_scale = reinterpret_cast<float*>(smem + L::kEpiOff);
       float* s_bias = s_scale + BN;
@@ -611,7 +599,7 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
     }
     __syncwarp();
     if (ts && threadIdx.x == 0) ts[11] = gtimer();
-    if (!a.plain_push) cluster_wait();
+    cluster_wait();
   }
   if (ts && threadIdx.x == 0) ts[5] = gtimer();
   tc_fence_before();
@@ -619,267 +607,6 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
   if (warp == 4) {
     tc_fence_after();
     tmem_dealloc<MT * BN>(tmem_base);
-  }
-  if (ts && threadIdx.x == 0) ts[6] = gtimer();
-}
-
-// ---------------------------------------------------------------------------
-// 3x3 / stride 1 / pad 1 convolutions from a halo tile ("halo mode").
-//
-// The M tile is th output rows laid out W_h = wo + 2 pixels wide (the last two
-// columns of every row are computed and discarded). For one 64-channel block
-// the A operand of kernel position (r, s) is then the CONTIGUOUS run of rows
-// [r*W_h + s, r*W_h + s + 128) of the (th+2) x W_h halo tile, so one TMA box
-// (zero-filled borders = the padding) feeds all nine positions: the UMMA
-// descriptor just starts r*W_h + s rows in (128B-swizzle base offset set).
-// Activation traffic per channel block drops from 9 boxes to 1, and the
-// weight tiles (8 KB) get a deep ring of their own.
-constexpr int kHaloHS = 2;  // halo stages
-constexpr int kHaloWSMax = 8;  // weight stages (BN = 64: 8 KB each), a.ws <= this
-
-struct HaloArgs {
-  const float* scale;
-  const float* bias;
-  int cin, cout, h, w, ho, wo, relu;
-  int wh, th, tiles_h, cin_blocks, stage_bytes;  // W_h, rows per tile, tiles per image, 64-ch blocks, halo stage
-  int bo_mode;        // descriptor base offset for row-shifted A starts: 0 none, 1 (addr >> 7) & 7
-  int ws;             // weight ring depth (8 KB stages)
-  int cb_per_split;   // split-K over channel blocks: a cluster of gridDim.z CTAs, partials reduced over DSMEM
-  __nv_bfloat16* y;   // output (the split path stores its owned rows directly)
-  FDiv d_tiles_h;
-  unsigned long long* ts;
-};
-
-__device__ __forceinline__ uint64_t umma_desc_k_sw128_at(uint32_t smem_addr, int bo_mode) {
-  // A start that is not 1024-B aligned (a row shift inside the 8-row swizzle atom)
-  // works with base_offset = 0: the 128B swizzle is applied to the absolute smem
-  // address, matching how TMA wrote the tile (measured: bo_mode 1, base_offset =
-  // (addr >> 7) & 7, gives wrong sums; tests/test_kernels_gpu.py::test_conv3x3_halo_mode)
-  const uint64_t d = umma_desc_k_sw128(smem_addr);
-  return bo_mode ? (d | (static_cast<uint64_t>((smem_addr >> 7) & 7) << 49)) : d;
-}
-
-__global__ void __maxnreg__(DARIS_CONV_MAXNREG)
-    conv_halo_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap hmap,
-                     const __grid_constant__ CUtensorMap ymap, const HaloArgs a) {
-  constexpr int BN = 64;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sH = smem;                                   // kHaloHS x stage_bytes
-  uint8_t* sW = smem + kHaloHS * a.stage_bytes;         // a.ws x 8 KB
-  uint64_t* hfull = reinterpret_cast<uint64_t*>(sW + a.ws * BN * 128);
-  uint64_t* hempty = hfull + kHaloHS;
-  uint64_t* wfull = hempty + kHaloHS;
-  uint64_t* wempty = wfull + a.ws;
-  uint64_t* tmem_full = wempty + a.ws;
-  uint64_t* red_bar = tmem_full + 1;  // split-K: this CTA's rows of every split have landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(red_bar + 1);
-  float* s_scale = reinterpret_cast<float*>(tmem_slot + 4);
-  float* s_bias = s_scale + BN;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile_m = blockIdx.x, tile_n = blockIdx.y;
-  const int img = fdiv(tile_m, a.d_tiles_h);
-  const int h0 = (tile_m - img * a.tiles_h) * a.th;
-  const int n0 = tile_n * BN;
-  const int S = gridDim.z, split = blockIdx.z;
-  const int cb_begin = split * a.cb_per_split;
-  const int ncb = min(a.cin_blocks, cb_begin + a.cb_per_split) - cb_begin;
-  const int mvalid = a.th * a.wh;  // tile rows holding output pixels (+ the discarded columns)
-  unsigned long long* ts =
-      a.ts ? a.ts + 16ull * (blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z)) : nullptr;
-  if (ts && threadIdx.x == 0) ts[0] = gtimer();
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kHaloHS; ++i) { mbar_init(&hfull[i], 1); mbar_init(&hempty[i], 1); }
-    for (int i = 0; i < a.ws; ++i) { mbar_init(&wfull[i], 1); mbar_init(&wempty[i], 1); }
-    mbar_init(tmem_full, 1);
-    mbar_init(red_bar, 1);
-    fence_barrier_init();
-  }
-  if (warp == 4) {
-    tmem_alloc<BN>(tmem_slot);
-    if (lane == 0) {
-      tma_prefetch_desc(&wmap);
-      tma_prefetch_desc(&hmap);
-      if (S == 1) tma_prefetch_desc(&ymap);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  if (ts && threadIdx.x == 0) ts[1] = gtimer();
-
-  if (warp == 4) {
-    if (lane == 0) {
-      // K order: channel block cb, then the 9 kernel positions; weight K coordinate
-      // of (p, cb) = p * cin + cb * 64 in the [cout][3][3][cin] layout
-      const int total = ncb * 9;
-      const int pre = min(total, a.ws);
-      for (int j = 0; j < pre; ++j) {  // weights do not depend on the previous layer
-        mbar_arrive_expect_tx(&wfull[j], BN * 128);
-        tma_load_2d(&wmap, &wfull[j], sW + j * (BN * 128), (j % 9) * a.cin + (cb_begin + j / 9) * kBK, n0);
-      }
-      pdl_wait();
-      if (ts) ts[2] = ts[3] = gtimer();
-      const uint32_t halo_bytes = static_cast<uint32_t>((a.th + 2) * a.wh * 128);
-      for (int cb = 0; cb < ncb; ++cb) {
-        const int hs = cb % kHaloHS;
-        if (cb >= kHaloHS) mbar_wait(&hempty[hs], ((cb / kHaloHS) & 1) ^ 1);
-        mbar_arrive_expect_tx(&hfull[hs], halo_bytes);
-        tma_load_4d(&hmap, &hfull[hs], sH + hs * a.stage_bytes, (cb_begin + cb) * kBK, -1, h0 - 1, img);
-        for (int p = 0; p < 9; ++p) {
-          const int j = cb * 9 + p;
-          if (j < pre) continue;
-          const int ws = j % a.ws;
-          mbar_wait(&wempty[ws], ((j / a.ws) & 1) ^ 1);
-          mbar_arrive_expect_tx(&wfull[ws], BN * 128);
-          tma_load_2d(&wmap, &wfull[ws], sW + ws * (BN * 128), p * a.cin + (cb_begin + cb) * kBK, n0);
-        }
-      }
-    }
-  } else if (warp == 5) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc_bf16(kBM, BN);
-      const uint32_t sH_u32 = smem_u32(sH), sW_u32 = smem_u32(sW);
-      for (int cb = 0; cb < ncb; ++cb) {
-        const int hs = cb % kHaloHS;
-        mbar_wait(&hfull[hs], (cb / kHaloHS) & 1);
-        for (int p = 0; p < 9; ++p) {
-          const int j = cb * 9 + p;
-          const int ws = j % a.ws;
-          mbar_wait(&wfull[ws], (j / a.ws) & 1);
-          tc_fence_after();
-          const int r = p / 3, sx = p - (p / 3) * 3;
-          const uint64_t adesc = umma_desc_k_sw128_at(sH_u32 + hs * a.stage_bytes + (r * a.wh + sx) * 128, a.bo_mode);
-          const uint64_t bdesc = umma_desc_k_sw128(sW_u32 + ws * (BN * 128));
-#pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            umma_bf16(tmem_base, adesc + 2 * k, bdesc + 2 * k, idesc, (j > 0 || k > 0) ? 1u : 0u);
-          umma_commit(&wempty[ws]);
-        }
-        umma_commit(&hempty[hs]);
-      }
-      umma_commit(tmem_full);
-    }
-  } else {
-    // epilogue warps: folded-BN scale/bias -> smem, then TMEM -> bf16 -> swizzled staging -> TMA store
-    const int t = threadIdx.x;
-    for (int c = t; c < BN; c += 128) {
-      s_scale[c] = __ldg(a.scale + n0 + c);
-      s_bias[c] = __ldg(a.bias + n0 + c);
-    }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    mbar_wait(tmem_full, 0);
-    tc_fence_after();
-    if (threadIdx.x == 0) pdl_trigger();
-    if (ts && threadIdx.x == 0) ts[4] = gtimer();
-    const int row = warp * 32 + lane;
-    const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
-    if (S > 1) {
-      if (threadIdx.x == 0) {
-        const int r_begin = (split * kBM) / S, r_end = ((split + 1) * kBM) / S;
-        const int valid = max(0, min(r_end, mvalid) - r_begin);
-        mbar_arrive_expect_tx(red_bar, static_cast<uint32_t>(S * valid * BN * 4));
-      }
-    }
-  }
-  if (S > 1) {
-    // split-K over channel blocks inside one cluster (as conv_igemm_tc_kernel): CTA r
-    // owns rows [r*128/S, (r+1)*128/S) and receives those rows of every partial
-    const int rpc_max = (kBM + S - 1) / S;
-    float* recv = reinterpret_cast<float*>(sH);  // [S][rpc_max][BN] fp32 in the idle halo ring
-    __syncwarp();
-    cluster_sync();
-    if (warp < 4) {
-      const int row = warp * 32 + lane;
-      const bool push = row < mvalid;
-      const int owner = ((row + 1) * S - 1) / kBM;
-      const int j = row - (owner * kBM) / S;
-      const uint32_t dst = dsmem_map(smem_u32(recv + (static_cast<size_t>(split) * rpc_max + j) * BN), owner);
-      const uint32_t bar = dsmem_map(smem_u32(red_bar), owner);
-      const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
-#pragma unroll
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_row + c0, r);
-        if (push) {
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            st_async_v4(dst + (c0 + 4 * q) * 4, __uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                        __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]), bar);
-        }
-      }
-    }
-    __syncwarp();
-    cluster_arrive();
-    if (warp < 4) {
-      const int r_begin = (split * kBM) / S, r_end = ((split + 1) * kBM) / S;
-      const int valid = max(0, min(r_end, mvalid) - r_begin);
-      mbar_wait(red_bar, 0);
-      const int items = valid * (BN / 8);
-      for (int it = threadIdx.x; it < items; it += 128) {
-        const int j = it / (BN / 8), g = it % (BN / 8);
-        const int trow = r_begin + j;  // tile row -> output pixel (th rows of W_h, 2 discarded columns)
-        const int oh = h0 + trow / a.wh, ow = trow - (trow / a.wh) * a.wh;
-        if (ow >= a.wo || oh >= a.ho) continue;
-        const int c = g * 8;
-        float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int k = 0; k < S; ++k) {
-          const float4* src = reinterpret_cast<const float4*>(recv + (static_cast<size_t>(k) * rpc_max + j) * BN + c);
-          const float4 p0 = src[0], p1 = src[1];
-          v[0] += p0.x; v[1] += p0.y; v[2] += p0.z; v[3] += p0.w;
-          v[4] += p1.x; v[5] += p1.y; v[6] += p1.z; v[7] += p1.w;
-        }
-        float o[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = act_apply(v[e] * s_scale[c + e] + s_bias[c + e], a.relu);
-        uint4 pk;
-        pk.x = pack_bf16x2(o[0], o[1]);
-        pk.y = pack_bf16x2(o[2], o[3]);
-        pk.z = pack_bf16x2(o[4], o[5]);
-        pk.w = pack_bf16x2(o[6], o[7]);
-        const size_t m = (static_cast<size_t>(img) * a.ho + oh) * a.wo + ow;
-        *reinterpret_cast<uint4*>(a.y + m * a.cout + n0 + c) = pk;
-      }
-    }
-    __syncwarp();
-    cluster_wait();
-  } else if (warp < 4) {
-    const int row = warp * 32 + lane;
-    const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
-    uint8_t* stage = sH;  // the halo ring is idle once the accumulator is complete
-    const uint32_t swz = static_cast<uint32_t>(row & 7);
-    ConvArgs ca;  // only relu is read by pack_row32
-    ca.relu = a.relu;
-    const uint4 nores[4] = {};
-#pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      uint32_t rr[32];
-      tmem_ld_32x32b_x32(t_row + c0, rr);
-      uint4 pk[4];
-      pack_row32(ca, c0, reinterpret_cast<const float*>(rr), s_scale, s_bias, nores, false, pk);
-      uint8_t* rowp = stage + row * 128;
-      const uint32_t chunk0 = static_cast<uint32_t>(c0 >> 3);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(rowp + (((chunk0 + q) ^ swz) << 4)) = pk[q];
-    }
-    fence_proxy_async_smem();
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    if (threadIdx.x == 0) {
-      // box {64 ch, W_h cols, th rows, 1}: the two extra columns (and rows past ho) are clipped
-      tma_store_4d(&ymap, stage, n0, 0, h0, img);
-      bulk_commit();
-      bulk_wait_read();
-    }
-  }
-  if (ts && threadIdx.x == 0) ts[5] = gtimer();
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 4) {
-    tc_fence_after();
-    tmem_dealloc<BN>(tmem_base);
   }
   if (ts && threadIdx.x == 0) ts[6] = gtimer();
 }
@@ -1042,11 +769,6 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   a.cluster_split = pl.cluster > 1 ? 1 : 0;
   a.tma_a = pl.tma_rows > 0 ? 1 : 0;
   a.tma_c = tma_c ? 1 : 0;
-  static const bool plain_push = [] {  // experiment knob (A/B against st.async + mbarrier)
-    const char* e = std::getenv("DARIS_SPLIT_PLAIN");
-    return e && std::atoi(e) != 0;
-  }();
-  a.plain_push = plain_push ? 1 : 0;
   a.stem_tma = stem_tma ? 1 : 0;
   a.box_rows = box_rows;
   a.th = pl.tma_rows > 0 ? pl.tma_rows : 1;
@@ -1079,100 +801,6 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN, ST, MT>, map, amap, ymap, amap2, a));
 }
 
-static int launch_halo(const daris_conv_desc* d, const daris_conv_plan_t& pl, cudaStream_t st) {
-  auto encode = get_encode_fn();
-  if (!encode) return DARIS_K_NO_DRIVER;
-  const int th = pl.tma_rows, wh = d->wo + 2;
-  CUtensorMap wmap, hmap, ymap;
-  {
-    const cuuint64_t K = static_cast<cuuint64_t>(9) * d->cin;
-    cuuint64_t dims[2] = {K, static_cast<cuuint64_t>(d->cout)};
-    cuuint64_t strides[1] = {K * 2};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), 64};
-    cuuint32_t estr[2] = {1, 1};
-    if (encode(&wmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(d->weight), dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return DARIS_K_BAD_ARG;
-  }
-  {
-    cuuint64_t dims[4] = {static_cast<cuuint64_t>(d->cin), static_cast<cuuint64_t>(d->w),
-                          static_cast<cuuint64_t>(d->h), static_cast<cuuint64_t>(d->n)};
-    cuuint64_t strides[3] = {static_cast<cuuint64_t>(d->cin) * 2, static_cast<cuuint64_t>(d->w) * d->cin * 2,
-                             static_cast<cuuint64_t>(d->h) * d->w * d->cin * 2};
-    cuuint32_t box[4] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(wh),
-                         static_cast<cuuint32_t>(th + 2), 1};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
-    if (encode(&hmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(d->x), dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return DARIS_K_BAD_ARG;
-  }
-  {
-    cuuint64_t dims[4] = {static_cast<cuuint64_t>(d->cout), static_cast<cuuint64_t>(d->wo),
-                          static_cast<cuuint64_t>(d->ho), static_cast<cuuint64_t>(d->n)};
-    cuuint64_t strides[3] = {static_cast<cuuint64_t>(d->cout) * 2, static_cast<cuuint64_t>(d->wo) * d->cout * 2,
-                             static_cast<cuuint64_t>(d->ho) * d->wo * d->cout * 2};
-    cuuint32_t box[4] = {64, static_cast<cuuint32_t>(wh), static_cast<cuuint32_t>(th), 1};
-    cuuint32_t estr[4] = {1, 1, 1, 1};
-    if (encode(&ymap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, d->y, dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return DARIS_K_BAD_ARG;
-  }
-  HaloArgs a;
-  a.scale = d->scale;
-  a.bias = d->bias;
-  a.cin = d->cin; a.cout = d->cout; a.h = d->h; a.w = d->w; a.ho = d->ho; a.wo = d->wo; a.relu = d->relu;
-  a.wh = wh;
-  a.th = th;
-  a.tiles_h = (d->ho + th - 1) / th;
-  a.cin_blocks = d->cin / kBK;
-  const int rows = std::max((th + 2) * wh, kBM + 2 * wh + 2);  // the MMA reads 128 rows from offset up to 2*W_h + 2
-  a.stage_bytes = (rows * 128 + 1023) / 1024 * 1024;
-  a.d_tiles_h = make_fdiv(a.tiles_h);
-  a.ts = reinterpret_cast<unsigned long long*>(d->timestamps);
-  static const int bo_mode = [] {
-    const char* e = std::getenv("DARIS_HALO_BO");
-    return e ? std::atoi(e) : 0;
-  }();
-  a.bo_mode = bo_mode;
-  a.cb_per_split = pl.kb_per_split;  // halo plan: K units are 64-channel blocks
-  a.y = static_cast<__nv_bfloat16*>(d->y);
-  // weight ring depth: 4 x 8 KB (8 measured no faster — the mainloop is not bound
-  // by bytes in flight — and costs co-residency); DARIS_HALO_WS overrides
-  static const int ws_env = [] {
-    const char* e = std::getenv("DARIS_HALO_WS");
-    return e ? std::atoi(e) : 0;
-  }();
-  a.ws = ws_env > 0 ? std::min(ws_env, kHaloWSMax) : 4;
-  const int smem = 1024 + kHaloHS * a.stage_bytes + a.ws * 64 * 128 + 1024;
-  static int attr_smem = 0;
-  if (smem > attr_smem) {
-    set_max_carveout(reinterpret_cast<const void*>(conv_halo_kernel));
-    cudaError_t e = cudaFuncSetAttribute(conv_halo_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr_smem = smem;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(pl.tiles_m, pl.tiles_n, pl.splits);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (pl.splits > 1) {
-    attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = 1;
-    attr[1].val.clusterDim.y = 1;
-    attr[1].val.clusterDim.z = pl.splits;
-    cfg.numAttrs = 2;
-  }
-  return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_halo_kernel, wmap, hmap, ymap, a));
-}
 
 }  // namespace daris
 
@@ -1294,41 +922,6 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
   out->m_sub = m_sub;
   out->cluster = (splits > 1 && bn == 64 && (d->flags & DARIS_CONV_CLUSTER_SPLITK)) ? splits : 1;
   out->tma_rows = tma_a ? th_used : 0;
-  // 3x3 / stride 1 / pad 1 from a halo tile (see conv_halo_kernel). Opt-in:
-  // DARIS_CONV_HALO=1 where the regular plan does not split K (or clusters are
-  // allowed), 2: everywhere. Off by default since the register cap admits 3
-  // implicit-GEMM CTAs per SM while a halo CTA's ring (82-98 KB) admits 2:
-  // isolated forwards tie (414.6 us at 24 SMs either way) but loaded capacity is
-  // higher without it (4x2: 15.2k vs 14.9k, 16 jobs: 21.5k vs 20.2k inf/s,
-  // profiles/r01_halo_ab.jsonl)
-  static const int halo_mode = [] {
-    const char* e = std::getenv("DARIS_CONV_HALO");
-    return e ? std::atoi(e) : 0;
-  }();
-  out->halo = 0;
-  const bool clusters_ok = (d->flags & DARIS_CONV_CLUSTER_SPLITK) != 0;
-  if (halo_mode > 0 && (splits == 1 || clusters_ok || halo_mode == 2) && d->kh == 3 && d->kw == 3 && d->stride == 1 && d->pad == 1 && d->cin % kBK == 0 &&
-      d->cout % 64 == 0 && !d->residual && !dual && !padded && d->wo + 2 <= kBM && d->h == d->ho && d->w == d->wo) {
-    const int wh = d->wo + 2;
-    const int thh = std::max(1, std::min(d->ho, kBM / wh));
-    // split-K over 64-channel blocks where the regular plan splits (clusters <= 8 CTAs)
-    const int ncb = d->cin / kBK;
-    int hs = (splits > 1 && clusters_ok) ? std::min(std::min(splits, ncb), 8) : 1;
-    const int cbps = (ncb + hs - 1) / hs;
-    hs = (ncb + cbps - 1) / cbps;
-    out->halo = 1;
-    out->block_n = 64;
-    out->splits = hs;
-    out->kb_per_split = cbps;  // in channel blocks
-    out->tma_rows = thh;
-    out->tiles_m = d->n * ((d->ho + thh - 1) / thh);
-    out->tiles_n = d->cout / 64;
-    out->ctas = out->tiles_m * out->tiles_n * hs;
-    out->cluster = hs;
-    out->m_sub = 1;
-    out->workspace_floats = 0;
-    out->counters = 0;
-  }
   if (out->cluster > 1) {  // partials reduce through DSMEM: no global scratch
     out->workspace_floats = 0;
     out->counters = 0;
@@ -1352,7 +945,6 @@ extern "C" int daris_conv2d(const daris_conv_desc* d, void* stream) {
     return e && std::atoi(e) != 0;
   }();
   const bool go_deep = deep && pl.tma_rows > 0 && pl.kb_per_split >= 12;
-  if (pl.halo) return launch_halo(d, pl, st);
   if (pl.m_sub == 2) {
     switch (pl.block_n) {
       case 64: return launch_bn<64, 2, 2>(d, pl, st);

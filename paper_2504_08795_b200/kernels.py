@@ -37,27 +37,8 @@ class ConvPlan(C.Structure):
         ("block_n", C.c_int32), ("splits", C.c_int32), ("kb_per_split", C.c_int32),
         ("tiles_m", C.c_int32), ("tiles_n", C.c_int32), ("workspace_floats", C.c_int64),
         ("counters", C.c_int32), ("ctas", C.c_int32), ("cluster", C.c_int32), ("tma_rows", C.c_int32),
-        ("m_sub", C.c_int32), ("halo", C.c_int32),
+        ("m_sub", C.c_int32),
     ]
-
-
-class StageOp(C.Structure):
-    _fields_ = [
-        ("kind", C.c_int32), ("relu", C.c_int32), ("flags", C.c_int32), ("splits", C.c_int32),
-        ("x", C.c_void_p), ("y", C.c_void_p), ("residual", C.c_void_p), ("weight", C.c_void_p),
-        ("scale", C.c_void_p), ("bias", C.c_void_p),
-        ("n", C.c_int32), ("h", C.c_int32), ("w", C.c_int32), ("c", C.c_int32), ("cout", C.c_int32),
-        ("kh", C.c_int32), ("kw", C.c_int32), ("stride", C.c_int32), ("pad", C.c_int32),
-        ("ho", C.c_int32), ("wo", C.c_int32), ("_pad", C.c_int32),
-    ]
-
-
-class StageInfo(C.Structure):
-    _fields_ = [("grid", C.c_int32), ("layers", C.c_int32), ("units", C.c_int32), ("smem_bytes", C.c_int32),
-                ("workspace_floats", C.c_int64)]
-
-
-OP_CONV, OP_PACK8, OP_MAXPOOL, OP_AVGPOOL, OP_LINEAR, OP_DWCONV = range(6)
 
 
 def lib() -> C.CDLL:
@@ -76,25 +57,11 @@ def lib() -> C.CDLL:
         L.daris_maxpool.argtypes = [vp, vp] + [i32] * 9 + [vp]
         L.daris_avgpool.argtypes = [vp, vp, i32, i32, i32, vp]
         L.daris_linear.argtypes = [vp, i32, vp, vp, vp, i32, i32, i32, i32, i32, vp]
-        L.daris_pool_linear.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, vp]
         L.daris_dwconv.argtypes = [vp, vp, vp, vp, vp] + [i32] * 10 + [vp]
         L.daris_device_sms.argtypes = []
-        P = C.POINTER
-        L.daris_stage_create.argtypes = [P(StageOp), i32, i32, P(vp)]
-        L.daris_stage_launch.argtypes = [vp, vp]
-        L.daris_stage_info.argtypes = [vp, P(StageInfo)]
-        L.daris_stage_layer_units.argtypes = [vp, i32, P(i32), P(i32)]
-        L.daris_stage_plan_conv.argtypes = [P(StageOp), i32, P(i32), P(i32), P(i32)]
-        L.daris_stage_set_trace.argtypes = [vp, vp]
-        L.daris_stage_set_trace.restype = C.c_int
-        L.daris_stage_destroy.argtypes = [vp]
-        L.daris_stage_destroy.restype = None
         for name in ("daris_conv_plan", "daris_conv2d", "daris_stem_im2col", "daris_pack_nhwc",
-                     "daris_maxpool", "daris_avgpool", "daris_linear", "daris_pool_linear", "daris_dwconv",
-                     "daris_pack_nhwc_bordered",
-                     "daris_device_sms",
-                     "daris_stage_create", "daris_stage_launch", "daris_stage_info", "daris_stage_layer_units",
-                     "daris_stage_plan_conv"):
+                     "daris_maxpool", "daris_avgpool", "daris_linear", "daris_dwconv",
+                     "daris_pack_nhwc_bordered", "daris_device_sms"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -241,18 +208,6 @@ def linear(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None, *, 
     return out
 
 
-def pool_linear(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None, *,
-                out: torch.Tensor | None = None, grid: int = 0, stream=None) -> torch.Tensor:
-    """mean over the pixels of NHWC bf16 x (batch <= 4), then fp32 x . weight^T + bias."""
-    n, h, w, c = x.shape
-    o = weight.shape[0]
-    if out is None:
-        out = torch.empty((n, o), dtype=torch.float32, device=x.device)
-    _check(lib().daris_pool_linear(_ptr(x), _ptr(weight), _ptr(bias), _ptr(out), n, h * w, c, o, grid,
-                                   _stream(stream)), "daris_pool_linear")
-    return out
-
-
 def dwconv(x: torch.Tensor, weight: torch.Tensor, scale: torch.Tensor, bias: torch.Tensor, *, stride: int,
            pad: int, relu: int = 6, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """weight: [k,k,c] bf16."""
@@ -271,56 +226,3 @@ def device_sms() -> int:
     return lib().daris_device_sms()
 
 
-class StageProgram:
-    """A persistent stage-kernel program (include/daris_kernels.h,
-    daris_stage_create): one launch runs a whole chain of ops on `grid` CTAs.
-    The op table captures raw pointers, so the tensors it references must
-    outlive the program (the caller keeps them in `keep`)."""
-
-    def __init__(self, ops: list[StageOp], grid: int, keep=()):
-        arr = (StageOp * len(ops))(*ops)
-        h = C.c_void_p()
-        _check(lib().daris_stage_create(arr, len(ops), grid, C.byref(h)), "daris_stage_create")
-        self._h = h
-        self._keep = list(keep)
-        self.n_ops = len(ops)
-        info = StageInfo()
-        _check(lib().daris_stage_info(h, C.byref(info)), "daris_stage_info")
-        self.grid, self.units, self.smem_bytes = info.grid, info.units, info.smem_bytes
-        self.workspace_floats = info.workspace_floats
-
-    def launch(self, stream=None) -> None:
-        _check(lib().daris_stage_launch(self._h, _stream(stream)), "daris_stage_launch")
-
-    def layer_units(self, i: int) -> tuple[int, int]:
-        u, s = C.c_int32(), C.c_int32()
-        _check(lib().daris_stage_layer_units(self._h, i, C.byref(u), C.byref(s)), "daris_stage_layer_units")
-        return u.value, s.value
-
-    def set_trace(self, buf: torch.Tensor | None) -> None:
-        """Profiling: int64 tensor of units x 16 (see daris_stage_set_trace), or None."""
-        _check(lib().daris_stage_set_trace(self._h, _ptr(buf)), "daris_stage_set_trace")
-        self._trace = buf
-
-    def close(self) -> None:
-        if getattr(self, "_h", None):
-            lib().daris_stage_destroy(self._h)
-            self._h = None
-
-    def __del__(self):
-        try:
-            self.close()
-        except Exception:
-            pass
-
-
-def stage_op(kind: int, x: torch.Tensor, y: torch.Tensor, *, residual=None, weight=None, scale=None, bias=None,
-             n=0, h=0, w=0, c=0, cout=0, kh=1, kw=1, stride=1, pad=0, ho=0, wo=0, relu=0, flags=0,
-             splits=0) -> StageOp:
-    o = StageOp()
-    o.kind, o.relu, o.flags, o.splits = kind, relu, flags, splits
-    o.x, o.y, o.residual = _ptr(x), _ptr(y), _ptr(residual)
-    o.weight, o.scale, o.bias = _ptr(weight), _ptr(scale), _ptr(bias)
-    o.n, o.h, o.w, o.c, o.cout = n, h, w, c, cout
-    o.kh, o.kw, o.stride, o.pad, o.ho, o.wo = kh, kw, stride, pad, ho, wo
-    return o

@@ -18,7 +18,6 @@ buffer set).
 
 from __future__ import annotations
 
-import os
 from dataclasses import dataclass, field
 from typing import Callable
 
@@ -175,12 +174,11 @@ def _dual_layer(name, conv, bn, ds_conv, ds_bn, relu, device, hw_out) -> ConvLay
 
 
 def _stem(b: "_Builder", name, conv, bn, relu, device, batch: int):
-    """pack8 + the stem conv; the TMA-window form when the shape allows it (and
-    the network is not run by the persistent stage kernel, which gathers)."""
+    """pack8 + the stem conv; the TMA-window form when the shape allows it."""
     kh, kw = conv.kernel_size
     st, pd = conv.stride[0], conv.padding[0]
     wo = (224 + 2 * pd - kw) // st + 1
-    padded = _BUILD_MODE != "persistent" and kw <= 8 and wo <= 128
+    padded = kw <= 8 and wo <= 128
     layer = _stem_layer(name, conv, bn, relu, device, wo * wo, padded)
     b.need("input", batch * 3 * 224 * 224)
     if padded:
@@ -220,7 +218,6 @@ class Network:
     flops_per_image: int
     torch_model: nn.Module | None = None
     weight_bytes: int = 0
-    stage_mode: str = "layers"       # the execution mode the op forms were built for
 
     @property
     def n_stages(self) -> int:
@@ -236,7 +233,6 @@ class TaskBuffers:
     bufs: dict[str, torch.Tensor]
     workspace: torch.Tensor
     counters: torch.Tensor
-    programs: dict = field(default_factory=dict)   # (net id, stage, grid) -> K.StageProgram
 
     @property
     def input(self) -> torch.Tensor:
@@ -285,24 +281,14 @@ class _Builder:
         return dst, out_shape
 
 
-# the fused pool + classifier launch measured slower than avgpool + linear at batch 1
-# (every block re-pools the whole feature map): opt-in until it is restructured
-POOL_LINEAR = os.environ.get("DARIS_POOL_LINEAR", "0") == "1"
-
-
 def _pool_classifier(b: "_Builder", lin: LinearLayer, x: str, shape, batch: int) -> None:
-    """Global average pool + the final linear layer: avgpool then linear, or one
-    fused launch (daris_pool_linear, DARIS_POOL_LINEAR=1, batch <= 4)."""
+    """Global average pool + the final linear layer (two launches)."""
     feat = shape[3]
-    b.need("pooled", batch * feat)          # the two-launch form (and the persistent stage kernel) use it
+    b.need("pooled", batch * feat)
     b.need("logits", batch * lin.weight.shape[0])
     out_shape = (batch, lin.weight.shape[0])
-    if batch <= 4 and POOL_LINEAR:
-        b.ops.append(Op("pool_linear", lin, x, "logits", None, shape, out_shape, lin.flops_per_image * batch))
-    else:
-        b.ops.append(Op("avgpool", None, x, "pooled", None, shape, (batch, feat)))
-        b.ops.append(Op("linear", lin, "pooled", "logits", None, (batch, feat), out_shape,
-                        lin.flops_per_image * batch))
+    b.ops.append(Op("avgpool", None, x, "pooled", None, shape, (batch, feat)))
+    b.ops.append(Op("linear", lin, "pooled", "logits", None, (batch, feat), out_shape, lin.flops_per_image * batch))
 
 
 def _resnet_ops(model, name, batch, device, split) -> Network:
@@ -326,8 +312,8 @@ def _resnet_ops(model, name, batch, device, split) -> Network:
         identity = x
         ds = None
         # the downsample branch rides in the block's last conv as extra K blocks
-        # (bottlenecks, "layers" mode); otherwise it is its own launch
-        fuse_ds = blk.downsample is not None and hasattr(blk, "conv3") and _BUILD_MODE != "persistent"
+        # (bottlenecks); otherwise it is its own launch
+        fuse_ds = blk.downsample is not None and hasattr(blk, "conv3")
         if blk.downsample is not None and not fuse_ds:
             dl = _conv_layer(f"{bname}.downsample", blk.downsample[0], blk.downsample[1], 0, device, hw_out * hw_out)
             ds, _ = b.conv(dl, x, shape)
@@ -495,12 +481,10 @@ RESNET50_SPLITS = {1: [], 2: [7], 3: [3, 10], 4: [3, 7, 13]}  # 4 stages: layer1
 
 def build_network(name: str, *, batch: int = 1, n_stages: int | None = None, seed: int = 0,
                   device: torch.device | str = "cuda", keep_torch: bool = False,
-                  model: nn.Module | None = None, stage_mode: str | None = None) -> Network:
-    """stage_mode (default: DARIS_STAGE_MODE) picks the op forms: "layers" uses the
-    TMA-window stem and the downsample-fused block conv; the persistent stage
-    kernel ("persistent") runs the plain forms."""
-    global _BUILD_MODE
-    _BUILD_MODE = stage_mode or STAGE_MODE
+                  model: nn.Module | None = None) -> Network:
+    """The network as a list of kernel launches (Op) with stage boundaries,
+    BN folded into bf16 weights + fp32 scale/bias, the TMA-window stem and the
+    downsample branch fused into each bottleneck's last conv."""
     device = torch.device(device)
     if model is None:
         model = make_torch_model(name, seed)
@@ -519,7 +503,6 @@ def build_network(name: str, *, batch: int = 1, n_stages: int | None = None, see
             raise ValueError(f"unknown model {name!r}; known: {MODELS}")
     if keep_torch:
         net.torch_model = model
-    net.stage_mode = _BUILD_MODE
     seen = set()
     wb = 0
     for op in net.ops:
@@ -595,10 +578,6 @@ def run_op(op: Op, tb: TaskBuffers, stream, sm_budget: int = 0, timestamps=None)
         if L.out_bf16 and out.dtype != torch.bfloat16:
             raise RuntimeError("bf16 linear output needs a bf16 buffer")
         K.linear(x, L.weight, L.bias, relu=L.relu, out=out, stream=stream)
-    elif op.kind == "pool_linear":
-        L = op.layer
-        K.pool_linear(_view(B[op.src], op.shape_in), L.weight, L.bias, out=_view(B[op.dst], op.shape_out),
-                      grid=0, stream=stream)
     elif op.kind == "dwconv":
         L = op.layer
         K.dwconv(_view(B[op.src], op.shape_in), L.weight, L.scale, L.bias, stride=L.stride, pad=L.pad, relu=L.relu,
@@ -607,103 +586,22 @@ def run_op(op: Op, tb: TaskBuffers, stream, sm_budget: int = 0, timestamps=None)
         raise ValueError(op.kind)
 
 
-# stage execution mode: "persistent" = one stage-kernel launch per stage
-# (csrc/kernels/stage_tc.cu), "layers" = one launch per op (conv_tc.cu + aux.cu)
-STAGE_MODE = os.environ.get("DARIS_STAGE_MODE", "layers")
-_BUILD_MODE = STAGE_MODE
-# persistent mode: CTAs per stage kernel (0 = the partition's SM count)
-STAGE_GRID = int(os.environ.get("DARIS_STAGE_GRID", "0"))
-
-
-def stage_ops(net: Network, stage: int, tb: TaskBuffers) -> list:
-    """The stage's ops as a persistent-kernel op table bound to this buffer set."""
-    B = tb.bufs
-    out = []
-    a, b = net.stage_bounds[stage], net.stage_bounds[stage + 1]
-    for op in net.ops[a:b]:
-        if op.kind == "pack8":
-            n, c, h, w = op.shape_in
-            out.append(K.stage_op(K.OP_PACK8, B["input"], B["packed"], n=n, c=c, h=h, w=w))
-        elif op.kind == "conv":
-            L = op.layer
-            n, h, w, c = op.shape_in
-            _, ho, wo, cout = op.shape_out
-            out.append(K.stage_op(K.OP_CONV, B[op.src], B[op.dst], residual=B[op.res] if op.res else None,
-                                  weight=L.weight, scale=L.scale, bias=L.bias, n=n, h=h, w=w, c=c, cout=cout,
-                                  kh=L.kh, kw=L.kw, stride=L.stride, pad=L.pad, ho=ho, wo=wo, relu=L.relu))
-        elif op.kind in ("maxpool", "maxpool2"):
-            n, h, w, c = op.shape_in
-            _, ho, wo, _ = op.shape_out
-            k, st, pd = (3, 2, 1) if op.kind == "maxpool" else (2, 2, 0)
-            out.append(K.stage_op(K.OP_MAXPOOL, B[op.src], B[op.dst], n=n, h=h, w=w, c=c, kh=k, kw=k, stride=st,
-                                  pad=pd, ho=ho, wo=wo))
-        elif op.kind == "avgpool":
-            n, h, w, c = op.shape_in
-            out.append(K.stage_op(K.OP_AVGPOOL, B[op.src], B[op.dst], n=n, h=h, w=w, c=c))
-        elif op.kind == "linear":
-            L = op.layer
-            src, dst = B[op.src], B[op.dst]
-            n, k = op.shape_in[0], 1
-            for d in op.shape_in[1:]:
-                k *= d
-            flags = (1 if src.dtype == torch.bfloat16 else 0) | (2 if L.out_bf16 else 0)
-            out.append(K.stage_op(K.OP_LINEAR, src, dst, weight=L.weight, bias=L.bias, n=n, c=k,
-                                  cout=op.shape_out[1], relu=L.relu, flags=flags))
-        elif op.kind == "pool_linear":  # the stage kernel runs it as avgpool + linear through "pooled"
-            L = op.layer
-            n, h, w, c = op.shape_in
-            out.append(K.stage_op(K.OP_AVGPOOL, B[op.src], B["pooled"], n=n, h=h, w=w, c=c))
-            out.append(K.stage_op(K.OP_LINEAR, B["pooled"], B[op.dst], weight=L.weight, bias=L.bias, n=n, c=c,
-                                  cout=op.shape_out[1], relu=L.relu, flags=0))
-        elif op.kind == "dwconv":
-            L = op.layer
-            n, h, w, c = op.shape_in
-            _, ho, wo, _ = op.shape_out
-            out.append(K.stage_op(K.OP_DWCONV, B[op.src], B[op.dst], weight=L.weight, scale=L.scale, bias=L.bias,
-                                  n=n, h=h, w=w, c=c, kh=L.k, kw=L.k, stride=L.stride, pad=L.pad, ho=ho, wo=wo,
-                                  relu=L.relu))
-        else:
-            raise ValueError(f"op {op.kind!r} has no persistent-kernel form")
-    return out
-
-
-def stage_launches(net: Network, stage: int, mode: str | None = None) -> int:
+def stage_launches(net: Network, stage: int) -> int:
     """Kernel launches one execution of the stage issues."""
-    if (mode or STAGE_MODE) == "persistent":
-        return 1
     return net.stage_bounds[stage + 1] - net.stage_bounds[stage]
 
 
-def stage_program(net: Network, stage: int, tb: TaskBuffers, grid: int) -> "K.StageProgram":
-    key = (id(net), stage, grid)
-    prog = tb.programs.get(key)
-    if prog is None:
-        a, b = net.stage_bounds[stage], net.stage_bounds[stage + 1]
-        prog = K.StageProgram(stage_ops(net, stage, tb), grid, keep=[op.layer for op in net.ops[a:b]])
-        tb.programs[key] = prog
-    return prog
-
-
-def run_stage(net: Network, stage: int, tb: TaskBuffers, stream, sm_budget: int = 0, mode: str | None = None) -> int:
-    """Launch one stage; returns the number of kernel launches issued."""
-    mode = mode or STAGE_MODE
-    if (mode == "persistent") != (net.stage_mode == "persistent"):
-        raise ValueError(f"network built for stage mode {net.stage_mode!r} cannot run in {mode!r} "
-                         "(build_network(stage_mode=...))")
-    if mode == "persistent":
-        grid = STAGE_GRID or (sm_budget if sm_budget > 0 else K.device_sms())
-        stage_program(net, stage, tb, grid).launch(stream)
-        return 1
+def run_stage(net: Network, stage: int, tb: TaskBuffers, stream, sm_budget: int = 0) -> int:
+    """Launch one stage (one kernel per op); returns the number of launches issued."""
     a, b = net.stage_bounds[stage], net.stage_bounds[stage + 1]
     for op in net.ops[a:b]:
         run_op(op, tb, stream, sm_budget)
     return b - a
 
 
-def forward(net: Network, tb: TaskBuffers, x: torch.Tensor | None = None, stream=None, sm_budget: int = 0,
-            mode: str | None = None):
+def forward(net: Network, tb: TaskBuffers, x: torch.Tensor | None = None, stream=None, sm_budget: int = 0):
     if x is not None:
         tb.input.copy_(x)
     for s in range(net.n_stages):
-        run_stage(net, s, tb, stream, sm_budget, mode)
+        run_stage(net, s, tb, stream, sm_budget)
     return _view(tb.output, net.output_shape)

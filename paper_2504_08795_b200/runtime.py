@@ -266,6 +266,20 @@ class RunResult:
         return window_stats(self.log, self.periods, {t.id for t in self.tasks if t.priority is Priority.HP},
                             warmup, step, n_steps, self.stalls, self.batch)
 
+    def p99_hp(self, start: float, end: float) -> float:
+        """Nearest-rank p99 (ordered[ceil(0.99 n) - 1]) of the response times of
+        HP jobs released in [start, end) that completed."""
+        log = self.log
+        hp = np.array(sorted(t.id for t in self.tasks if t.priority is Priority.HP))
+        kind, t, job = log["kind"], log["time"], log["job"]
+        n = int(job.max()) + 1 if len(job) else 1
+        rel = np.full(n, np.nan)
+        m = (kind == 0) & np.isin(log["task"], hp) & (t >= start) & (t < end)
+        rel[job[m]] = t[m]
+        m = kind == 5
+        resp = np.sort((t[m] - rel[job[m]])[~np.isnan(rel[job[m]])])
+        return float(resp[max(0, int(math.ceil(0.99 * len(resp))) - 1)]) if len(resp) else 0.0
+
 
 def window_stats(log: np.ndarray, periods: dict[int, float], hp_ids: set[int], warmup: float, step: float,
                  n_steps: int, stalls=(), batch: dict[int, int] | None = None) -> list[dict]:
@@ -424,10 +438,6 @@ class DarisRuntime:
             ctxs = range(1, self.gpu.n_contexts + 1)
             if homes is not None and t.priority is Priority.HP:
                 ctxs = [homes[t.id]]
-            for s in range(self.exec.slots):  # stage programs allocate: build them outside capture
-                for st in range(net.n_stages):
-                    if nets.STAGE_MODE == "persistent":
-                        nets.stage_program(net, st, self.buffers[(t.id, s)], nets.STAGE_GRID or self.sm_budget)
             for k in ctxs:
                 for s in range(self.exec.slots):
                     tb = self.buffers[(t.id, s)]

@@ -1,11 +1,14 @@
 """bench.py's measurement logic on a fake runtime (CPU): the knee search picks
 the feasible rate with the most completed inferences/s (not the highest
-feasible rate), LP jobs rejected by admission count as lost, and a window with
-a GPU-wide stall is re-measured."""
+feasible rate); a rate is feasible only when EVERY window of its run has HP
+miss 0 and LP loss < 2 % (admission rejections count as lost); the timed run
+is never re-measured at the same rate — any failing window steps the rate
+down and repeats the whole run; failures after a GPU-wide pause are tagged."""
 
 from types import SimpleNamespace
 
 import bench
+from paper_2504_08795_b200.runtime import window_ok
 
 
 def _rep(jps, missed_hp=0, released_lp=1000, missed_lp=0, rejected_lp=0, accepted_lp=None):
@@ -16,31 +19,41 @@ def _rep(jps, missed_hp=0, released_lp=1000, missed_lp=0, rejected_lp=0, accepte
                            response_hp=SimpleNamespace(p99=0.0005))
 
 
+def _win(imgs, missed_hp=0, released_lp=100, lost_lp=0, stalls=0):
+    return {"released_hp": 100, "released_lp": released_lp, "missed_hp": missed_hp, "missed_lp": 0,
+            "rejected_lp": lost_lp, "lp_loss": lost_lp / released_lp, "completed_images": imgs, "stalls": stalls}
+
+
 class FakeRuntime:
     """Throughput rises with the rate up to a cliff at 1000/task where admission
-    rejects every LP job (still "feasible" by DMR), HP misses start at 1300."""
+    rejects every LP job, HP misses start at 1300. `pause_at` puts a GPU-wide
+    pause into window 3 of the first `pauses` runs at rates >= 600: that window
+    and every later one lose LP jobs (the MRET-inflated task stays rejected)."""
 
-    def __init__(self, stall_first=0):
+    def __init__(self, pauses=0):
         self.rate = 0.0
         self.afet = {}
-        self.calls = 0
-        self.stall_first = stall_first
+        self.runs = []
+        self.pauses = pauses
 
     def set_rate(self, r):
         self.rate = r
 
     def run(self, duration, warmup, full_load=None):
-        self.calls += 1
-        stalls = 1 if self.calls <= self.stall_first else 0
         r = self.rate
-        if r < 1000:
-            rep = _rep(8 * r)
-        elif r < 1300:
-            rep = _rep(4 * r, rejected_lp=1000)          # every LP job rejected
-        else:
-            rep = _rep(4 * r, missed_hp=3, rejected_lp=1000)
-        return SimpleNamespace(report=rep, stats={"stalls": stalls, "first_stall_at": 0.1,
-                                                   "progress_gap_max": 0.0017})
+        self.runs.append(r)
+        pause = len(self.runs) <= self.pauses and r >= 600
+
+        def windows(warm, step, n):
+            out = []
+            for k in range(n):
+                imgs = 8 * r * step if r < 1000 else 4 * r * step
+                w = _win(imgs, missed_hp=3 if r >= 1300 else 0, lost_lp=100 if r >= 1000 else 0)
+                if pause and k >= 3:
+                    w = _win(imgs, lost_lp=30, stalls=1 if k == 3 else 0)
+                out.append(w)
+            return out
+        return SimpleNamespace(report=_rep(8 * r), windows=windows, stats={"stalls": 0}, trace=[])
 
 
 def test_lp_rejections_count_as_loss():
@@ -48,19 +61,33 @@ def test_lp_rejections_count_as_loss():
     assert not bench.feasible(_rep(100, rejected_lp=30))            # DMR 0 but 3 % of LP jobs lost
     assert bench.feasible(_rep(100, rejected_lp=10, missed_lp=5))   # 1.5 % lost
     assert not bench.feasible(_rep(100, missed_hp=1))
+    assert window_ok(_win(10, lost_lp=1)) and not window_ok(_win(10, lost_lp=2))
+    assert not window_ok(_win(10, missed_hp=1))
 
 
 def test_knee_is_the_throughput_maximum_below_the_admission_cliff():
     rt = FakeRuntime()
-    rate = bench.knee_search(rt, 400.0, 0.1, lambda m: None)
+    rate = bench.knee_search(rt, 400.0, 1.0, 0.5, lambda m: None)
     assert 900 < rate < 1000, rate
 
 
-def test_stalled_windows_are_re_measured():
-    rt = FakeRuntime(stall_first=2)
-    rt.set_rate(500.0)
-    res, attempts, seen = bench.run_clean(rt, 0.1, 0.01, lambda m: None, "t")
-    assert attempts == 3 and seen == 2 and res.stats["stalls"] == 0
+def test_timed_run_steps_down_until_every_window_passes():
+    rt = FakeRuntime(pauses=100)      # every run at >= 600/task is hit by a pause
+    args = SimpleNamespace(step_seconds=0.5, warmup=2, steps=20, timed_attempts=8)
+    rate, res, s, clocks, wall, attempts = bench.timed_knee(rt, 950.0, args, lambda m: None, "t")
+    assert [round(r, 2) for r in rt.runs] == [a["rate_per_task"] for a in attempts]   # one run per attempt
+    assert rate < 600 and s["ok"] and s["windows_failed"] == 0
+    assert all(r2 < r1 for r1, r2 in zip(rt.runs, rt.runs[1:]))
+    # the failing runs failed only in windows at or after the pause
+    assert all(a["windows_failed"] == 17 and a["windows_failed_without_pause"] == 0 for a in attempts[:-1])
+    assert attempts[-1]["windows_failed"] == 0
+
+
+def test_summarize_counts_and_pause_attribution():
+    ws = [_win(50), _win(50, missed_hp=1), _win(50, stalls=1, lost_lp=5), _win(50, lost_lp=5)]
+    s = bench.summarize(ws, 0.5)
+    assert s["windows_failed"] == 3 and s["windows_failed_without_pause"] == 1
+    assert s["inf_per_s"] == 200 / 2.0 and s["missed_hp"] == 1 and not s["ok"]
 
 
 def test_reference_arm_prints_the_contract_line():

@@ -18,13 +18,12 @@ COS = 0.998
 
 @pytest.mark.parametrize("name", ["resnet18", "resnet50", "vgg16", "mobilenet_v2"])
 @pytest.mark.parametrize("batch", [1, 2])
-@pytest.mark.parametrize("mode", ["persistent", "layers"])
-def test_network_matches_torch_cpu(name, batch, mode):
-    net = nets.build_network(name, batch=batch, keep_torch=True, stage_mode=mode)
+def test_network_matches_torch_cpu(name, batch):
+    net = nets.build_network(name, batch=batch, keep_torch=True)
     tb = nets.allocate_buffers(net, sm_budget=74)
     g = torch.Generator().manual_seed(11)
     x = torch.randn(batch, 3, 224, 224, generator=g)
-    out = nets.forward(net, tb, x.cuda(), stream=None, sm_budget=74, mode=mode).float().cpu().clone()
+    out = nets.forward(net, tb, x.cuda(), stream=None, sm_budget=74).float().cpu().clone()
     torch.cuda.synchronize()
     with torch.no_grad():
         ref = net.torch_model(x).float()
@@ -45,65 +44,14 @@ def test_stage_split_covers_network():
     assert abs(r18.flops_per_image - 3.63e9) / 3.63e9 < 0.02
 
 
-@pytest.mark.parametrize("grid", [5, 37, 74, 148, 300])
-def test_persistent_stage_kernel_grid_and_relaunch(grid):
-    """The stage kernel's result must not depend on the grid (claim-order
-    scheduling, any co-residency) and its self-resetting counters must make
-    back-to-back launches of one program identical; it must also agree with
-    the one-launch-per-layer path to bf16 rounding."""
-    net = nets.build_network("resnet50", batch=1, stage_mode="persistent")
-    tb = nets.allocate_buffers(net, sm_budget=grid)
-    x = torch.randn(1, 3, 224, 224, generator=torch.Generator().manual_seed(3)).cuda()
-    outs = []
-    for _ in range(3):
-        tb.input.copy_(x)
-        for st in range(net.n_stages):
-            nets.run_stage(net, st, tb, None, grid, mode="persistent")
-        outs.append(tb.output.clone())
-    torch.cuda.synchronize()
-    net_l = nets.build_network("resnet50", batch=1, stage_mode="layers")  # same seed, same weights
-    tb2 = nets.allocate_buffers(net_l, sm_budget=74)
-    ref = nets.forward(net_l, tb2, x, sm_budget=74, mode="layers").clone()
-    torch.cuda.synchronize()
-    for o in outs[1:]:
-        rel_rep = ((o - outs[0]).norm() / outs[0].norm()).item()
-        assert rel_rep < 1e-2, rel_rep  # split-K fp32 atomics reorder sums: equal up to bf16 rounding
-    rel = ((outs[0] - ref).norm() / ref.norm()).item()
-    assert rel < 2e-2, rel
-
-
-def test_persistent_stage_kernel_concurrent_programs():
-    """Several programs running concurrently on different streams (as DARIS
-    tenants do) produce the same results as when run alone."""
-    net = nets.build_network("resnet18", batch=1, stage_mode="persistent")
-    xs = [torch.randn(1, 3, 224, 224, generator=torch.Generator().manual_seed(20 + i)).cuda() for i in range(6)]
-    alone = []
-    for x in xs:
-        tb = nets.allocate_buffers(net, sm_budget=74)
-        alone.append(nets.forward(net, tb, x, sm_budget=74, mode="persistent").clone())
-    torch.cuda.synchronize()
-    tbs = [nets.allocate_buffers(net, sm_budget=74) for _ in xs]
-    streams = [torch.cuda.Stream() for _ in xs]
-    for _ in range(3):
-        for x, tb, s in zip(xs, tbs, streams):
-            with torch.cuda.stream(s):
-                tb.input.copy_(x)
-                for st in range(net.n_stages):
-                    nets.run_stage(net, st, tb, s.cuda_stream, 74, mode="persistent")
-    torch.cuda.synchronize()
-    for a, tb in zip(alone, tbs):
-        rel = ((tb.output - a).norm() / a.norm()).item()
-        assert rel < 1e-2, rel
-
-
 @pytest.mark.parametrize("name,batch", [("resnet50", 1), ("resnet50", 2), ("resnet18", 1), ("mobilenet_v2", 1)])
 def test_network_at_the_executor_plan(name, batch):
-    """Grids planned for the C2 per-job share (23 SMs): 256-row tiles, fused
+    """Grids planned for the C2 per-job share (23 SMs): split-K, fused
     downsample, stems by TMA — the forms the executor captures."""
-    net = nets.build_network(name, batch=batch, keep_torch=True, stage_mode="layers")
+    net = nets.build_network(name, batch=batch, keep_torch=True)
     tb = nets.allocate_buffers(net, sm_budget=23)
     x = torch.randn(batch, 3, 224, 224, generator=torch.Generator().manual_seed(5))
-    out = nets.forward(net, tb, x.cuda(), stream=None, sm_budget=23, mode="layers").float().cpu().clone()
+    out = nets.forward(net, tb, x.cuda(), stream=None, sm_budget=23).float().cpu().clone()
     torch.cuda.synchronize()
     with torch.no_grad():
         ref = net.torch_model(x).float()

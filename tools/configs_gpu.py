@@ -9,8 +9,10 @@
   tasks   ResNet-50 task count {8,12,16,24} at 4x2 OS=2, knee per count
   c5      C5 on one GPU: task count raised at a fixed per-task rate until the first HP miss
 
-Every knee uses bench.py's search (HP miss = 0, LP DMR < 2 %) and its GPU-stall
-re-measure rule. One JSON object per cell on stdout.
+Every knee uses bench.py's protocol: a probe search over runs whose every 0.5-s
+window must meet HP miss 0 and LP loss < 2 %, then a continuous confirmation
+run (--confirm-seconds) stepping the rate down until all of its windows pass.
+No re-measurement at the same rate. One JSON object per cell on stdout.
 
   python tools/configs_gpu.py c1 c3 c4 tasks [--probe-seconds 0.6] [--c4-cells 2x2_1,4x2_2]
 """
@@ -40,29 +42,38 @@ def emit(d):
     print(json.dumps(d), flush=True)
 
 
-def summary(rep) -> dict:
-    return {"jps": round(rep.jps, 1), "hp_miss": int(rep.missed_hp), "dmr_lp": round(rep.dmr_lp, 4),
-            "lp_loss": round(bench.lp_loss(rep), 4), "constraints_met": bench.feasible(rep),
-            "rejected_lp": int(rep.rejected_lp), "p99_hp_ms": round(rep.response_hp.p99 * 1e3, 3),
-            "p99_lp_ms": round(rep.response_lp.p99 * 1e3, 3)}
+STEP = 0.5
+
+
+def summary(res, warm: float, n: int) -> dict:
+    w = bench.summarize(res.windows(warm, STEP, n), STEP)
+    rep = res.report
+    return {"jps": round(w["inf_per_s"], 1), "hp_miss": w["missed_hp"], "lp_loss": round(w["lp_loss"], 4),
+            "constraints_met": w["ok"], "windows": w["windows"], "windows_failed": w["windows_failed"],
+            "gpu_pauses": w["stalls"], "rejected_lp": w["rejected_lp"],
+            "p99_hp_ms": round(rep.response_hp.p99 * 1e3, 3), "p99_lp_ms": round(rep.response_lp.p99 * 1e3, 3)}
 
 
 def knee_factor(rt, set_factor, f0: float, probe: float) -> tuple[float, None]:
     """bench.py's knee: the feasible rate factor with the most completed jobs/s."""
-    return bench.knee_search(rt, f0, probe, log, set_rate=set_factor), None
+    return bench.knee_search(rt, f0, probe, STEP, log, set_rate=set_factor), None
 
 
 def confirm(rt, set_factor, f: float, seconds: float):
-    """Timed confirmation at the knee; step down 5 % while it breaks the constraints
-    (bench.TIMED_ATTEMPTS windows; the result records whether they were met)."""
-    for _ in range(bench.TIMED_ATTEMPTS):
+    """Continuous confirmation run at the knee: every window must pass, else
+    the factor steps down (bench.STEP_DOWN) and the run repeats."""
+    n = max(1, int(round(seconds / STEP)))
+    res = None
+    for _ in range(8):
         set_factor(f)
-        res = bench.run_clean(rt, seconds, seconds * 0.1, log, f"confirm {f:.3g}")[0]
-        if bench.feasible(res.report):
-            res.constraints_met = True
+        res = rt.run(duration=1.0 + n * STEP, warmup=1.0, full_load=rt.afet)
+        row = summary(res, 1.0, n)
+        log(f"confirm {f:.4g} {row}")
+        if row["constraints_met"]:
+            res.row = row
             return f, res
-        f *= 0.95
-    res.constraints_met = False
+        f *= bench.STEP_DOWN
+    res.row = row
     return f, res
 
 
@@ -72,13 +83,13 @@ def c1(args):
     rt = DarisRuntime(tasks, gpu, slots=3, seed=0)
     rt.capture_all()
     rt.afet = rt.calibrate_full_load(0.3)
-    res = bench.run_clean(rt, 3.0, 0.3, log, "c1 30jps")[0]
+    res = rt.run(duration=1.0 + 10.0, warmup=1.0, full_load=rt.afet)
     out = {"config": "c1", "rate_per_task": 30.0, "partition_sms": [p["sm_count"] for p in rt.exec.partitions],
-           "isolated_ms": round(sum(rt.stage_nominal["resnet18"]) * 1e3, 3), **summary(res.report)}
+           "isolated_ms": round(sum(rt.stage_nominal["resnet18"]) * 1e3, 3), **summary(res, 1.0, 20)}
     iso = sum(rt.stage_nominal["resnet18"])
     f, best = knee_factor(rt, rt.set_rate, 0.6 * 4 / max(rt.afet.values()) / 2, args.probe_seconds)
-    f, res = confirm(rt, rt.set_rate, f, 2.0)
-    out["knee"] = {"rate_per_task": round(f, 1), **summary(res.report)}
+    f, res = confirm(rt, rt.set_rate, f, args.confirm_seconds)
+    out["knee"] = {"rate_per_task": round(f, 1), **res.row}
     emit(out)
     rt.close()
 
@@ -104,7 +115,7 @@ def c3(args):
         # factor f: every task at f / (its isolated latency); start below the loaded capacity
         f0 = 0.6 * 8 / sum(rt.afet[t.id] / iso[t.model] for t in rt.tasks)
         f, best = knee_factor(rt, set_factor, f0, args.probe_seconds)
-        f, res = confirm(rt, set_factor, f, 2.0)
+        f, res = confirm(rt, set_factor, f, args.confirm_seconds)
         per_model = {}
         for t in rt.tasks:
             per_model.setdefault(t.model, 0.0)
@@ -114,7 +125,7 @@ def c3(args):
         emit({"config": "c3", "stage_migration": mig, "knee_factor": round(f, 4),
               "isolated_ms": {m: round(v * 1e3, 3) for m, v in iso.items()},
               "rate_per_task": {m: round(per_model[m] / 2, 1) for m in models},
-              "model_tflops": round(tflops, 2), **summary(res.report)})
+              "model_tflops": round(tflops, 2), **res.row})
         rt.close()
 
 
@@ -138,10 +149,10 @@ def c4(args):
         iso = sum(rt.stage_nominal["resnet50"])
         f, best = knee_factor(rt, rt.set_rate, 0.6 * min(8, nc * ns) / max(rt.afet.values()) / 8,
                               args.probe_seconds)
-        f, res = confirm(rt, rt.set_rate, f, 1.0)
+        f, res = confirm(rt, rt.set_rate, f, args.confirm_seconds)
         emit({"config": "c4", "cell": f"{nc}x{ns}_{os_:g}", "contexts": nc, "streams": ns, "oversubscription": os_,
               "partition_sms": rt.exec.partitions[0]["sm_count"], "isolated_ms": round(iso * 1e3, 3),
-              "knee_rate_per_task": round(f, 1), "seconds": round(time.time() - t0, 1), **summary(res.report)})
+              "knee_rate_per_task": round(f, 1), "seconds": round(time.time() - t0, 1), **res.row})
         rt.close()
 
 
@@ -153,9 +164,9 @@ def task_scaling(args):
         rt.afet = rt.calibrate_full_load(0.2)
         iso = sum(rt.stage_nominal["resnet50"])
         f, best = knee_factor(rt, rt.set_rate, 0.6 * 8 / max(rt.afet.values()) / n, args.probe_seconds)
-        f, res = confirm(rt, rt.set_rate, f, 1.0)
+        f, res = confirm(rt, rt.set_rate, f, args.confirm_seconds)
         emit({"config": "tasks", "tasks": n, "contexts": 4, "streams": 2, "oversubscription": 2.0,
-              "knee_rate_per_task": round(f, 1), **summary(res.report)})
+              "knee_rate_per_task": round(f, 1), **res.row})
         rt.close()
 
 
@@ -170,10 +181,11 @@ def c5(args):
         rt = DarisRuntime(bench.c2_tasks(rate, list(range(n))), gpu, slots=3, seed=0)
         rt.capture_all()
         rt.afet = rt.calibrate_full_load(0.2)
-        res = bench.run_clean(rt, 1.5, 0.15, log, f"c5 n={n}")[0]
-        ok = bench.feasible(res.report)
-        row = {"config": "c5", "tasks": n, "rate_per_task": rate, **summary(res.report)}
-        log(f"c5 tasks={n} ok={ok} {summary(res.report)}")
+        nwin = max(1, int(round(args.confirm_seconds / STEP)))
+        res = rt.run(duration=1.0 + nwin * STEP, warmup=1.0, full_load=rt.afet)
+        row = {"config": "c5", "tasks": n, "rate_per_task": rate, **summary(res, 1.0, nwin)}
+        ok = row["constraints_met"]
+        log(f"c5 tasks={n} ok={ok} {row}")
         rt.close()
         if not ok:
             emit({**row, "first_failing": True, "max_feasible_tasks": last_ok["tasks"] if last_ok else 0,
@@ -187,7 +199,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("which", nargs="+", choices=["c1", "c3", "c4", "tasks", "c5"])
     ap.add_argument("--c5-rate", type=float, default=500.0, help="per-task JPS for the c5 task-count scan")
-    ap.add_argument("--probe-seconds", type=float, default=0.6)
+    ap.add_argument("--probe-seconds", type=float, default=1.0)
+    ap.add_argument("--confirm-seconds", type=float, default=10.0)
     ap.add_argument("--c4-cells", default="")
     args = ap.parse_args()
     for w in args.which:
