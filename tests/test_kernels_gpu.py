@@ -284,3 +284,46 @@ def test_linear_wide_k(batch, k, o, x_bf16, relu):
     torch.cuda.synchronize()
     ref = x.float() @ w.float().t() + bias
     _close(y, ref.clamp_min(0) if relu else ref)
+
+
+@pytest.mark.parametrize("n,h,cin,cout,k,stride,pad,relu,residual,bn", [
+    (16, 56, 64, 64, 3, 1, 1, 1, False, 0),      # layer1 conv2 at batch 16 (BN=64)
+    (16, 56, 64, 256, 1, 1, 0, 1, True, 128),    # layer1 conv3 + residual (BN=128, short K)
+    (8, 56, 256, 128, 3, 2, 1, 6, False, 128),   # strided, ReLU6
+    (32, 14, 256, 1024, 1, 1, 0, 0, True, 128),  # two-image-row tiles, no activation
+    (4, 28, 128, 128, 3, 1, 1, 1, True, 64),
+])
+def test_conv_persistent_tile_loop(n, h, cin, cout, k, stride, pad, relu, residual, bn):
+    """Large-M launches take conv_persist_kernel (one CTA per planned SM walking
+    tiles, TMEM double-buffered, epilogue overlapped with the next tile): the
+    plan must pick it at a small SM budget, and the result must match torch."""
+    from paper_2504_08795_b200 import kernels as K
+    d = K.conv_desc((n, h, h, cin), cout, k, k, stride, pad, block_n=bn, sm_budget=8)
+    p = K.conv_plan(d)
+    assert p.persist_ctas == 8 and p.splits == 1, (p.persist_ctas, p.splits)
+    _conv_case(n, h, h, cin, cout, k, stride, pad, relu=relu, residual=residual, block_n=bn, sm_budget=8)
+
+
+def test_conv_persistent_matches_one_tile_per_cta():
+    """Same layer, persistent loop vs the one-tile-per-CTA kernel (DARIS_CONV_PERSIST=0):
+    identical bf16 outputs (same MMA order per tile, no split-K)."""
+    import os
+    import subprocess
+    import sys
+    code = ("import torch; from paper_2504_08795_b200 import kernels as K; "
+            "g = torch.Generator().manual_seed(3); "
+            "x = torch.randn(8, 28, 28, 128, generator=g).bfloat16().cuda(); "
+            "w = (torch.randn(256, 3, 3, 128, generator=g) / 34).bfloat16().cuda(); "
+            "s = torch.rand(256, generator=g).cuda() + 0.5; b = torch.randn(256, generator=g).cuda(); "
+            "r = torch.randn(8, 28, 28, 256, generator=g).bfloat16().cuda(); "
+            "y = K.conv2d(x, w, s, b, stride=1, pad=1, residual=r, sm_budget=16); torch.cuda.synchronize(); "
+            "torch.save(y.cpu(), sys.argv[1])")
+    outs = []
+    for flag in ("4", "0"):
+        path = f"/tmp/persist_ab_{flag}.pt"
+        env = dict(os.environ, DARIS_CONV_PERSIST=flag)
+        r = subprocess.run([sys.executable, "-c", "import sys; " + code, path], env=env, capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(torch.load(path))
+    assert torch.equal(outs[0], outs[1])
