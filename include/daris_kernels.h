@@ -82,11 +82,6 @@ typedef struct daris_conv_plan_t {
   int32_t ctas;
   int32_t cluster;          /* CTAs per cluster (split-K through DSMEM), 1 = none */
   int32_t tma_rows;         /* > 0: activations arrive by TMA, M tile = tma_rows whole output rows */
-  int32_t m_sub;            /* UMMA M=128 sub-tiles per CTA: 2 = a 256-row tile (TMA path, no split-K),
-                               opt-in (DARIS_M256) */
-  int32_t persist_ctas;     /* > 0: persistent tile loop on this many CTAs (one per planned SM, TMEM
-                               double-buffered, epilogue overlapped with the next tile's mainloop);
-                               large-M launches: TMA activations, no split-K, >= 4 waves of tiles */
 } daris_conv_plan_t;
 
 int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out);

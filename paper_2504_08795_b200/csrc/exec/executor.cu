@@ -472,34 +472,10 @@ struct NiceGuard {
   }
 };
 
-// DARIS_EXEC_PIN=1: the executor thread runs on one core (the highest one it
-// may use) for the run, so the scheduler never migrates the polling loop.
-struct PinGuard {
-  cpu_set_t old;
-  bool set = false;
-  PinGuard() {
-    const char* e = std::getenv("DARIS_EXEC_PIN");
-    if (!(e && e[0] == '1')) return;
-    if (sched_getaffinity(0, sizeof(old), &old) != 0) return;
-    int last = -1;
-    for (int i = 0; i < CPU_SETSIZE; ++i)
-      if (CPU_ISSET(i, &old)) last = i;
-    if (last < 0) return;
-    cpu_set_t one;
-    CPU_ZERO(&one);
-    CPU_SET(last, &one);
-    set = sched_setaffinity(0, sizeof(one), &one) == 0;
-  }
-  ~PinGuard() {
-    if (set) sched_setaffinity(0, sizeof(old), &old);
-  }
-};
-
 int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warmup, const double* phases,
                    int32_t collect_log, daris_report* report, daris_exec_stats* stats) {
   using clock = std::chrono::steady_clock;
   NiceGuard loop_priority;
-  PinGuard loop_core;
   const daris_exec_config& c = ex->cfg;
   int32_t n_tasks = 0;
   daris_n_tasks(h, &n_tasks);

@@ -104,11 +104,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-template <int BN, int ST = Depth<BN>::kStages, int MT = 1>
+template <int BN, int ST = Depth<BN>::kStages>
 struct SmemLayout {
   static constexpr int kStages = ST;
   static constexpr int kLag = kStages - 1;  // cp.async groups kept in flight per producer thread
-  static constexpr int kABytes = MT * kBM * 128;  // MT = 2: a 256-row A tile (two UMMA M=128 sub-tiles)
+  static constexpr int kABytes = kBM * 128;
   static constexpr int kBBytes = BN * 128;
   static constexpr int kAOff = 0;
   static constexpr int kBOff = kStages * kABytes;
@@ -165,12 +165,12 @@ __device__ __forceinline__ void finalize_row32(const ConvArgs& a, int m, int col
   for (int q = 0; q < 4; ++q) yp[q] = pk[q];
 }
 
-template <int BN, int ST, int MT>
+template <int BN, int ST>
 __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
     conv_igemm_tc_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
                          const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap amap2,
                          const ConvArgs a) {
-  using L = SmemLayout<BN, ST, MT>;
+  using L = SmemLayout<BN, ST>;
   constexpr int kStages = L::kStages;
   constexpr int kLag = L::kLag;
   extern __shared__ uint8_t smem_raw[];
@@ -222,7 +222,7 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
     fence_barrier_init();
   }
   if (warp == 4) {
-    tmem_alloc<MT * BN>(tmem_slot);
+    tmem_alloc<BN>(tmem_slot);
     if (lane == 0) {
       tma_prefetch_desc(&wmap);
       if (a.tma_a) tma_prefetch_desc(&amap);
@@ -351,39 +351,29 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
       const int c1 = a.tma_a ? h0 * a.wo : m0;
       const int c2 = a.tma_a ? img : 0;
 #pragma unroll 1
-      for (int sub = 0; sub < MT; ++sub) {  // MT = 2: rows 128..255 of the tile come from TMEM cols [BN, 2 BN)
-        const int srow = sub * kBM + row;
-        const bool sres = a.res != nullptr && srow < mvalid;
-        const __nv_bfloat16* sres_row = sres ? a.res + static_cast<size_t>(m0 + srow) * a.cout + n0 : nullptr;
-        if (sub > 0 && sres) {
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        uint4 res_nxt[4];
+        if (has_res && c0 + 32 < BN) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) res_cur[q] = ldg_nc16(sres_row + 8 * q);
+          for (int q = 0; q < 4; ++q) res_nxt[q] = ldg_nc16(res_row + c0 + 32 + 8 * q);
         }
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          uint32_t r[32];
-          uint4 res_nxt[4];
-          if (sres && c0 + 32 < BN) {
+        tmem_ld_32x32b_x32(t_row + c0, r);
+        uint8_t* rowp = stage + (c0 >> 6) * (kBM * 128) + row * 128;
+        const uint32_t chunk0 = static_cast<uint32_t>((c0 & 63) >> 3);
+        uint4 pk[4];
+        pack_row32(a, c0, reinterpret_cast<const float*>(r), s_scale, s_bias, res_cur, has_res, pk);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) res_nxt[q] = ldg_nc16(sres_row + c0 + 32 + 8 * q);
-          }
-          tmem_ld_32x32b_x32(t_row + sub * BN + c0, r);
-          uint8_t* rowp = stage + (c0 >> 6) * (MT * kBM * 128) + srow * 128;
-          const uint32_t chunk0 = static_cast<uint32_t>((c0 & 63) >> 3);
-          uint4 pk[4];
-          pack_row32(a, c0, reinterpret_cast<const float*>(r), s_scale, s_bias, res_cur, sres, pk);
+        for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(rowp + (((chunk0 + q) ^ swz) << 4)) = pk[q];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(rowp + (((chunk0 + q) ^ swz) << 4)) = pk[q];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) res_cur[q] = res_nxt[q];
-        }
+        for (int q = 0; q < 4; ++q) res_cur[q] = res_nxt[q];
       }
       fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the TMA engine
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (threadIdx.x == 0) {
 #pragma unroll
         for (int h = 0; h < BN / 64; ++h)
-          tma_store_3d(&ymap, stage + h * (MT * kBM * 128), n0 + h * 64, c1, c2);
+          tma_store_3d(&ymap, stage + h * (kBM * 128), n0 + h * 64, c1, c2);
         bulk_commit();
         bulk_wait_read();
       }
@@ -507,14 +497,11 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
         mbar_wait(&full[s], (i / kStages) & 1);
         tc_fence_after();
         const uint64_t bdesc = umma_desc_k_sw128(sB_u32 + s * L::kBBytes);
+        const uint64_t adesc = umma_desc_k_sw128(sA_u32 + s * L::kABytes);
 #pragma unroll
-        for (int sub = 0; sub < MT; ++sub) {  // M sub-tile sub: A rows [128 sub, 128 sub + 128), TMEM cols [BN sub, ...)
-          const uint64_t adesc = umma_desc_k_sw128(sA_u32 + s * L::kABytes + sub * (kBM * 128));
-#pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            // +32 B along K inside the 128 B swizzle atom = +2 in the encoded start address
-            umma_bf16(tmem_base + sub * BN, adesc + 2 * k, bdesc + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
-          }
+        for (int k = 0; k < kBK / 16; ++k) {
+          // +32 B along K inside the 128 B swizzle atom = +2 in the encoded start address
+          umma_bf16(tmem_base, adesc + 2 * k, bdesc + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
         }
         umma_commit(&empty[s]);
       }
@@ -606,239 +593,12 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
   __syncthreads();
   if (warp == 4) {
     tc_fence_after();
-    tmem_dealloc<MT * BN>(tmem_base);
+    tmem_dealloc<BN>(tmem_base);
   }
   if (ts && threadIdx.x == 0) ts[6] = gtimer();
 }
 
 // ---------------------------------------------------------------------------
-// Persistent tile loop for large-M convolutions (batched jobs, single-tenant
-// batching): TMA activations (th whole output rows per M tile, as above), no
-// split-K, TMA-store epilogue. One CTA per SM walks tiles t = blockIdx.x,
-// + gridDim.x, ... (N-tile fastest, so concurrent CTAs share an A tile in L2).
-// The accumulator is double-buffered in TMEM (2 x BN columns) and the output
-// staging in smem (2 buffers): the MMA thread fills buffer j & 1 for tile j
-// while the epilogue drains the other, and the operand ring runs across tile
-// boundaries, so the one-tile-per-CTA kernel's fixed per-tile cost (TMEM
-// alloc, barrier init, pipeline fill, an epilogue nothing overlaps) is paid
-// once per SM. TMA requests from one thread are served one after another
-// (tools/tma_stream_probe.cu), so three warps issue them:
-//   warps 0-3  epilogue: TMEM -> regs -> scale/bias (+ residual, read from the
-//              staging buffer) -> act -> bf16 written in place -> TMA store
-//   warp 4     weight (B) producer, TMEM owner
-//   warp 5     MMA issuer (one thread)
-//   warp 6     activation (A) producer
-//   warp 7     epilogue producer: scale/bias (1-D bulk copies) and the residual
-//              tile (TMA, same 128B-swizzled layout as the output) into the
-//              staging buffer before the epilogue reaches it
-constexpr int kPThreads = 256;
-
-template <int BN, int ST>
-struct PersistLayout {
-  static constexpr int kABytes = kBM * 128;
-  static constexpr int kBBytes = BN * 128;
-  static constexpr int kAOff = 0;
-  static constexpr int kBOff = ST * kABytes;
-  static constexpr int kCBytes = (BN / 64) * kBM * 128;   // one staging buffer: BN/64 halves of 128 rows x 128 B
-  static constexpr int kCOff = kBOff + ST * kBBytes;      // 2 staging buffers
-  static constexpr int kSOff = kCOff + 2 * kCBytes;       // 2 x (scale[BN], bias[BN]) fp32
-  static constexpr int kBarOff = kSOff + 2 * 2 * BN * 4;
-  static constexpr int kTotal = kBarOff + 256 + 1024;
-};
-
-template <int BN, int ST>
-__global__ void __launch_bounds__(kPThreads, (BN == 64 ? 2 : 1))
-    conv_persist_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
-                        const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap amap2,
-                        const __grid_constant__ CUtensorMap rmap, const ConvArgs a, int tiles_n, int n_tiles) {
-  using L = PersistLayout<BN, ST>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem + L::kAOff;
-  uint8_t* sB = smem + L::kBOff;
-  uint8_t* sC = smem + L::kCOff;
-  float* sS = reinterpret_cast<float*>(smem + L::kSOff);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
-  uint64_t* empty = full + ST;
-  uint64_t* tfull = empty + ST;     // [2] accumulator buffer ready (MMA -> epilogue)
-  uint64_t* tempty = tfull + 2;     // [2] accumulator buffer drained (epilogue -> MMA)
-  uint64_t* cready = tempty + 2;    // [2] staging buffer: scale/bias (+ residual) landed
-  uint64_t* cfree = cready + 2;     // [2] staging buffer: its TMA store has read it
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(cfree + 2);
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  const bool has_res = a.res != nullptr;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < ST; ++s) {
-      mbar_init(&full[s], 2);  // A and B producers each arrive with their own expect_tx
-      mbar_init(&empty[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);  // one elected lane per epilogue warp
-      mbar_init(&cready[b], 1);
-      mbar_init(&cfree[b], 1);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 4) {
-    tmem_alloc<2 * BN>(tmem_slot);
-    if (lane == 0) {
-      tma_prefetch_desc(&wmap);
-      tma_prefetch_desc(&amap);
-      tma_prefetch_desc(&ymap);
-      if (a.kb_seg1 < a.num_kb) tma_prefetch_desc(&amap2);
-      if (has_res) tma_prefetch_desc(&rmap);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem_base = *tmem_slot;
-  const int nkb = a.num_kb;
-
-  if (warp == 4 || warp == 6) {
-    if (lane == 0) {
-      // ---------------- operand producers: warp 4 weights, warp 6 activations ----------------
-      const bool is_b = warp == 4;
-      const uint32_t a_bytes = static_cast<uint32_t>(a.th * a.wo * 128);
-      if (!is_b) pdl_wait();  // activations come from the previous layer
-      int g = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int tm = t / tiles_n, tn = t - tm * tiles_n;
-        const int img = fdiv(tm, a.d_tiles_h);
-        const int h0 = (tm - img * a.tiles_h) * a.th;
-        const int n0 = tn * BN;
-        for (int i = 0; i < nkb; ++i, ++g) {
-          const int s = g % ST;
-          if (g >= ST) mbar_wait(&empty[s], ((g / ST) & 1) ^ 1);
-          if (is_b) {
-            mbar_arrive_expect_tx(&full[s], L::kBBytes);
-            tma_load_2d(&wmap, &full[s], sB + s * L::kBBytes, i * kBK, n0);
-            continue;
-          }
-          mbar_arrive_expect_tx(&full[s], a_bytes);
-          uint8_t* dst = sA + s * L::kABytes;
-          if (a.stem_tma) {
-            tma_load_4d(&amap, &full[s], dst, 0, 0, h0 * a.stride + i, img);
-          } else if (i >= a.kb_seg1) {
-            tma_load_4d(&amap2, &full[s], dst, (i - a.kb_seg1) * kBK, 0, h0 * a.stride2, img);
-          } else {
-            const int kpos = fdiv(i, a.d_cinb);
-            const int cb = i - kpos * a.cin_blocks;
-            const int r_ = fdiv(kpos, a.d_kw), s_ = kpos - r_ * a.kw;
-            tma_load_4d(&amap, &full[s], dst, cb * kBK, s_ - a.pad, h0 * a.stride - a.pad + r_, img);
-          }
-        }
-      }
-    }
-  } else if (warp == 7) {
-    if (lane == 0) {
-      // ---------------- epilogue producer: scale/bias + residual into the staging buffer ----------------
-      pdl_wait();  // residuals come from earlier layers
-      const uint32_t res_bytes = has_res ? static_cast<uint32_t>(a.box_rows * BN * 2) : 0u;
-      int j = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++j) {
-        const int tm = t / tiles_n, tn = t - tm * tiles_n;
-        const int img = fdiv(tm, a.d_tiles_h);
-        const int h0 = (tm - img * a.tiles_h) * a.th;
-        const int n0 = tn * BN;
-        const int sb = j & 1;
-        mbar_wait(&cfree[sb], ((j >> 1) & 1) ^ 1);  // the TMA store of tile j - 2 has read this buffer
-        mbar_arrive_expect_tx(&cready[sb], static_cast<uint32_t>(2 * BN * 4) + res_bytes);
-        bulk_load_1d(sS + sb * 2 * BN, a.scale + n0, BN * 4, &cready[sb]);
-        bulk_load_1d(sS + sb * 2 * BN + BN, a.bias + n0, BN * 4, &cready[sb]);
-        if (has_res) {
-#pragma unroll
-          for (int hh = 0; hh < BN / 64; ++hh)
-            tma_load_3d(&rmap, &cready[sb], sC + sb * L::kCBytes + hh * (kBM * 128), n0 + hh * 64, h0 * a.wo, img);
-        }
-      }
-    }
-  } else if (warp == 5) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
-      constexpr uint32_t idesc = umma_idesc_bf16(kBM, BN);
-      const uint32_t sA_u32 = smem_u32(sA), sB_u32 = smem_u32(sB);
-      int g = 0, j = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++j) {
-        const int b = j & 1;
-        mbar_wait(&tempty[b], ((j >> 1) & 1) ^ 1);  // the epilogue drained this buffer (free at first use)
-        tc_fence_after();
-        const uint32_t d = tmem_base + static_cast<uint32_t>(b * BN);
-        for (int i = 0; i < nkb; ++i, ++g) {
-          const int s = g % ST;
-          mbar_wait(&full[s], (g / ST) & 1);
-          tc_fence_after();
-          const uint64_t adesc = umma_desc_k_sw128(sA_u32 + s * L::kABytes);
-          const uint64_t bdesc = umma_desc_k_sw128(sB_u32 + s * L::kBBytes);
-#pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) umma_bf16(d, adesc + 2 * k, bdesc + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
-          umma_commit(&empty[s]);  // the ring slot is free once these MMAs have read it
-        }
-        umma_commit(&tfull[b]);
-      }
-    }
-  } else {
-    // ---------------- epilogue (warps 0-3: TMEM lanes 32*warp ...) ----------------
-    const int row = warp * 32 + lane;
-    const uint32_t swz = static_cast<uint32_t>(row & 7);
-    const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
-    int j = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++j) {
-      const int tm = t / tiles_n, tn = t - tm * tiles_n;
-      const int img = fdiv(tm, a.d_tiles_h);
-      const int h0 = (tm - img * a.tiles_h) * a.th;
-      const int n0 = tn * BN;
-      const int b = j & 1, sb = j & 1;
-      mbar_wait(&cready[sb], (j >> 1) & 1);
-      mbar_wait(&tfull[b], (j >> 1) & 1);
-      tc_fence_after();
-      if (threadIdx.x == 0 && t + static_cast<int>(gridDim.x) >= n_tiles) pdl_trigger();  // last tile's MMAs are done
-      const float* s_scale = sS + sb * 2 * BN;
-      const float* s_bias = s_scale + BN;
-      uint8_t* stage = sC + sb * L::kCBytes;
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_row + static_cast<uint32_t>(b * BN + c0), r);
-        uint8_t* rowp = stage + (c0 >> 6) * (kBM * 128) + row * 128;
-        const uint32_t chunk0 = static_cast<uint32_t>((c0 & 63) >> 3);
-        uint4 res4[4];
-        if (has_res) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) res4[q] = *reinterpret_cast<const uint4*>(rowp + (((chunk0 + q) ^ swz) << 4));
-        }
-        uint4 pk[4];
-        pack_row32(a, c0, reinterpret_cast<const float*>(r), s_scale, s_bias, res4, has_res, pk);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(rowp + (((chunk0 + q) ^ swz) << 4)) = pk[q];
-      }
-      // this warp's TMEM rows are in registers: hand the accumulator buffer back to the MMA thread
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[b]);
-      fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the TMA engine
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (threadIdx.x == 0) {
-#pragma unroll
-        for (int hh = 0; hh < BN / 64; ++hh) tma_store_3d(&ymap, stage + hh * (kBM * 128), n0 + hh * 64, h0 * a.wo, img);
-        bulk_commit();
-        bulk_wait_read_n<1>();                      // tile j - 1's store has read its buffer ...
-        if (j > 0) mbar_arrive(&cfree[sb ^ 1]);    // ... which the epilogue producer may refill
-      }
-    }
-    if (threadIdx.x == 0) bulk_wait_read_n<0>();
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 4) {
-    tc_fence_after();
-    tmem_dealloc<2 * BN>(tmem_base);
-  }
-}
-
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -853,10 +613,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
-template <int BN, int ST = Depth<BN>::kStages, int MT = 1, bool PERSIST = false>
+template <int BN, int ST = Depth<BN>::kStages>
 static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cudaStream_t st) {
-  using L = SmemLayout<BN, ST, MT>;
-  using PL = PersistLayout<BN, ST>;
+  using L = SmemLayout<BN, ST>;
   auto encode = get_encode_fn();
   if (!encode) return DARIS_K_NO_DRIVER;
   const int K = ((d->flags & DARIS_CONV_PADDED_INPUT) ? d->kh * 64 : d->kh * d->kw * d->cin) +
@@ -907,9 +666,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
 
   // epilogue by TMA store (splits == 1): the output as a 3-D tensor {cout, rows, images}
   // whose box is one M tile (th whole output rows of one image, or 128 flat rows)
-  static const bool no_tma_c = std::getenv("DARIS_NO_TMA_STORE") != nullptr;  // experiment knob
-  const bool tma_c = !no_tma_c && pl.splits == 1;
-  if (MT > 1 && !tma_c) return DARIS_K_BAD_SHAPE;  // 256-row tiles leave through the TMA-store epilogue only
+  const bool tma_c = pl.splits == 1;
   CUtensorMap ymap;
   std::memset(&ymap, 0, sizeof(ymap));
   int box_rows = 0;
@@ -947,39 +704,12 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   }
 
   static bool attr_set = false;  // per template instantiation
-  if constexpr (PERSIST) {
-   if (!attr_set) {
-    set_max_carveout(reinterpret_cast<const void*>(conv_persist_kernel<BN, ST>));
-    cudaError_t e = cudaFuncSetAttribute(conv_persist_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         PL::kTotal);
+  if (!attr_set) {
+    set_max_carveout(reinterpret_cast<const void*>(conv_igemm_tc_kernel<BN, ST>));
+    cudaError_t e =
+        cudaFuncSetAttribute(conv_igemm_tc_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
     if (e != cudaSuccess) return e;
     attr_set = true;
-   }
-  }
-  if (!PERSIST && !attr_set) {
-    set_max_carveout(reinterpret_cast<const void*>(conv_igemm_tc_kernel<BN, ST, MT>));
-    cudaError_t e = cudaFuncSetAttribute(conv_igemm_tc_kernel<BN, ST, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         L::kTotal);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-    if (std::getenv("DARIS_PRINT_OCC")) {  // diagnostics: resident CTAs per SM for this instantiation
-      int occ = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, conv_igemm_tc_kernel<BN, ST, MT>, kThreads, L::kTotal);
-      cudaFuncAttributes fa{};
-      cudaFuncGetAttributes(&fa, conv_igemm_tc_kernel<BN, ST, MT>);
-      std::fprintf(stderr, "conv_igemm_tc_kernel<%d,%d,%d>: %d CTAs/SM (smem %d B dyn + %zu static, %d regs)\n", BN, ST,
-                   MT, occ, L::kTotal, fa.sharedSizeBytes, fa.numRegs);
-      for (int sm : {0, 16384, 32768, 49152, 65536, 70000, 100000}) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, conv_igemm_tc_kernel<BN, ST, MT>, kThreads, sm);
-        std::fprintf(stderr, "   dyn smem %d: %d CTAs/SM\n", sm, occ);
-      }
-      int carve = -1, maxdyn = -1;
-      cudaFuncGetAttributes(&fa, conv_igemm_tc_kernel<BN, ST, MT>);
-      carve = fa.preferredShmemCarveout;
-      maxdyn = fa.maxDynamicSharedSizeBytes;
-      std::fprintf(stderr, "   carveout attr %d, max dyn %d, maxThreads %d, localBytes %zu\n", carve, maxdyn,
-                   fa.maxThreadsPerBlock, fa.localSizeBytes);
-    }
   }
   ConvArgs a;
   a.x = static_cast<const __nv_bfloat16*>(d->x);
@@ -1036,31 +766,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
     attr[cfg.numAttrs].val.clusterDim.z = pl.cluster;
     cfg.numAttrs++;
   }
-  if constexpr (PERSIST) {
-    if (!tma_c || pl.tma_rows <= 0 || pl.splits != 1 || pl.persist_ctas < 1) return DARIS_K_BAD_SHAPE;
-    // the residual as the output's 3-D tensor {cout, rows, images}: its boxes land in the
-    // staging buffer in exactly the layout the epilogue writes the output in
-    CUtensorMap rmap;
-    std::memset(&rmap, 0, sizeof(rmap));
-    if (d->residual) {
-      const cuuint64_t rows = static_cast<cuuint64_t>(d->ho) * d->wo;
-      cuuint64_t rdims[3] = {static_cast<cuuint64_t>(d->cout), rows, static_cast<cuuint64_t>(d->n)};
-      cuuint64_t rstr[2] = {static_cast<cuuint64_t>(d->cout) * 2, rows * d->cout * 2};
-      cuuint32_t rbox[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
-      cuuint32_t restr[3] = {1, 1, 1};
-      if (encode(&rmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(d->residual), rdims, rstr, rbox, restr,
-                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return DARIS_K_BAD_ARG;
-    }
-    cfg.gridDim = dim3(pl.persist_ctas);
-    cfg.blockDim = dim3(kPThreads);
-    cfg.dynamicSmemBytes = PL::kTotal;
-    return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_persist_kernel<BN, ST>, map, amap, ymap, amap2, rmap, a,
-                                               pl.tiles_n, pl.tiles_m * pl.tiles_n));
-  } else {
-    return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN, ST, MT>, map, amap, ymap, amap2, a));
-  }
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN, ST>, map, amap, ymap, amap2, a));
 }
 
 
@@ -1095,33 +801,22 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
   const int budget = d->sm_budget > 0 ? d->sm_budget : daris_device_sms();
   // Activations by TMA (4-D box of th whole output rows) unless the layer is a
   // stem (8 channels: pixel-chunk gather) or a box side would exceed 256.
-  static const bool tma_off = std::getenv("DARIS_CONV_GATHER") != nullptr;  // experiment knob
   const int th = std::max(1, std::min(d->ho, kBM / d->wo));
   const bool tma_a = padded || dual ||
-                     (!tma_off && d->cin % kBK == 0 && d->wo * d->stride <= 256 && th * d->stride <= 256 &&
+                     (d->cin % kBK == 0 && d->wo * d->stride <= 256 && th * d->stride <= 256 &&
                       d->wo <= kBM);
   const int tiles_h = (d->ho + th - 1) / th;
   const int tiles_m = tma_a ? d->n * tiles_h : (M + kBM - 1) / kBM;
   int bn = d->block_n;
   if (bn == 0) {
-    static const int bn_max = [] {  // experiment knob: widest automatic tile
-      const char* e = std::getenv("DARIS_CONV_BN_MAX");
-      return e ? std::atoi(e) : 128;
-    }();
-    bn = (d->cout % 128 == 0 && bn_max >= 128) ? 128 : 64;
+    bn = d->cout % 128 == 0 ? 128 : 64;
     // 64-wide tiles when the 128-wide grid leaves resident CTA slots of the
     // planned SMs idle (3 per SM) and the 64-wide grid still fits in them:
     // twice the CTAs, each with half the epilogue, finish sooner. Batch 1 at 23
     // planned SMs: loaded capacity 15.2k -> 15.6k inf/s at 4x2, 21.5k -> 22.7k at
     // 16 jobs; large batches keep their 128-wide plans (profiles/r01_bn_rule_ab.txt).
-    // DARIS_BN_RULE=0: the earlier rule (narrow only below one CTA per SM);
-    // 1: narrow whenever the 128-wide grid is below 3 CTAs per SM
-    static const int bn_rule = [] {
-      const char* e = std::getenv("DARIS_BN_RULE");
-      return e ? std::atoi(e) : 2;
-    }();
     const int t128 = tiles_m * (d->cout / 128), t64 = 2 * t128;
-    if (bn == 128 && (bn_rule == 0 ? t128 < budget : t128 < 3 * budget && (bn_rule != 2 || t64 <= 3 * budget)))
+    if (bn == 128 && t128 < 3 * budget && t64 <= 3 * budget)
       bn = 64;
   }
   if (bn != 64 && bn != 128 && bn != 256) return DARIS_K_BAD_SHAPE;
@@ -1141,64 +836,21 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
       if (splits < 1) splits = 1;
     }
   }
-  static const int split_cap = [] {
-    const char* e = std::getenv("DARIS_SPLITK_MAX");  // experiment knob: cap the split-K factor
-    return e ? std::atoi(e) : 0;
-  }();
-  if (split_cap > 0 && splits > split_cap) splits = split_cap;
   // a cluster holds at most 8 CTAs (portable size)
   if ((d->flags & DARIS_CONV_CLUSTER_SPLITK) && bn == 64 && splits > 8) splits = 8;
   if (splits > num_kb) splits = num_kb;
   int kbps = (num_kb + splits - 1) / splits;
   splits = (num_kb + kbps - 1) / kbps;  // no empty splits
-  // 256-row tiles (two UMMA M=128 sub-tiles, 2*BN TMEM columns) when the grid
-  // would exceed the planned SMs anyway: half the CTAs, each weight tile loaded
-  // once for twice the rows. Measured slower at batch 1 (ResNet-50 at 24 SMs
-  // 0.44 vs 0.37 ms isolated, 13.9k vs 15.6k inf/s loaded capacity: the lost
-  // parallelism costs more than the per-CTA overheads saved) — opt-in, DARIS_M256=1
-  // DARIS_M256=1: everywhere; DARIS_M256=stem: the 8-channel stem only
-  static const int m256_mode = [] {
-    const char* e = std::getenv("DARIS_M256");
-    if (!e || std::getenv("DARIS_NO_TMA_STORE")) return 0;
-    return std::strcmp(e, "stem") == 0 ? 2 : 1;
-  }();
-  const bool m256_here = m256_mode == 1 || (m256_mode == 2 && padded);
-  int m_sub = 1;
-  int th_used = th, tiles_m_used = tiles_m;
-  if (m256_here && tma_a && splits == 1 && bn <= 128 && tiles > budget) {
-    const int th2 = std::max(1, std::min(d->ho, 2 * kBM / d->wo));
-    if (th2 * d->wo > kBM && th2 * d->stride <= 256 && (!dual || th2 * d->stride2 <= 256)) {
-      m_sub = 2;
-      th_used = th2;
-      tiles_m_used = d->n * ((d->ho + th2 - 1) / th2);
-    }
-  }
-  // Persistent tile loop (conv_persist_kernel) for large-M launches: TMA
-  // activations, no split-K, at least PERSIST_WAVES waves of tiles over the
-  // planned SMs; one CTA per planned SM. DARIS_CONV_PERSIST=0 turns it off.
-  static const int persist_waves = [] {
-    const char* e = std::getenv("DARIS_CONV_PERSIST");
-    return e ? std::atoi(e) : 4;
-  }();
-  out->persist_ctas = 0;
-  static const int persist_cps = [] {  // experiment: persistent CTAs per planned SM (2: 64-wide tiles)
-    const char* e = std::getenv("DARIS_PERSIST_CPS");
-    return e ? std::atoi(e) : 1;
-  }();
-  if (persist_waves > 0 && tma_a && splits == 1 && m_sub == 1 && tiles >= persist_waves * budget &&
-      !std::getenv("DARIS_NO_TMA_STORE"))
-    out->persist_ctas = std::min(tiles, persist_cps * budget);
   out->block_n = bn;
   out->splits = splits;
   out->kb_per_split = kbps;
-  out->tiles_m = tiles_m_used;
+  out->tiles_m = tiles_m;
   out->tiles_n = tiles_n;
   out->workspace_floats = splits > 1 ? static_cast<int64_t>(tiles) * kBM * bn : 0;  // zero-initialised
   out->counters = splits > 1 ? 2 * tiles : 0;  // ticket + done per tile
-  out->ctas = tiles_m_used * tiles_n * splits;
-  out->m_sub = m_sub;
+  out->ctas = tiles_m * tiles_n * splits;
   out->cluster = (splits > 1 && bn == 64 && (d->flags & DARIS_CONV_CLUSTER_SPLITK)) ? splits : 1;
-  out->tma_rows = tma_a ? th_used : 0;
+  out->tma_rows = tma_a ? th : 0;
   if (out->cluster > 1) {  // partials reduce through DSMEM: no global scratch
     out->workspace_floats = 0;
     out->counters = 0;
@@ -1215,32 +867,9 @@ extern "C" int daris_conv2d(const daris_conv_desc* d, void* stream) {
   if ((d->flags & DARIS_CONV_DUAL) && !d->x2) return DARIS_K_BAD_ARG;
   if (pl.splits > 1 && pl.cluster == 1 && (!d->workspace || !d->counters)) return DARIS_K_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // Deeper rings for long K loops by TMA (each CTA streams >= 12 K blocks): more
-  // bytes in flight per SM at the cost of co-residency (experiment knob for now)
-  static const bool deep = [] {
-    const char* e = std::getenv("DARIS_CONV_DEEP");
-    return e && std::atoi(e) != 0;
-  }();
-  const bool go_deep = deep && pl.tma_rows > 0 && pl.kb_per_split >= 12;
-  if (pl.m_sub == 2) {
-    switch (pl.block_n) {
-      case 64: return launch_bn<64, 2, 2>(d, pl, st);
-      case 128: return launch_bn<128, 2, 2>(d, pl, st);
-    }
-    return DARIS_K_BAD_SHAPE;
-  }
-  if (pl.persist_ctas > 0) {
-    switch (pl.block_n) {
-      case 64:
-        if (pl.persist_ctas > 148) return launch_bn<64, 3, 1, true>(d, pl, st);  // 2 per SM
-        return launch_bn<64, 6, 1, true>(d, pl, st);
-      case 128: return launch_bn<128, 4, 1, true>(d, pl, st);
-    }
-    return DARIS_K_BAD_SHAPE;
-  }
   switch (pl.block_n) {
-    case 64: return go_deep ? launch_bn<64, 5>(d, pl, st) : launch_bn<64>(d, pl, st);
-    case 128: return go_deep ? launch_bn<128, 4>(d, pl, st) : launch_bn<128>(d, pl, st);
+    case 64: return launch_bn<64>(d, pl, st);
+    case 128: return launch_bn<128>(d, pl, st);
     case 256: return launch_bn<256>(d, pl, st);
   }
   return DARIS_K_BAD_SHAPE;
