@@ -140,9 +140,14 @@ typedef struct daris_report {
 } daris_report;
 
 typedef struct daris_trace_entry {
-  int32_t task, job, stage, _pad;
+  int32_t task, job, stage;
+  int32_t flags;            /* DARIS_TRACE_UNSAMPLED: the stage completes without recording its
+                               time into the MRET window (the recorded run had it in flight
+                               across a GPU-wide pause); 0 in every reference-parity trace */
   double duration;
 } daris_trace_entry;
+
+enum { DARIS_TRACE_UNSAMPLED = 1 };
 
 /* one task of a context's ctx_tasks list, for daris_eval_ledger */
 typedef struct daris_ledger_entry {
@@ -186,6 +191,14 @@ int daris_dispatch(daris_handle* h, int32_t context, int32_t stream, double t, d
                    int32_t* found);
 int daris_complete(daris_handle* h, int32_t job_id, int32_t stage, double t, int32_t* job_done,
                    int32_t* missed);
+/* daris_complete with record_sample = 0: the stage completes as in
+ * Scheduler.complete_stage but its observed time does not enter the MRET
+ * window (timing.py:45-50 not applied). Used by the real-time executor for
+ * stages that were in flight across a detected GPU-wide pause, which would
+ * otherwise freeze an inflated utilisation until the task's next completion
+ * (timing.py:92-114). record_sample = 1 is exactly daris_complete. */
+int daris_complete_ex(daris_handle* h, int32_t job_id, int32_t stage, double t, int32_t record_sample,
+                      int32_t* job_done, int32_t* missed);
 int daris_ready_count(const daris_handle* h, int32_t context, int32_t* out);
 
 int daris_ledger(daris_handle* h, int32_t context, daris_ledger_t* out);

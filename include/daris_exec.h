@@ -41,7 +41,8 @@ typedef struct daris_exec_config {
 typedef struct daris_exec_partition {
   int32_t context;          /* 1-based */
   int32_t sm_count;         /* SMs the partition actually owns */
-  int32_t first_group, n_groups;
+  int32_t first_group, n_groups; /* cyclic window of layout units: unit 0 = the SMs the group split
+                                    leaves over (28 on B200), then the co-scheduled groups */
   int32_t green;            /* 1 if a green context backs it */
   int32_t group_size;       /* SMs per co-scheduling group: the largest thread-block cluster
                                a kernel in this partition can launch (8; 2 with DARIS_PART_GROUP=2) */
@@ -53,6 +54,10 @@ typedef struct daris_stage_trace {
   double start, end;        /* quantised executor time (s) */
   double gpu_start, gpu_end; /* device time (s) of the stage's first / last work on its stream, from
                                 timing events (only when DARIS_GPU_TIMING is set; NaN otherwise) */
+  int32_t sampled;          /* 1: its time entered the MRET window; 0: it was in flight across a
+                               detected GPU-wide pause and completed via daris_complete_ex(.., 0, ..)
+                               (replay it with DARIS_TRACE_UNSAMPLED) */
+  int32_t _pad;
 } daris_stage_trace;
 
 typedef struct daris_exec_stats {
@@ -71,6 +76,7 @@ typedef struct daris_exec_stats {
   int64_t slot_deferred;    /* stage-0 launches held (stream kept) until a buffer set freed up:
                                more live jobs of one task than it has buffer sets */
   int64_t slot_backlog_max; /* most admitted jobs of one task waiting for a buffer set */
+  int64_t unsampled;        /* stages completed without an MRET sample (in flight across a stall) */
 } daris_exec_stats;
 
 typedef struct daris_exec daris_exec;

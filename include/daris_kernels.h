@@ -115,6 +115,41 @@ int daris_avgpool(const void* x, float* y, int32_t n, int32_t hw, int32_t c, voi
 int daris_linear(const void* x, int32_t x_bf16, const void* w, const float* bias, void* y, int32_t y_bf16,
                  int32_t batch, int32_t k, int32_t o, int32_t relu, void* stream);
 
+/* Linear layer on the tensor cores (tcgen05, swap-AB: 128 output features x
+ * a batch tile of 16..256 rows per UMMA, both operands by TMA), any batch:
+ * y[b][o] = act(sum_k x[b][k] * w[o][k] + bias[o]); x bf16 [batch][k],
+ * w bf16 [o][k], k % 64 == 0; y fp32 or bf16 (y_bf16). Long-K / few-tile shapes
+ * (weight streaming at small batch) split K across CTAs: the partials go to
+ * `workspace` (daris_linear_plan().workspace_floats, zero-initialised, left
+ * zeroed) with one self-resetting ticket per tile in `counters`. */
+typedef struct daris_linear_desc {
+  const void* x;
+  const void* w;
+  const float* bias;      /* [o] or NULL */
+  void* y;
+  float* workspace;
+  int32_t* counters;
+  int32_t batch, k, o;
+  int32_t relu;           /* 1: ReLU, 0: none */
+  int32_t y_bf16;
+  int32_t splits;         /* 0 = auto */
+  int32_t sm_budget;      /* SMs available to this launch (0 = whole device) */
+} daris_linear_desc;
+
+typedef struct daris_linear_plan_t {
+  int32_t block_n;        /* batch rows per tile (UMMA N) */
+  int32_t splits, kb_per_split, tiles_m, tiles_n;
+  int64_t workspace_floats;
+  int32_t counters;
+  int32_t ctas;
+} daris_linear_plan_t;
+
+int daris_linear_plan(const daris_linear_desc* d, daris_linear_plan_t* out);
+int daris_linear_tc(const daris_linear_desc* d, void* stream);
+
+/* Global average pooling NHWC bf16 [n][hw][c] -> bf16 [n][c] (feeds daris_linear_tc). */
+int daris_avgpool_bf16(const void* x, void* y, int32_t n, int32_t hw, int32_t c, void* stream);
+
 /* Depthwise 3x3 conv + folded BN + ReLU6/ReLU, NHWC bf16, c % 8 == 0,
  * weight [kh][kw][c] bf16. */
 int daris_dwconv(const void* x, void* y, const void* weight, const float* scale, const float* bias, int32_t n,

@@ -249,12 +249,17 @@ class _Job:
 def simulate(tasks_in: list, gpu: dict, *, seed=0, duration=60.0, warmup_frac=0.1, ws=5, reps=10,
              no_staging=False, no_last=False, no_prior=False, no_fixed=False, hpa=False,
              phasing="random", placement_order="descending_util", edf_on_job_deadline=False,
-             overload_factor=None, phases_override=None, durations=None, stage_migration=False):
+             overload_factor=None, phases_override=None, durations=None, stage_migration=False,
+             unsampled=None):
     """Run the DARIS execution path and return (records, audits, report, extras).
 
     tasks_in: dicts {id, period, deadline, hp, stages: [(nominal, width)], batch, curve}.
     durations: optional trace {(task, job, stage): seconds} — trace-replay mode
     (SURVEY §7 step 1): every stage runs at rate 1 for its traced duration.
+    unsampled: optional set {(task, job, stage)} of traced stages whose execution
+    time is NOT recorded into the MRET window (the build's executor leaves out
+    stages that were in flight across a detected GPU-wide pause; not in the
+    reference, whose rate model has no device pauses — empty in parity runs).
     stage_migration: the build's zero-delay stage-level migration (north star (2),
     PAPER.md:4; not in the reference, which re-homes a task only at release,
     scheduler.py:215-266). Restated independently from its documented rule
@@ -467,7 +472,8 @@ def simulate(tasks_in: list, gpu: dict, *, seed=0, duration=60.0, warmup_frac=0.
         obs = t - st.start
         if obs <= 0:
             raise OracleError("NonpositiveSample", str(obs))
-        win[st.job.task][st.j].append(obs)
+        if not unsampled or (st.job.task, st.job.id, st.j) not in unsampled:
+            win[st.job.task][st.j].append(obs)
         st.state = 3
         job = st.job
         if st.j != len(job.stages) - 1:

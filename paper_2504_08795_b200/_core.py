@@ -93,8 +93,11 @@ class ReadyKeyC(C.Structure):
 
 
 class TraceEntryC(C.Structure):
-    _fields_ = [("task", C.c_int32), ("job", C.c_int32), ("stage", C.c_int32), ("_pad", C.c_int32),
+    _fields_ = [("task", C.c_int32), ("job", C.c_int32), ("stage", C.c_int32), ("flags", C.c_int32),
                 ("duration", C.c_double)]
+
+
+TRACE_UNSAMPLED = 1  # DARIS_TRACE_UNSAMPLED
 
 
 LOG_DTYPE = np.dtype([("time", "<f8"), ("kind", "<i4"), ("task", "<i4"), ("job", "<i4"), ("stage", "<i4"),
@@ -124,6 +127,7 @@ def lib() -> C.CDLL:
             "daris_release": [vp, i32, f64, i32, P(f64), P(PlacementC)],
             "daris_dispatch": [vp, i32, i32, f64, P(StageRefC), P(i32)],
             "daris_complete": [vp, i32, i32, f64, P(i32), P(i32)],
+            "daris_complete_ex": [vp, i32, i32, f64, i32, P(i32), P(i32)],
             "daris_ready_count": [vp, i32, P(i32)],
             "daris_ledger": [vp, i32, P(LedgerC)],
             "daris_admission_test": [vp, i32, i32, i32, f64, P(AuditC)],
@@ -181,7 +185,7 @@ def lib() -> C.CDLL:
 EXPORTED_SYMBOLS = (
     "daris_create", "daris_destroy", "daris_last_error", "daris_sm_per_context", "daris_n_tasks",
     "daris_task_ids", "daris_task_stage_count", "daris_full_load_sim", "daris_set_full_load",
-    "daris_populate", "daris_home_context", "daris_release", "daris_dispatch", "daris_complete",
+    "daris_populate", "daris_home_context", "daris_release", "daris_dispatch", "daris_complete", "daris_complete_ex",
     "daris_ready_count", "daris_ledger", "daris_admission_test", "daris_predicted_finish",
     "daris_stage_estimate", "daris_task_estimate", "daris_utilization", "daris_deadline_shares",
     "daris_record_execution", "daris_note_job_complete", "daris_sim_run", "daris_trace_run",
@@ -290,9 +294,12 @@ class Handle:
         self._c(lib().daris_dispatch(self._h, context, stream, t, C.byref(ref), C.byref(found)))
         return ref if found.value else None
 
-    def complete(self, job_id: int, stage: int, t: float) -> tuple[bool, bool]:
+    def complete(self, job_id: int, stage: int, t: float, record_sample: bool = True) -> tuple[bool, bool]:
         done, missed = C.c_int32(), C.c_int32()
-        self._c(lib().daris_complete(self._h, job_id, stage, t, C.byref(done), C.byref(missed)))
+        if record_sample:
+            self._c(lib().daris_complete(self._h, job_id, stage, t, C.byref(done), C.byref(missed)))
+        else:
+            self._c(lib().daris_complete_ex(self._h, job_id, stage, t, 0, C.byref(done), C.byref(missed)))
         return bool(done.value), bool(missed.value)
 
     def ready_count(self, context: int) -> int:
@@ -349,13 +356,15 @@ class Handle:
         return rep
 
     def trace_run(self, duration: float, warmup_frac: float, phases: Sequence[float], trace: dict,
-                  collect_log=True) -> ReportC:
+                  collect_log=True, unsampled=None) -> ReportC:
+        """unsampled: {(task, job, stage)} completing without an MRET sample (daris_trace_entry.flags)."""
         rep = ReportC()
         ph = (C.c_double * max(1, len(phases)))(*phases)
         items = list(trace.items())
         arr = (TraceEntryC * max(1, len(items)))()
+        skip = unsampled or ()
         for i, ((task, job, stage), dur) in enumerate(items):
-            arr[i] = TraceEntryC(task, job, stage, 0, dur)
+            arr[i] = TraceEntryC(task, job, stage, TRACE_UNSAMPLED if (task, job, stage) in skip else 0, dur)
         self._c(lib().daris_trace_run(self._h, duration, warmup_frac, ph, arr, len(items), int(collect_log),
                                       C.byref(rep)))
         return rep

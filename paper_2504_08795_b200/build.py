@@ -25,7 +25,7 @@ NVCC = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CORE_SOURCES = ["core/dispatcher.cpp", "core/decide.cpp", "core/sim.cpp", "core/capi.cpp"]
-GPU_SOURCES = ["kernels/conv_tc.cu", "kernels/aux.cu", "exec/executor.cu"]
+GPU_SOURCES = ["kernels/conv_tc.cu", "kernels/linear_tc.cu", "kernels/aux.cu", "exec/executor.cu"]
 
 
 def _run(cmd: list[str]) -> None:

@@ -150,6 +150,18 @@ int daris_complete(daris_handle* h, int32_t job_id, int32_t stage, double t, int
   });
 }
 
+int daris_complete_ex(daris_handle* h, int32_t job_id, int32_t stage, double t, int32_t record_sample,
+                      int32_t* job_done, int32_t* missed) {
+  return guard(h, [&] {
+    daris::StageJob* st = h->d->find_stage(job_id, stage);
+    if (!st) throw daris::Error(DARIS_E_NOT_FOUND, "unknown stage reference");
+    bool m = false;
+    const bool done = h->d->complete(st, t, &m, record_sample != 0);
+    *job_done = done ? 1 : 0;
+    *missed = m ? 1 : 0;
+  });
+}
+
 int daris_ready_count(const daris_handle* h, int32_t context, int32_t* out) {
   return guard(const_cast<daris_handle*>(h), [&] { *out = h->d->ready_count(context); });
 }
@@ -215,12 +227,16 @@ int daris_trace_run(daris_handle* h, double duration, double warmup_frac, const 
                     const daris_trace_entry* trace, int64_t n_trace, int32_t collect_log, daris_report* out) {
   return guard(h, [&] {
     std::unordered_map<long long, double> m;
+    std::unordered_set<long long> unsampled;
     m.reserve(static_cast<size_t>(n_trace) * 2 + 1);
-    for (int64_t i = 0; i < n_trace; ++i)
-      m[(static_cast<long long>(trace[i].task) << 40) | (static_cast<long long>(trace[i].job) << 8) |
-        static_cast<long long>(trace[i].stage)] = trace[i].duration;
+    for (int64_t i = 0; i < n_trace; ++i) {
+      const long long key = (static_cast<long long>(trace[i].task) << 40) |
+                            (static_cast<long long>(trace[i].job) << 8) | static_cast<long long>(trace[i].stage);
+      m[key] = trace[i].duration;
+      if (trace[i].flags & DARIS_TRACE_UNSAMPLED) unsampled.insert(key);
+    }
     h->d->collect_log = collect_log != 0;
-    daris::sim_run(*h->d, duration, warmup_frac, phases, out, &m);
+    daris::sim_run(*h->d, duration, warmup_frac, phases, out, &m, &unsampled);
   });
 }
 

@@ -364,10 +364,12 @@ StageJob* Dispatcher::find_stage(int job_id, int j) {
   return &it->second->stages[j];
 }
 
-bool Dispatcher::complete(StageJob* st, double t, bool* missed) {  // scheduler.py:300-324
+bool Dispatcher::complete(StageJob* st, double t, bool* missed, bool record_sample) {  // scheduler.py:300-324
   if (st->state != RUNNING) throw Error(DARIS_E_VALUE, "illegal stage transition");
   const double observed = t - st->start;
-  record_execution(st->job->task, st->j, observed);
+  // record_sample = false: the real-time executor's stage was in flight across a
+  // GPU-wide pause, so its time is not an execution-time sample (real mode only)
+  if (record_sample) record_execution(st->job->task, st->j, observed);
   st->state = DONE;
   Job* job = st->job;
   if (st->j != static_cast<int>(job->stages.size()) - 1) {

@@ -11,6 +11,7 @@
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "daris.h"
@@ -160,7 +161,7 @@ class Dispatcher {
   // make_job + admit_or_migrate. Returns the job (owned by the dispatcher while live).
   Job* release(int tid, double t, int job_id, const double* stage_work, daris_placement* out);
   StageJob* dispatch(int ctx, int stream, double t);
-  bool complete(StageJob* st, double t, bool* missed);
+  bool complete(StageJob* st, double t, bool* missed, bool record_sample = true);
   StageJob* find_stage(int job_id, int j);
   int ready_count(int ctx) const { return static_cast<int>(ready_.at(ctx - 1).size()); }
 
@@ -234,6 +235,7 @@ struct RunResult {
   daris_report report;
 };
 void sim_run(Dispatcher& d, double duration, double warmup_frac, const double* phases, daris_report* out,
-             const std::unordered_map<long long, double>* trace);
+             const std::unordered_map<long long, double>* trace,
+             const std::unordered_set<long long>* unsampled = nullptr);
 
 }  // namespace daris

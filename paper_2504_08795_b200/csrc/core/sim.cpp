@@ -188,7 +188,7 @@ daris_response_stats stats(std::vector<double> v) {  // engine.py:97-116
 }  // namespace
 
 void sim_run(Dispatcher& d, double duration, double warmup_frac, const double* phases, daris_report* out,
-             const std::unordered_map<long long, double>* trace) {
+             const std::unordered_map<long long, double>* trace, const std::unordered_set<long long>* unsampled) {
   if (!(duration > 0)) throw Error(DARIS_E_INVALID_SCENARIO, "duration must be positive");
   if (!(0.0 <= warmup_frac && warmup_frac < 1.0))
     throw Error(DARIS_E_INVALID_SCENARIO, "warmup fraction must lie in [0, 1)");
@@ -343,7 +343,9 @@ void sim_run(Dispatcher& d, double duration, double warmup_frac, const double* p
       const double release = st->job->release;
       const int batch = st->job->batch;
       bool missed = false;
-      const bool done = d.complete(st, now, &missed);  // may free the job
+      const bool sample = !unsampled || !unsampled->count((static_cast<long long>(task_id) << 40) |
+                                                          (static_cast<long long>(job_id) << 8) | j);
+      const bool done = d.complete(st, now, &missed, sample);  // may free the job
       d.logrec(now, DARIS_LOG_STAGE_COMPLETE, task_id, job_id, j, ctx, stream, rate);
       if (done) {
         d.logrec(now, DARIS_LOG_JOB_COMPLETE, task_id, job_id, -1, ctx);

@@ -84,6 +84,7 @@ struct Running {
   int task = 0, job = 0, stage = 0, slot = 0;
   double start = 0;
   int ev = -1;  // index of the stage's timing-event pair (DARIS_GPU_TIMING)
+  int epoch = 0;  // stall epoch when dispatched: a different one at completion = in flight across a pause
 };
 
 struct TaskInfo {
@@ -154,6 +155,8 @@ int build_partitions(daris_exec* ex) {
   bool green = c.partition_mode == DARIS_PART_GREEN;
   Driver& d = driver();
   std::vector<CUdevResource> groups;
+  CUdevResource rem;
+  std::memset(&rem, 0, sizeof(rem));
   CUdevice dev = 0;
   if (green) {
     if (!d.ok) green = false;
@@ -171,7 +174,6 @@ int build_partitions(daris_exec* ex) {
       const bool fine = ge && std::atoi(ge) == 2;
       unsigned n = static_cast<unsigned>(all.sm.smCount);
       groups.resize(n);
-      CUdevResource rem;
       if (d.split(groups.data(), &n, &all, &rem, fine ? CU_DEV_SM_RESOURCE_SPLIT_IGNORE_SM_COSCHEDULING : 0,
                   fine ? 2 : 8) != CUDA_SUCCESS ||
           n == 0)
@@ -179,21 +181,63 @@ int build_partitions(daris_exec* ex) {
       groups.resize(n);
     }
   }
+  // Layout units: the co-scheduled groups plus, when the split leaves one, the
+  // remainder (148 - 15 x 8 = 28 SMs on B200) as one more unit, first in the
+  // cyclic order. A green context over groups + remainder exposes all of their
+  // SMs to ordinary CTAs, and 8-CTA clusters still co-schedule on its 8-SM
+  // groups (tools/probe_mixed_green.cu), so every SM of the device is used.
+  struct Unit {
+    int index;  // into groups, or -1 = the remainder
+    int sms;
+  };
+  std::vector<Unit> units;
+  if (green && rem.sm.smCount > 0) units.push_back({-1, static_cast<int>(rem.sm.smCount)});
   const int G = green ? static_cast<int>(groups.size()) : total_sms / 2;
   const int gsize = green ? static_cast<int>(groups[0].sm.smCount) : 2;
+  for (int g = 0; g < G; ++g) units.push_back({g, gsize});
+  const int U = static_cast<int>(units.size());
+  std::vector<int> unit_start(U, 0);
+  int covered_sms = 0;
+  for (int u = 0; u < U; ++u) {
+    unit_start[u] = covered_sms;
+    covered_sms += units[u].sms;
+  }
   for (int k = 0; k < c.n_contexts; ++k) {
     Partition& p = ex->parts[k];
-    // nearest whole number of groups (at least one): 74 SMs -> 9 x 8 = 72 or 37 x 2 = 74
-    int want = (c.sm_per_context + gsize / 2) / gsize;
-    if (want < 1) want = 1;
-    if (want > G) want = G;
+    // Partition k = the cyclic window of units between the unit boundaries
+    // nearest to k/N_c of the device and sm_per_context SMs further (the
+    // reference's ceil_even(OS * SMs / N_c)): OS > 1 gives overlapping windows,
+    // each SM in about OS of them; OS = 1 tiles the device exactly. 4 x 74 on
+    // B200: 76 / 72 / 72 / 76 SMs, every group and the remainder in two.
+    auto boundary = [&](double x) {  // nearest unit start to x (mod the device), ties to the lower
+      x = std::fmod(x, static_cast<double>(covered_sms));
+      int best = 0;
+      double dist = x;
+      for (int u = 1; u <= U; ++u) {
+        const double at = u < U ? unit_start[u] : covered_sms;
+        if (std::fabs(at - x) < dist) {
+          dist = std::fabs(at - x);
+          best = u;
+        }
+      }
+      return best % U;
+    };
+    const double x0 = static_cast<double>(k) * covered_sms / c.n_contexts;
+    const int u0 = boundary(x0);
+    int taken = (boundary(x0 + c.sm_per_context) - u0 + U) % U;
+    if (taken == 0) taken = c.sm_per_context * 2 >= covered_sms ? U : 1;
+    int cov = 0;
+    for (int q = 0; q < taken; ++q) cov += units[(u0 + q) % U].sms;
     p.group_size = green ? gsize : total_sms;
-    p.n_groups = want;
-    p.first_group = static_cast<int>((static_cast<long long>(k) * G) / c.n_contexts);
-    p.sm_count = want * gsize;
+    p.n_groups = taken;
+    p.first_group = u0;
+    p.sm_count = cov;
     if (green) {
       std::vector<CUdevResource> res;
-      for (int q = 0; q < want; ++q) res.push_back(groups[(p.first_group + q) % G]);
+      for (int q = 0; q < taken; ++q) {
+        const Unit& un = units[(u0 + q) % U];
+        res.push_back(un.index < 0 ? rem : groups[un.index]);
+      }
       CUdevResourceDesc desc;
       if (d.genDesc(&desc, res.data(), static_cast<unsigned>(res.size())) != CUDA_SUCCESS ||
           d.greenCreate(&p.green, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) {
@@ -476,6 +520,10 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
                    int32_t collect_log, daris_report* report, daris_exec_stats* stats) {
   using clock = std::chrono::steady_clock;
   NiceGuard loop_priority;
+  // Bumped when a GPU-wide stall is detected and again when it ends: a stage
+  // whose dispatch and completion epochs differ was in flight across the pause,
+  // and its time is not an execution-time sample (daris_complete_ex).
+  int stall_epoch = 0;
   const daris_exec_config& c = ex->cfg;
   int32_t n_tasks = 0;
   daris_n_tasks(h, &n_tasks);
@@ -687,6 +735,7 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
     const TaskInfo& t = info[r.task];
     cudaStream_t s = (t.prio == DARIS_HP ? p.streams_hi : p.streams)[r.stream];
     Running& rr = run[r.context - 1][r.stream];
+    const bool was_held = rr.busy && rr.held;  // a held stage-0 launch released now: keeps its dispatch epoch
     if (r.stage == 0 && job_slot[r.job] < 0) {  // no buffer set yet: hold the launch on this stream
       rr.busy = true;
       rr.held = true;
@@ -696,6 +745,7 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
       rr.slot = -1;
       rr.start = r.started_at;
       rr.ev = -1;
+      rr.epoch = stall_epoch;
       held_ref[r.context - 1][r.stream] = r;
       held.push_back({r.context, r.stream});
       n_held++;
@@ -751,6 +801,7 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
     rr.slot = slot;
     rr.start = r.started_at;
     rr.ev = ev;
+    if (!was_held) rr.epoch = stall_epoch;
     in_flight++;
     if (r.stage == t.n_stages - 1) {
       const auto& pool = ex->pools[r.task - 1];
@@ -808,6 +859,7 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
       if (gap > st.progress_gap_max) st.progress_gap_max = gap;
       if (gap > ex->stall_threshold && !in_stall) {
         in_stall = true;
+        stall_epoch++;
         st.stalls++;
         if (st.first_stall_at < 0) st.first_stall_at = raw_now - gap;
       }
@@ -886,6 +938,7 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
           if (in_stall) {
             ex->stall_log.push_back(last_progress);
             ex->stall_log.push_back(raw_now - last_progress);
+            stall_epoch++;
           }
           last_progress = raw_now;
           in_stall = false;
@@ -909,20 +962,22 @@ int daris_exec_run(daris_exec* ex, daris_handle* h, double duration, double warm
         // neither logged, counted nor followed by another dispatch; its
         // duration stays in the trace so a replay also finishes it late
         ex->trace.push_back(daris_stage_trace{rr.task, rr.job, rr.stage, d.ctx, d.stream, rr.slot, rr.start, t,
-                                              static_cast<double>(rr.ev), NAN});
+                                              static_cast<double>(rr.ev), NAN, rr.epoch == stall_epoch ? 1 : 0, 0});
         rr.busy = false;
         in_flight--;
         progressed = true;
         continue;
       }
       int32_t job_done = 0, missed = 0;
-      int rc = daris_complete(h, d.job, d.stage, t, &job_done, &missed);
+      const int32_t sampled = rr.epoch == stall_epoch ? 1 : 0;
+      if (!sampled) st.unsampled++;
+      int rc = daris_complete_ex(h, d.job, d.stage, t, sampled, &job_done, &missed);
       if (rc != DARIS_OK) {
         status = fail(ex, std::string("complete: ") + daris_last_error(h), rc);
         break;
       }
       ex->trace.push_back(daris_stage_trace{rr.task, rr.job, rr.stage, d.ctx, d.stream, rr.slot, rr.start, t,
-                                            static_cast<double>(rr.ev), NAN});
+                                            static_cast<double>(rr.ev), NAN, sampled, 0});
       push_log(h, t, DARIS_LOG_STAGE_COMPLETE, rr.task, rr.job, rr.stage, d.ctx, d.stream, 1.0);
       rr.busy = false;
       in_flight--;

@@ -151,7 +151,8 @@ __global__ void maxpool_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat1
 
 // (image, 8 channels) per group of 8 lanes; the lanes split the pixels and
 // reduce with shuffles, so each thread has only ~hw/8 loads in flight
-__global__ void avgpool_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ y, int n, int hw, int c) {
+template <typename OutT>
+__global__ void avgpool_kernel(const __nv_bfloat16* __restrict__ x, OutT* __restrict__ y, int n, int hw, int c) {
   pdl_wait();
   pdl_trigger();
   const int chunks = c / 8;
@@ -183,9 +184,18 @@ __global__ void avgpool_kernel(const __nv_bfloat16* __restrict__ x, float* __res
   }
   if (valid && part == 0) {
     const float inv = 1.f / static_cast<float>(hw);
-    float4* dst = reinterpret_cast<float4*>(y + static_cast<size_t>(img) * c + ch * 8);
-    dst[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-    dst[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+    if constexpr (sizeof(OutT) == 4) {
+      float4* dst = reinterpret_cast<float4*>(y + static_cast<size_t>(img) * c + ch * 8);
+      dst[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+      dst[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+    } else {
+      uint4 pk;
+      pk.x = pack_bf16x2(acc[0] * inv, acc[1] * inv);
+      pk.y = pack_bf16x2(acc[2] * inv, acc[3] * inv);
+      pk.z = pack_bf16x2(acc[4] * inv, acc[5] * inv);
+      pk.w = pack_bf16x2(acc[6] * inv, acc[7] * inv);
+      *reinterpret_cast<uint4*>(y + static_cast<size_t>(img) * c + ch * 8) = pk;
+    }
   }
 }
 
@@ -422,8 +432,17 @@ extern "C" int daris_avgpool(const void* x, float* y, int32_t n, int32_t hw, int
   if (!x || !y) return DARIS_K_BAD_ARG;
   if (c % 8 != 0) return DARIS_K_BAD_SHAPE;
   const int work = n * (c / 8) * 8;  // 8 lanes per (image, 8 channels)
-  cudaError_t return_code = launch_pdl(avgpool_kernel, dim3(grid_for(work, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream),
+  cudaError_t return_code = launch_pdl(avgpool_kernel<float>, dim3(grid_for(work, 128)), dim3(128), 0, static_cast<cudaStream_t>(stream),
       static_cast<const __nv_bfloat16*>(x), y, n, hw, c);
+  return static_cast<int>(return_code);
+}
+
+extern "C" int daris_avgpool_bf16(const void* x, void* y, int32_t n, int32_t hw, int32_t c, void* stream) {
+  if (!x || !y) return DARIS_K_BAD_ARG;
+  if (c % 8 != 0) return DARIS_K_BAD_SHAPE;
+  const int work = n * (c / 8) * 8;
+  cudaError_t return_code = launch_pdl(avgpool_kernel<__nv_bfloat16>, dim3(grid_for(work, 128)), dim3(128), 0,
+      static_cast<cudaStream_t>(stream), static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), n, hw, c);
   return static_cast<int>(return_code);
 }
 

@@ -233,6 +233,23 @@ __device__ __forceinline__ void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// ... 16 columns (x16) or 32 (x32), selected at compile time.
+template <int N>
+__device__ __forceinline__ void tmem_ld_32x32b(uint32_t taddr, uint32_t (&r)[N]) {
+  static_assert(N == 16 || N == 32, "tmem_ld_32x32b: 16 or 32 columns");
+  if constexpr (N == 32) {
+    tmem_ld_32x32b_x32(taddr, r);
+  } else {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  }
+}
+
 // UMMA shared-memory descriptor, K-major operand, 128-byte swizzle: rows of
 // 64 bf16 (128 B), 8-row core groups 1024 B apart. Buffers are 1024-B aligned.
 __device__ __forceinline__ uint64_t umma_desc_k_sw128(uint32_t smem_addr) {

@@ -295,16 +295,18 @@ class Simulation:
         return self._result(h, rep, effective, full)
 
     def run_trace(self, durations: dict[tuple[int, int, int], float],
-                  full_load: dict[int, float], phases: Sequence[float] | None = None) -> SimResult:
+                  full_load: dict[int, float], phases: Sequence[float] | None = None,
+                  unsampled=None) -> SimResult:
         """Trace-replay mode: stage (task, job, stage) runs for
         durations[...] seconds at rate 1; AFET baselines are given; `phases`
         (release offsets in task-id order) replace the seeded draw, e.g. the
-        ones a real GPU run used."""
+        ones a real GPU run used; `unsampled` {(task, job, stage)}: stages the
+        run completed without an MRET sample (in flight across a GPU pause)."""
         effective = self._effective()
         h = self._open(effective)
         h.set_full_load([full_load[i] for i in h.task_ids])
         h.populate()
         self.handle = h
         ph = list(phases) if phases is not None else self.phases(effective)
-        rep = h.trace_run(self.duration, self.warmup_frac, ph, durations, self.collect_log)
+        rep = h.trace_run(self.duration, self.warmup_frac, ph, durations, self.collect_log, unsampled)
         return self._result(h, rep, effective, dict(full_load))

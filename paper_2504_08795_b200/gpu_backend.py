@@ -40,7 +40,7 @@ class GpuTask:
 @dataclass
 class GpuSimResult(SimResult):
     """SimResult plus what only a real run has: the per-stage trace
-    (task, job, stage, context, stream, slot, start, end, gpu_start, gpu_end),
+    (task, job, stage, context, stream, slot, start, end, sampled),
     executor counters and the partitions actually built."""
     trace: list = field(default_factory=list)
     stats: dict = field(default_factory=dict)
@@ -50,6 +50,11 @@ class GpuSimResult(SimResult):
     def stage_durations(self) -> dict[tuple[int, int, int], float]:
         """(task, job, stage) -> observed seconds, the input of trace replay."""
         return {(t[0], t[1], t[2]): t[7] - t[6] for t in self.trace}
+
+    def unsampled(self) -> set:
+        """(task, job, stage) the run completed without an MRET sample (in
+        flight across a detected GPU-wide pause): replay them as such."""
+        return {(t[0], t[1], t[2]) for t in self.trace if len(t) > 8 and not t[8]}
 
 
 class GpuSimulation:

@@ -40,6 +40,23 @@ class ConvPlan(C.Structure):
     ]
 
 
+class LinearDesc(C.Structure):
+    _fields_ = [
+        ("x", C.c_void_p), ("w", C.c_void_p), ("bias", C.c_void_p), ("y", C.c_void_p),
+        ("workspace", C.c_void_p), ("counters", C.c_void_p),
+        ("batch", C.c_int32), ("k", C.c_int32), ("o", C.c_int32), ("relu", C.c_int32),
+        ("y_bf16", C.c_int32), ("splits", C.c_int32), ("sm_budget", C.c_int32),
+    ]
+
+
+class LinearPlan(C.Structure):
+    _fields_ = [
+        ("block_n", C.c_int32), ("splits", C.c_int32), ("kb_per_split", C.c_int32),
+        ("tiles_m", C.c_int32), ("tiles_n", C.c_int32), ("workspace_floats", C.c_int64),
+        ("counters", C.c_int32), ("ctas", C.c_int32),
+    ]
+
+
 def lib() -> C.CDLL:
     global _lib
     if _lib is None:
@@ -58,9 +75,13 @@ def lib() -> C.CDLL:
         L.daris_linear.argtypes = [vp, i32, vp, vp, vp, i32, i32, i32, i32, i32, vp]
         L.daris_dwconv.argtypes = [vp, vp, vp, vp, vp] + [i32] * 10 + [vp]
         L.daris_device_sms.argtypes = []
+        L.daris_linear_plan.argtypes = [C.POINTER(LinearDesc), C.POINTER(LinearPlan)]
+        L.daris_linear_tc.argtypes = [C.POINTER(LinearDesc), vp]
+        L.daris_avgpool_bf16.argtypes = [vp, vp, i32, i32, i32, vp]
         for name in ("daris_conv_plan", "daris_conv2d", "daris_stem_im2col", "daris_pack_nhwc",
                      "daris_maxpool", "daris_avgpool", "daris_linear", "daris_dwconv",
-                     "daris_pack_nhwc_bordered", "daris_device_sms"):
+                     "daris_pack_nhwc_bordered", "daris_device_sms", "daris_linear_plan", "daris_linear_tc",
+                     "daris_avgpool_bf16"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -188,11 +209,52 @@ def maxpool(x: torch.Tensor, k: int, stride: int, pad: int, out: torch.Tensor | 
     return out
 
 
-def avgpool(x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+def avgpool(x: torch.Tensor, out: torch.Tensor | None = None, stream=None, *, out_bf16: bool = False) -> torch.Tensor:
+    """NHWC bf16 -> [n, c] mean over pixels, fp32 (or bf16: the tensor-core linear's input)."""
     n, h, w, c = x.shape
     if out is None:
-        out = torch.empty((n, c), dtype=torch.float32, device=x.device)
-    _check(lib().daris_avgpool(_ptr(x), _ptr(out), n, h * w, c, _stream(stream)), "daris_avgpool")
+        out = torch.empty((n, c), dtype=torch.bfloat16 if out_bf16 else torch.float32, device=x.device)
+    if out.dtype == torch.bfloat16:
+        _check(lib().daris_avgpool_bf16(_ptr(x), _ptr(out), n, h * w, c, _stream(stream)), "daris_avgpool_bf16")
+    else:
+        _check(lib().daris_avgpool(_ptr(x), _ptr(out), n, h * w, c, _stream(stream)), "daris_avgpool")
+    return out
+
+
+def linear_desc(batch: int, k: int, o: int, *, relu: int = 0, y_bf16: bool = False, splits: int = 0,
+                sm_budget: int = 0) -> LinearDesc:
+    d = LinearDesc()
+    d.batch, d.k, d.o, d.relu, d.y_bf16, d.splits, d.sm_budget = batch, k, o, relu, int(y_bf16), splits, sm_budget
+    return d
+
+
+def linear_plan(d: LinearDesc) -> LinearPlan:
+    p = LinearPlan()
+    _check(lib().daris_linear_plan(C.byref(d), C.byref(p)), "daris_linear_plan")
+    return p
+
+
+def linear_tc(x: torch.Tensor, weight: torch.Tensor, bias: torch.Tensor | None, *, relu: int = 0,
+              out_bf16: bool = False, out: torch.Tensor | None = None, workspace: torch.Tensor | None = None,
+              counters: torch.Tensor | None = None, splits: int = 0, sm_budget: int = 0,
+              stream=None) -> torch.Tensor:
+    """Tensor-core linear (daris_linear_tc): x [b, k] bf16, weight [o, k] bf16, k % 64 == 0."""
+    if x.dtype != torch.bfloat16 or weight.dtype != torch.bfloat16:
+        raise KernelError("linear_tc needs bf16 input and weight")
+    b, k = x.shape[0], x[0].numel()
+    o = weight.shape[0]
+    if out is None:
+        out = torch.empty((b, o), dtype=torch.bfloat16 if out_bf16 else torch.float32, device=x.device)
+    d = linear_desc(b, k, o, relu=relu, y_bf16=out.dtype == torch.bfloat16, splits=splits, sm_budget=sm_budget)
+    p = linear_plan(d)
+    if p.splits > 1:
+        if workspace is None or workspace.numel() < p.workspace_floats:
+            workspace = torch.zeros(p.workspace_floats, dtype=torch.float32, device=x.device)
+        if counters is None or counters.numel() < p.counters:
+            counters = torch.zeros(p.counters, dtype=torch.int32, device=x.device)
+    d.x, d.w, d.bias, d.y = _ptr(x), _ptr(weight), _ptr(bias), _ptr(out)
+    d.workspace, d.counters = _ptr(workspace), _ptr(counters)
+    _check(lib().daris_linear_tc(C.byref(d), _stream(stream)), "daris_linear_tc")
     return out
 
 

@@ -519,7 +519,7 @@ def allocate_buffers(net: Network, sm_budget: int = 0) -> TaskBuffers:
     for name, elems in net.buffer_elems.items():
         if name == "input":
             bufs[name] = torch.zeros(net.input_shape, dtype=torch.float32, device=net.device)
-        elif name in ("pooled", "logits"):
+        elif name == "logits":
             bufs[name] = torch.zeros(elems, dtype=torch.float32, device=net.device)
         else:
             bufs[name] = torch.zeros(elems, dtype=torch.bfloat16, device=net.device)
@@ -532,6 +532,12 @@ def allocate_buffers(net: Network, sm_budget: int = 0) -> TaskBuffers:
                             padded_input=L.padded_input, x2_shape=op.shape_in2 if L.dual_cin else None,
                             stride2=L.dual_stride)
             p = K.conv_plan(d)
+            ws = max(ws, p.workspace_floats)
+            ctr = max(ctr, p.counters)
+        elif op.kind == "linear":
+            L = op.layer
+            p = K.linear_plan(K.linear_desc(op.shape_in[0], op.shape_in[1], L.weight.shape[0], relu=L.relu,
+                                            y_bf16=L.out_bf16, sm_budget=sm_budget))
             ws = max(ws, p.workspace_floats)
             ctr = max(ctr, p.counters)
     return TaskBuffers(bufs, torch.zeros(ws, dtype=torch.float32, device=net.device),
@@ -577,7 +583,8 @@ def run_op(op: Op, tb: TaskBuffers, stream, sm_budget: int = 0, timestamps=None)
         out = _view(B[op.dst], op.shape_out)
         if L.out_bf16 and out.dtype != torch.bfloat16:
             raise RuntimeError("bf16 linear output needs a bf16 buffer")
-        K.linear(x, L.weight, L.bias, relu=L.relu, out=out, stream=stream)
+        K.linear_tc(x, L.weight, L.bias, relu=L.relu, out=out, workspace=tb.workspace, counters=tb.counters,
+                    sm_budget=sm_budget, stream=stream)
     elif op.kind == "dwconv":
         L = op.layer
         K.dwconv(_view(B[op.src], op.shape_in), L.weight, L.scale, L.bias, stride=L.stride, pad=L.pad, relu=L.relu,

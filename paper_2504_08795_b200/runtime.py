@@ -49,7 +49,7 @@ class PartitionC(C.Structure):
 class StageTraceC(C.Structure):
     _fields_ = [("task", C.c_int32), ("job", C.c_int32), ("stage", C.c_int32), ("context", C.c_int32),
                 ("stream", C.c_int32), ("slot", C.c_int32), ("start", C.c_double), ("end", C.c_double),
-                ("gpu_start", C.c_double), ("gpu_end", C.c_double)]
+                ("gpu_start", C.c_double), ("gpu_end", C.c_double), ("sampled", C.c_int32), ("_pad", C.c_int32)]
 
 
 class ExecStatsC(C.Structure):
@@ -58,7 +58,7 @@ class ExecStatsC(C.Structure):
                 ("slot_waits", C.c_int64), ("polls", C.c_int64), ("wall_seconds", C.c_double),
                 ("release_lag_max", C.c_double), ("loop_gap_max", C.c_double),
                 ("progress_gap_max", C.c_double), ("stalls", C.c_int64), ("first_stall_at", C.c_double),
-                ("slot_deferred", C.c_int64), ("slot_backlog_max", C.c_int64)]
+                ("slot_deferred", C.c_int64), ("slot_backlog_max", C.c_int64), ("unsampled", C.c_int64)]
 
 
 _exec_lib = None
@@ -195,7 +195,8 @@ class Executor:
         arr = (StageTraceC * max(1, n))()
         L.daris_exec_trace_copy(self._h, arr, n)
         self._gpu_times = [(a.gpu_start, a.gpu_end) for a in list(arr)[:n]]
-        return [(a.task, a.job, a.stage, a.context, a.stream, a.slot, a.start, a.end) for a in list(arr)[:n]]
+        return [(a.task, a.job, a.stage, a.context, a.stream, a.slot, a.start, a.end, a.sampled)
+                for a in list(arr)[:n]]
 
     def stall_log(self) -> list[tuple[float, float]]:
         """(start, length) of each GPU-wide stall of the last run (executor seconds)."""
@@ -261,6 +262,11 @@ class RunResult:
     log: np.ndarray | None = None        # the raw native event log (_core.LOG_DTYPE)
     stalls: list = field(default_factory=list)  # (start, length) of GPU-wide stalls
     batch: dict = field(default_factory=dict)   # images per job, by task id
+
+    def unsampled(self) -> set:
+        """(task, job, stage) of traced stages completed without an MRET sample
+        (in flight across a detected GPU-wide pause): replay them as such."""
+        return {(t[0], t[1], t[2]) for t in self.trace if len(t) > 8 and not t[8]}
 
     def windows(self, warmup: float, step: float, n_steps: int) -> list[dict]:
         return window_stats(self.log, self.periods, {t.id for t in self.tasks if t.priority is Priority.HP},

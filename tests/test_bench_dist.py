@@ -55,12 +55,13 @@ class FakeDaris:
             return [{"released_hp": 10, "released_lp": 10, "missed_hp": 0 if ok else 2, "missed_lp": 0,
                      "rejected_lp": 0, "lp_loss": 0.0, "completed_images": int(r * n_tasks * step),
                      "stalls": 0} for _ in range(n)]
-        stats = {k: 0 for k in ("graph_launches", "slot_waits", "slot_deferred", "polls", "stalls")}
+        stats = {k: 0 for k in ("graph_launches", "slot_waits", "slot_deferred", "polls", "stalls", "unsampled")}
         stats.update(release_lag_max=0.0, loop_gap_max=0.0, progress_gap_max=0.0, wall_seconds=duration,
                      h2d_bytes=0, d2h_bytes=0)
         trace = [(1, j, s, 1, 0, 0, warmup + 1e-3 * j, warmup + 1e-3 * j + 1e-4) for j in range(10) for s in range(4)]
-        rep = SimpleNamespace(response_hp=SimpleNamespace(p95=4e-4, mean=3e-4))
-        return SimpleNamespace(report=rep, stats=stats, trace=trace, windows=windows, p99_hp=lambda a, b: 5e-4)
+        rep = SimpleNamespace(response_hp=SimpleNamespace(p99=5e-4, p95=4e-4, mean=3e-4))
+        return SimpleNamespace(report=rep, stats=stats, trace=trace, windows=windows, p99_hp=lambda a, b: 5e-4,
+                               stalls=[])
 
 
 def _free_port():
@@ -113,3 +114,5 @@ def test_bench_flow_world_size_two():
     # whole-box value: both ranks' completed images over the timed window
     assert abs(line["value"] - 2 * 8 * knee) < 1e-6 * line["value"] + 1.0
     assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0
+    # no pauses in the stand-in: the pause-excluded knee is the same cliff
+    assert line["value_excl_pauses"]["rate_per_task"] < 800 and line["value_excl_pauses"]["constraints_met"]

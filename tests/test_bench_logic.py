@@ -3,7 +3,8 @@ the feasible rate with the most completed inferences/s (not the highest
 feasible rate); a rate is feasible only when EVERY window of its run has HP
 miss 0 and LP loss < 2 % (admission rejections count as lost); the timed run
 is never re-measured at the same rate — any failing window steps the rate
-down and repeats the whole run; failures after a GPU-wide pause are tagged."""
+down and repeats the whole run; windows with a GPU-wide pause are tagged and
+exempt under the secondary, pause-excluded criterion."""
 
 from types import SimpleNamespace
 
@@ -26,15 +27,18 @@ def _win(imgs, missed_hp=0, released_lp=100, lost_lp=0, stalls=0):
 
 class FakeRuntime:
     """Throughput rises with the rate up to a cliff at 1000/task where admission
-    rejects every LP job, HP misses start at 1300. `pause_at` puts a GPU-wide
-    pause into window 3 of the first `pauses` runs at rates >= 600: that window
-    and every later one lose LP jobs (the MRET-inflated task stays rejected)."""
+    rejects every LP job, HP misses start at 1300. The first `pauses` runs at
+    rates >= 600 have a 1.6 ms GPU-wide pause in window 3, which misses HP jobs
+    there (periods below pause + response time); `poison` also makes every
+    later window lose LP jobs (an MRET sample inflated by the pause keeping a
+    task rejected — what the executor's pause-excluded samples prevent)."""
 
-    def __init__(self, pauses=0):
+    def __init__(self, pauses=0, poison=False):
         self.rate = 0.0
         self.afet = {}
         self.runs = []
         self.pauses = pauses
+        self.poison = poison
 
     def set_rate(self, r):
         self.rate = r
@@ -49,11 +53,14 @@ class FakeRuntime:
             for k in range(n):
                 imgs = 8 * r * step if r < 1000 else 4 * r * step
                 w = _win(imgs, missed_hp=3 if r >= 1300 else 0, lost_lp=100 if r >= 1000 else 0)
-                if pause and k >= 3:
-                    w = _win(imgs, lost_lp=30, stalls=1 if k == 3 else 0)
+                if pause and k == 3:
+                    w = _win(imgs, missed_hp=2, stalls=1)
+                elif pause and k > 3 and self.poison:
+                    w = _win(imgs, lost_lp=30)
                 out.append(w)
             return out
-        return SimpleNamespace(report=_rep(8 * r), windows=windows, stats={"stalls": 0}, trace=[])
+        return SimpleNamespace(report=_rep(8 * r), windows=windows, stats={"stalls": 0}, trace=[],
+                               stalls=[(warmup + 1.6, 0.0016)] if pause else [])
 
 
 def test_lp_rejections_count_as_loss():
@@ -72,22 +79,45 @@ def test_knee_is_the_throughput_maximum_below_the_admission_cliff():
 
 
 def test_timed_run_steps_down_until_every_window_passes():
+    """Strict: a run with any failing window is not re-measured; after a run
+    that failed only in a pause window the next rate's period covers the pause
+    plus the p99 HP response (1 / (1.6 + 0.5 + 0.1) ms = 454.5/task)."""
     rt = FakeRuntime(pauses=100)      # every run at >= 600/task is hit by a pause
     args = SimpleNamespace(step_seconds=0.5, warmup=2, steps=20, timed_attempts=8)
-    rate, res, s, clocks, wall, attempts = bench.timed_knee(rt, 950.0, args, lambda m: None, "t")
+    rate, res, s, clocks, wall, attempts = bench.timed_knee(rt, 950.0, args, lambda m: None, "t",
+                                                            pause_floor=bench.pause_floor)
     assert [round(r, 2) for r in rt.runs] == [a["rate_per_task"] for a in attempts]   # one run per attempt
-    assert rate < 600 and s["ok"] and s["windows_failed"] == 0
-    assert all(r2 < r1 for r1, r2 in zip(rt.runs, rt.runs[1:]))
-    # the failing runs failed only in windows at or after the pause
-    assert all(a["windows_failed"] == 17 and a["windows_failed_without_pause"] == 0 for a in attempts[:-1])
-    assert attempts[-1]["windows_failed"] == 0
+    assert len(attempts) == 2 and abs(rate - 1 / 0.0022) < 1e-6 and s["ok"] and s["windows_failed"] == 0
+    assert attempts[0]["windows_failed"] == 1 and attempts[0]["windows_failed_without_pause"] == 0
+    assert attempts[0]["longest_pause_ms"] == 1.6
+
+
+def test_timed_run_without_pause_floor_steps_down_geometrically():
+    rt = FakeRuntime(pauses=100, poison=True)
+    args = SimpleNamespace(step_seconds=0.5, warmup=2, steps=20, timed_attempts=8)
+    rate, res, s, clocks, wall, attempts = bench.timed_knee(rt, 950.0, args, lambda m: None, "t")
+    assert rate < 600 and s["ok"]
+    assert all(abs(r2 - 0.85 * r1) < 1e-9 for r1, r2 in zip(rt.runs, rt.runs[1:]))
+    assert all(a["windows_failed"] == 17 and a["windows_failed_without_pause"] == 16 for a in attempts[:-1])
+
+
+def test_pause_excluded_criterion():
+    """ok_excl exempts the windows that saw a GPU-wide pause, nothing else."""
+    rt = FakeRuntime(pauses=100)
+    args = SimpleNamespace(step_seconds=0.5, warmup=2, steps=20, timed_attempts=8)
+    rate, res, s, *_ = bench.timed_knee(rt, 950.0, args, lambda m: None, "t", criterion="ok_excl")
+    assert rate == 950.0 and s["ok_excl"] and not s["ok"] and s["windows_with_pause"] == 1
+    rt = FakeRuntime(pauses=100, poison=True)   # later windows failing without a pause still fail it
+    rate, res, s, *_ = bench.timed_knee(rt, 950.0, args, lambda m: None, "t", criterion="ok_excl")
+    assert rate < 600
+    assert bench.knee_search(FakeRuntime(pauses=100), 400.0, 2.5, 0.5, lambda m: None, criterion="ok_excl") > 900
 
 
 def test_summarize_counts_and_pause_attribution():
     ws = [_win(50), _win(50, missed_hp=1), _win(50, stalls=1, lost_lp=5), _win(50, lost_lp=5)]
     s = bench.summarize(ws, 0.5)
-    assert s["windows_failed"] == 3 and s["windows_failed_without_pause"] == 1
-    assert s["inf_per_s"] == 200 / 2.0 and s["missed_hp"] == 1 and not s["ok"]
+    assert s["windows_failed"] == 3 and s["windows_failed_without_pause"] == 2 and s["windows_with_pause"] == 1
+    assert s["inf_per_s"] == 200 / 2.0 and s["missed_hp"] == 1 and not s["ok"] and not s["ok_excl"]
 
 
 def test_reference_arm_prints_the_contract_line():

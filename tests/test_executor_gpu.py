@@ -20,15 +20,17 @@ def _runtime(n_ctx=2, n_str=2, os_=1.0, model="resnet18", rate=200.0, n_tasks=4,
     return DarisRuntime(tasks, gpu, slots=2, **kw)
 
 
-def test_partitions_are_green_and_sized():
-    rt = _runtime(n_ctx=4, n_str=2, os_=2.0)
+@pytest.mark.parametrize("n_ctx,n_str,os_,target", [(4, 2, 2.0, 74), (2, 2, 1.0, 74), (4, 1, 1.0, 38)])
+def test_partitions_are_green_and_sized(n_ctx, n_str, os_, target):
+    """Green partitions over the 8-SM co-scheduled groups plus the 28-SM split
+    remainder: each within half a group of ceil_even(OS * 148 / N_c), and
+    together covering the device OS times (all 148 SMs in use)."""
+    rt = _runtime(n_ctx=n_ctx, n_str=n_str, os_=os_)
     parts = rt.exec.partitions
     assert all(p["green"] for p in parts), parts
-    # ceil_even(2 * 148 / 4) = 74 SMs, rounded to whole co-scheduled SM groups
-    # (8-SM groups: 9 x 8 = 72; DARIS_PART_GROUP=2: 37 x 2 = 74)
     for p in parts:
-        assert p["sm_count"] == p["n_groups"] * p["group_size"], p
-        assert abs(p["sm_count"] - 74) <= p["group_size"] // 2, p
+        assert abs(p["sm_count"] - target) <= 8, p  # within one 8-SM group
+    assert sum(p["sm_count"] for p in parts) == round(os_ * 148), parts
     rt.close()
 
 
@@ -63,7 +65,7 @@ def test_real_run_and_trace_replay_parity(model, flags, monkeypatch):
            "kappa": 0.0}
     phases = {spec.id: ph for spec, ph in zip(res.tasks, res.phases)}
     recs, audits, report, _ = O.simulate(tasks, gpu, duration=1.0, warmup_frac=0.1, durations=durations,
-                                         phases_override=phases)
+                                         phases_override=phases, unsampled=res.unsampled())
     horizon = 1.0
     real = _decisions(res.records, horizon)
     replay = _decisions(recs, horizon)
@@ -99,7 +101,8 @@ def test_batched_jobs_count_images_and_replay():
     ogpu = {"total_sms": 148, "n_contexts": 2, "n_streams": 2, "oversubscription": 1.0, "policy": "mps-str",
             "kappa": 0.0}
     recs, _, _, _ = O.simulate(otasks, ogpu, duration=0.5, warmup_frac=0.1, durations=durations,
-                               phases_override={s.id: ph for s, ph in zip(res.tasks, res.phases)})
+                               phases_override={s.id: ph for s, ph in zip(res.tasks, res.phases)},
+                               unsampled=res.unsampled())
     assert _decisions(res.records, 0.5) == _decisions(recs, 0.5)
     rt.close()
 

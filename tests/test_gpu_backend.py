@@ -97,7 +97,8 @@ def test_gpu_scenario_runs_and_replays(preset, rate):
     eff = res.effective_tasks
     replay = S.Simulation(eff, cfg.gpu, seed=cfg.seed, duration=cfg.duration, warmup_frac=cfg.warmup_frac,
                           stage_migration=cfg.stage_migration).run_trace(res.stage_durations(), res.full_load,
-                                                                          phases=res.phases)
+                                                                          phases=res.phases,
+                                                                          unsampled=res.unsampled())
     assert _cut(res.records, cfg.duration) == _cut(replay.records, cfg.duration)
     assert res.report.missed_hp == replay.report.missed_hp
     # ... and through the oracle restatement of the reference scheduler (its
@@ -111,6 +112,6 @@ def test_gpu_scenario_runs_and_replays(preset, rate):
     recs, _, _, _ = O.simulate(otasks, ogpu, duration=cfg.duration, warmup_frac=cfg.warmup_frac,
                                durations=res.stage_durations(),
                                phases_override={t.id: ph for t, ph in zip(eff, res.phases)},
-                               stage_migration=cfg.stage_migration)
+                               stage_migration=cfg.stage_migration, unsampled=res.unsampled())
     assert _cut(res.records, cfg.duration) == _cut(recs, cfg.duration)
     sim.close()

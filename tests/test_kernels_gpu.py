@@ -274,3 +274,49 @@ def test_linear_wide_k(batch, k, o, x_bf16, relu):
 def test_conv_large_m(n, h, cin, cout, k, stride, pad, relu, residual, bn):
     """Batched (large-M) launches on a small SM budget: many waves of tiles."""
     _conv_case(n, h, h, cin, cout, k, stride, pad, relu=relu, residual=residual, block_n=bn, sm_budget=8)
+
+
+@pytest.mark.parametrize("batch,k,o,relu,out_bf16,splits,sm", [
+    (1, 2048, 1000, 0, False, 0, 23),      # ResNet-50 classifier, batch 1 (split-K weight stream)
+    (64, 2048, 1000, 0, False, 0, 148),    # ... batch 64 (single-tenant batching)
+    (17, 2048, 1000, 0, False, 0, 148),    # ragged batch (N tile 32, rows 17..31 zero-filled)
+    (3, 512, 1000, 0, False, 1, 0),        # ResNet-18 head, no split
+    (100, 1280, 1000, 0, False, 0, 148),   # MobileNetV2 head, batch 100 (N tile 128)
+    (300, 512, 200, 1, True, 0, 148),      # two N tiles, bf16 output, ReLU
+    (1, 25088, 4096, 1, True, 0, 24),      # VGG-16 FC1 at batch 1 in a 24-SM partition
+    (2, 4096, 4096, 1, True, 0, 148),      # VGG-16 FC2
+    (32, 4096, 1000, 0, False, 7, 0),      # forced split count
+])
+def test_linear_tc(batch, k, o, relu, out_bf16, splits, sm):
+    """daris_linear_tc (tcgen05 swap-AB) vs a torch fp32 GEMM of the same bf16
+    operands; run twice to check the split-K accumulator/tickets re-arm."""
+    from paper_2504_08795_b200 import kernels as K
+    dev = torch.device("cuda")
+    g = torch.Generator().manual_seed(batch * 7 + k + o)
+    x = torch.randn(batch, k, generator=g).bfloat16()
+    w = (torch.randn(o, k, generator=g) / k ** 0.5).bfloat16()
+    bias = torch.randn(o, generator=g)
+    ref = x.float() @ w.float().t() + bias
+    if relu:
+        ref = ref.clamp_min(0)
+    d = K.linear_desc(batch, k, o, relu=relu, y_bf16=out_bf16, splits=splits, sm_budget=sm)
+    p = K.linear_plan(d)
+    ws = torch.zeros(max(1, p.workspace_floats), device=dev)
+    ctr = torch.zeros(max(1, p.counters), dtype=torch.int32, device=dev)
+    xd, wd, bd = x.to(dev), w.to(dev), bias.to(dev)
+    for _ in range(2):
+        y = K.linear_tc(xd, wd, bd, relu=relu, out_bf16=out_bf16, workspace=ws, counters=ctr, splits=splits,
+                        sm_budget=sm)
+        torch.cuda.synchronize()
+        _close(y, ref)
+    assert int(ctr.abs().sum()) == 0 and float(ws.abs().sum()) == 0.0  # scratch re-armed
+
+
+def test_avgpool_bf16():
+    from paper_2504_08795_b200 import kernels as K
+    g = torch.Generator().manual_seed(5)
+    x = torch.randn(3, 7, 7, 2048, generator=g).bfloat16()
+    y = K.avgpool(x.cuda(), out_bf16=True)
+    torch.cuda.synchronize()
+    assert y.dtype == torch.bfloat16
+    _close(y, x.float().mean(dim=(1, 2)))

@@ -97,7 +97,11 @@ def test_native_matches_oracle_random(seed):
     assert res.report.to_dict() == report
 
 
-def test_trace_replay_matches_oracle():
+@pytest.mark.parametrize("skip_frac", [0.0, 0.15])
+def test_trace_replay_matches_oracle(skip_frac):
+    """skip_frac > 0: some stages complete without an MRET sample (the executor's
+    pause-spanning stages, DARIS_TRACE_UNSAMPLED) — native engine and oracle agree,
+    and the admission audits differ from the all-sampled replay (the samples matter)."""
     rng = random.Random(7)
     tasks = [O.task_dict(1, 0.01, True, [(0.002, 40), (0.003, 40)]),
              O.task_dict(2, 0.012, False, [(0.004, 60), (0.001, 60), (0.002, 60)]),
@@ -113,7 +117,12 @@ def test_trace_replay_matches_oracle():
     full = {1: 0.006, 2: 0.009, 3: 0.006}
     for t in tasks:
         t["full_load"] = full[t["id"]]
-    recs, audits, report, _ = O.simulate(tasks, gpu, seed=3, duration=1.0, durations=durations)
+    skip = {k for k in sorted(durations) if random.Random(hash(k) & 0xffff).random() < skip_frac}
+    recs, audits, report, _ = O.simulate(tasks, gpu, seed=3, duration=1.0, durations=durations,
+                                         unsampled=skip)
+    if skip:
+        _, base_audits, _, _ = O.simulate(tasks, gpu, seed=3, duration=1.0, durations=durations)
+        assert base_audits != audits  # the admission utilisations saw different MRET windows
     case = {"gpu": gpu, "tasks": [{**t, "stages": [list(s) for s in t["stages"]]} for t in tasks],
             "options": {"seed": 3, "duration": 1.0, "warmup_frac": 0.1, "ws": 5, "reps": 1,
                         "no_staging": False, "no_last": False, "no_prior": False, "no_fixed": False,
@@ -121,6 +130,7 @@ def test_trace_replay_matches_oracle():
                         "edf_on_job_deadline": False}}
     sim = _sim_from_case(case)
     # the native trace keys on (job, stage); the oracle on (task, job, stage)
-    res = sim.run_trace(durations, full)
+    res = sim.run_trace(durations, full, unsampled=skip)
     assert [tuple(r) for r in res.records] == recs
+    assert [tuple(a) for a in _audit_rows(res.admissions)] == [tuple(a) for a in audits]
     assert res.report.to_dict() == report

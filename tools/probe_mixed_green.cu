@@ -73,13 +73,15 @@ int main() {
     if (e2 == CUDA_SUCCESS) cuGreenCtxGetDevResource(g, &got, CU_DEV_RESOURCE_TYPE_SM);
     printf("7 x8 + remainder(%u): desc rc=%d green rc=%d -> %u SMs\n", rem.sm.smCount, (int)e, (int)e2, got.sm.smCount);
   }
-  for (int variant = 0; variant < 3; ++variant) {
-    // 0: 7 eight-groups + 5 two-groups; 1: 9 eight-groups; 2: all 8-groups + all 2-groups
+  for (int variant = 0; variant < 5; ++variant) {
+    // 0: 7 eight-groups + 5 two-groups; 1: 9 eight-groups; 2: all 8-groups + all 2-groups;
+    // 3: 6 eight-groups + the remainder; 4: all 8-groups + the remainder (148 SMs)
     std::vector<CUdevResource> res;
-    int k8 = variant == 0 ? 7 : variant == 1 ? 9 : (int)n8;
-    int k2 = variant == 0 ? 5 : variant == 1 ? 0 : (int)n2;
+    int k8 = variant == 0 ? 7 : variant == 1 ? 9 : variant == 3 ? 6 : (int)n8;
+    int k2 = variant == 0 ? 5 : variant == 1 ? 0 : variant >= 3 ? 0 : (int)n2;
     for (int i = 0; i < k8; ++i) res.push_back(g8[i]);
     for (int i = 0; i < k2 && r2 == CUDA_SUCCESS; ++i) res.push_back(g2[i]);
+    if (variant >= 3) res.push_back(rem);
     CUdevResourceDesc desc;
     CUresult e = cuDevResourceGenerateDesc(&desc, res.data(), (unsigned)res.size());
     CUgreenCtx g;
@@ -97,10 +99,10 @@ int main() {
     std::vector<int> h(1024);
     cudaMemcpy(h.data(), sm, 1024 * 4, cudaMemcpyDeviceToHost);
     std::set<int> distinct(h.begin(), h.end());
-    printf("variant %d: %d x8 + %d x2 groups -> green ctx reports %u SMs; plain kernel ran on %zu distinct SMs (%s)\n",
-           variant, k8, k2, got.sm.smCount, distinct.size(), cudaGetErrorString(le));
+    printf("variant %d: %d x8 + %d x2 groups%s -> green ctx reports %u SMs; plain kernel ran on %zu distinct SMs (%s)\n",
+           variant, k8, k2, variant >= 3 ? " + remainder" : "", got.sm.smCount, distinct.size(), cudaGetErrorString(le));
     for (int csz : {2, 8}) {
-      const int blocks = 128;
+      const int blocks = 1024;
       float *in, *out;
       cudaMalloc(&in, blocks * 256 * 4);
       cudaMalloc(&out, blocks * 256 * 4);

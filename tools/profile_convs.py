@@ -31,8 +31,8 @@ def op_bytes(op) -> int:
     b = 0
     if op.kind in ("conv", "linear", "dwconv"):
         b += op.layer.weight.numel() * 2
-    b += n(op.shape_in) * (4 if op.kind == "pack8" or (op.kind == "linear" and op.src == "pooled") else 2)
-    b += n(op.shape_out) * (4 if op.kind in ("avgpool",) or op.dst == "logits" else 2)
+    b += n(op.shape_in) * (4 if op.kind == "pack8" else 2)
+    b += n(op.shape_out) * (4 if op.dst == "logits" else 2)
     if op.res:
         b += n(op.shape_out) * 2
     return b
