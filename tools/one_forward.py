@@ -26,13 +26,14 @@ def main():
     ap.add_argument("--sms", type=int, default=74, help="partition size (rounded to whole SM groups)")
     ap.add_argument("--plan", type=int, default=23, help="SMs the layer grids are planned for")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--batch", type=int, default=1)
     args = ap.parse_args()
     ex = Executor(max(1, 148 // args.sms), 1, args.sms, slots=1, max_tasks=1, max_stages=8)
-    net = nets.build_network(args.model, batch=1)
+    net = nets.build_network(args.model, batch=args.batch)
     tb = nets.allocate_buffers(net, sm_budget=args.plan)
     sp = ex.stream(1, 0)
     s = torch.cuda.ExternalStream(sp)
-    x = torch.randn(1, 3, 224, 224, generator=torch.Generator().manual_seed(0)).cuda()
+    x = torch.randn(args.batch, 3, 224, 224, generator=torch.Generator().manual_seed(0)).cuda()
     with torch.cuda.stream(s):
         for _ in range(args.reps):
             out = nets.forward(net, tb, x, stream=sp, sm_budget=args.plan)
