@@ -66,8 +66,8 @@ __device__ __forceinline__ void red_add_f32(float* p, float v) {
   asm volatile("red.global.add.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
-__device__ __forceinline__ void lin_store(const LinArgs& a, int b, int o, float v) {
-  v += a.bias ? __ldg(a.bias + o) : 0.f;
+__device__ __forceinline__ void lin_store(const LinArgs& a, int b, int o, float v, float bias) {
+  v += bias;
   if (a.relu == 1) v = fmaxf(v, 0.f);
   const size_t i = static_cast<size_t>(b) * a.o + o;
   if (a.y_bf16)
@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
     const int orow = o0 + row;
     const bool row_ok = orow < a.o;
     const int nb_valid = min(NB, a.batch - b0);
+    const float bias_o = (a.bias && row_ok) ? __ldg(a.bias + orow) : 0.f;  // before the wait: a constant
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     if (threadIdx.x == 0) pdl_trigger();
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(kLThreads, 1)
         if (row_ok) {
 #pragma unroll
           for (int j = 0; j < kChunk; ++j)
-            if (c0 + j < nb_valid) lin_store(a, b0 + c0 + j, orow, __uint_as_float(r[j]));
+            if (c0 + j < nb_valid) lin_store(a, b0 + c0 + j, orow, __uint_as_float(r[j]), bias_o);
         }
       }
     } else {
@@ -196,11 +197,20 @@ __global__ void __launch_bounds__(kLThreads, 1)
       if (*last_flag) {
         __threadfence();
         if (row_ok) {
-          for (int j = 0; j < nb_valid; ++j) {
-            float* p = acc + j * kLM + row;
-            const float v = __ldcg(p);
-            __stcg(p, 0.f);  // re-arm for the next launch
-            lin_store(a, b0 + j, orow, v);
+          // a chunk of sums loaded together (one L2 round trip, not one per
+          // batch row: the re-arming stores would otherwise order every load
+          // behind the previous row's store), then re-armed and stored
+#pragma unroll 1
+          for (int c0 = 0; c0 < nb_valid; c0 += kChunk) {
+            float v[kChunk];
+#pragma unroll
+            for (int j = 0; j < kChunk; ++j) v[j] = c0 + j < nb_valid ? __ldcg(acc + (c0 + j) * kLM + row) : 0.f;
+#pragma unroll
+            for (int j = 0; j < kChunk; ++j)
+              if (c0 + j < nb_valid) __stcg(acc + (c0 + j) * kLM + row, 0.f);  // re-arm for the next launch
+#pragma unroll
+            for (int j = 0; j < kChunk; ++j)
+              if (c0 + j < nb_valid) lin_store(a, b0 + c0 + j, orow, v[j], bias_o);
           }
         }
         if (threadIdx.x == 0) *ticket = 0;
