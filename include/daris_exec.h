@@ -45,7 +45,8 @@ typedef struct daris_exec_partition {
                                     leaves over (28 on B200), then the co-scheduled groups */
   int32_t green;            /* 1 if a green context backs it */
   int32_t group_size;       /* SMs per co-scheduling group: the largest thread-block cluster
-                               a kernel in this partition can launch (8; 2 with DARIS_PART_GROUP=2) */
+                               a kernel in this partition can launch (8; 2 with DARIS_PART_GROUP=2;
+                               1 for a partition of only the split remainder) */
 } daris_exec_partition;
 
 /* per-stage execution record (one per completed stage) */

@@ -228,7 +228,12 @@ int build_partitions(daris_exec* ex) {
     if (taken == 0) taken = c.sm_per_context * 2 >= covered_sms ? U : 1;
     int cov = 0;
     for (int q = 0; q < taken; ++q) cov += units[(u0 + q) % U].sms;
-    p.group_size = green ? gsize : total_sms;
+    // the largest cluster its kernels may launch: a co-scheduled group's size if
+    // the partition holds one, else 1 (the remainder's SMs are scattered over
+    // GPCs, so an 8-CTA cluster may not fit: split-K then reduces through L2)
+    bool has_group = false;
+    for (int q = 0; q < taken; ++q) has_group |= units[(u0 + q) % U].index >= 0;
+    p.group_size = green ? (has_group ? gsize : 1) : total_sms;
     p.n_groups = taken;
     p.first_group = u0;
     p.sm_count = cov;

@@ -144,6 +144,11 @@ class Executor:
     def __del__(self):
         self.close()
 
+    def cluster_partition(self) -> int:
+        """1-based context of the first partition that holds a co-scheduled SM
+        group (8-CTA clusters launch there), e.g. for single-partition tools."""
+        return next((p["context"] for p in self.partitions if p["group_size"] >= 8), 1)
+
     def stream(self, context: int, stream: int) -> int:
         out = C.c_void_p()
         self._c(exec_lib().daris_exec_stream(self._h, context, stream, C.byref(out)), "daris_exec_stream")

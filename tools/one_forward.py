@@ -31,7 +31,8 @@ def main():
     ex = Executor(max(1, 148 // args.sms), 1, args.sms, slots=1, max_tasks=1, max_stages=8)
     net = nets.build_network(args.model, batch=args.batch)
     tb = nets.allocate_buffers(net, sm_budget=args.plan)
-    sp = ex.stream(1, 0)
+    ctx = ex.cluster_partition()
+    sp = ex.stream(ctx, 0)
     s = torch.cuda.ExternalStream(sp)
     x = torch.randn(args.batch, 3, 224, 224, generator=torch.Generator().manual_seed(0)).cuda()
     with torch.cuda.stream(s):

@@ -50,7 +50,8 @@ def main():
     ex = Executor(n_ctx, 1, args.sms, slots=1, max_tasks=1, max_stages=8)
     net = nets.build_network(args.model, batch=args.batch)
     tb = nets.allocate_buffers(net, sm_budget=args.sms)
-    stream_ptr = ex.stream(1, 0)
+    ctx = ex.cluster_partition()
+    stream_ptr = ex.stream(ctx, 0)
     s = torch.cuda.ExternalStream(stream_ptr)
     # warm: every op once eagerly (sets kernel attributes before capture)
     for op in net.ops:

@@ -36,9 +36,10 @@ def main():
     ex = Executor(max(1, 148 // args.sms), 1, args.sms, slots=1, max_tasks=1, max_stages=8)
     net = nets.build_network(args.model, batch=1)
     tb = nets.allocate_buffers(net, sm_budget=args.sms)
-    sp = ex.stream(1, 0)
+    ctx = ex.cluster_partition()
+    sp = ex.stream(ctx, 0)
     s = torch.cuda.ExternalStream(sp)
-    args.sms = ex.partitions[0]["sm_count"]  # the partition's actual SM count (whole 8-SM groups)
+    args.sms = ex.partitions[ctx - 1]["sm_count"]  # the partition's actual SM count (whole 8-SM groups)
     ts = {}
     for i, op in enumerate(net.ops):
         if op.kind == "conv":
