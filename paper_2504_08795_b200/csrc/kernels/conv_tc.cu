@@ -182,7 +182,6 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
   uint64_t* tmem_full = empty + kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
-  uint64_t* red_bar = tmem_full + 2;  // cluster split-K: this CTA's rows of every split have landed
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -218,7 +217,6 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tmem_full, 1);
-    mbar_init(red_bar, 1);
     fence_barrier_init();
   }
   if (warp == 4) {
@@ -330,15 +328,6 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
     asm volatile("bar.sync 1, 128;" ::: "memory");  // scale/bias in smem visible to all producers
     if (ts && threadIdx.x == 0) ts[4] = gtimer();
     const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
-    if (BN == 64 && a.cluster_split && threadIdx.x == 0) {
-      // Split-K inside one cluster: CTA r owns rows [r*128/S, (r+1)*128/S) of
-      // the tile and receives those rows of all S partials (st.async into its
-      // idle A ring); arm its mbarrier for them before the cluster barrier.
-      const int S = a.splits;
-      const int r_begin = (split * kBM) / S, r_end = ((split + 1) * kBM) / S;
-      const int valid = max(0, min(r_end, mvalid) - r_begin);
-      mbar_arrive_expect_tx(red_bar, static_cast<uint32_t>(S * valid * BN * 4));
-    }
     if (BN == 64 && a.cluster_split) {
       // (cluster barrier and reduction below, executed by all 192 threads)
     } else if (a.splits == 1 && a.tma_c) {
@@ -510,58 +499,72 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
   }
 
   if (BN == 64 && a.cluster_split) {
+    // Split-K inside one cluster, pulled: every CTA stages its fp32 partial tile
+    // in its own (now idle) A ring, row per thread, 16-B chunks XOR-swizzled by
+    // row; after one cluster barrier CTA r reduces rows [r*V/S, (r+1)*V/S)
+    // (V = the tile's valid rows) by reading them from every CTA's stage (ld.shared::cluster,
+    // 8 lanes per 256-B row), applies the epilogue and stores. Staging + pulling
+    // measured 1.44 us per exchange vs 2.08 us for st.async pushes of whole
+    // rows (tools/dsmem_probe.cu, profiles/r02_dsmem_probe.txt).
     const int S = a.splits;
-    const int rpc_max = (kBM + S - 1) / S;
-    float* recv = reinterpret_cast<float*>(sA);  // [S][rpc_max][BN] fp32
+    float* stage = reinterpret_cast<float*>(sA);  // [128][BN] fp32
     __syncwarp();
     if (ts && threadIdx.x == 0) ts[8] = gtimer();
-    cluster_sync();  // every split's MMAs are done (rings idle) and every receiver is armed
-    if (ts && threadIdx.x == 0) ts[9] = gtimer();
     if (warp < 4) {
-      // push this thread's accumulator row to the CTA that owns it (st.async;
-      // measured faster than staging locally + one bulk DMA per owner)
       const int row = warp * 32 + lane;
-      const bool push = row < mvalid;
-      const int owner = ((row + 1) * S - 1) / kBM;
-      const int j = row - (owner * kBM) / S;
-      const uint32_t dst = dsmem_map(smem_u32(recv + (static_cast<size_t>(split) * rpc_max + j) * BN), owner);
-      const uint32_t bar = dsmem_map(smem_u32(red_bar), owner);
       const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
 #pragma unroll
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
-        tmem_ld_32x32b_x32(t_row + c0, r);  // warp-collective (.sync.aligned): every lane loads
-        if (push) {
+        tmem_ld_32x32b_x32(t_row + c0, r);  // warp-collective: every lane loads
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            st_async_v4(dst + (c0 + 4 * q) * 4, __uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                        __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]), bar);
+        for (int q = 0; q < 8; ++q) {
+          const int chunk = (c0 >> 2) + q;  // 16-B chunk index in the row (BN / 4 per row)
+          *reinterpret_cast<float4*>(stage + row * BN + ((chunk ^ (row & 15)) << 2)) =
+              make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
+                          __uint_as_float(r[4 * q + 3]));
         }
       }
     }
-    __syncwarp();
-    cluster_arrive();  // (released before exit: no CTA leaves while peers may still push to it)
+    cluster_sync();  // every split's partial is staged
+    if (ts && threadIdx.x == 0) ts[9] = gtimer();
     if (warp < 4) {
-      const int r_begin = (split * kBM) / S, r_end = ((split + 1) * kBM) / S;
-      const int valid = max(0, min(r_end, mvalid) - r_begin);
-      mbar_wait(red_bar, 0);
-      if (ts && threadIdx.x == 0) ts[10] = gtimer();
+      // the tile's valid rows split evenly over the S CTAs (layer4 at batch 1:
+      // 49 rows -> 16 / 16 / 17, not 43 / 6 / 0)
+      const int r_begin = (split * mvalid) / S, r_end = ((split + 1) * mvalid) / S;
+      const int valid = r_end - r_begin;
       float* s_scale = reinterpret_cast<float*>(smem + L::kEpiOff);
       float* s_bias = s_scale + BN;
+      const uint32_t stage_u32 = smem_u32(stage);
       const int items = valid * (BN / 8);  // (row, 8-column group)
       for (int it = threadIdx.x; it < items; it += 128) {
         const int j = it / (BN / 8), g = it % (BN / 8);
-        const int m = m0 + r_begin + j;
+        const int rr = r_begin + j;
+        const int m = m0 + rr;
         const int c = g * 8;
         const size_t off = static_cast<size_t>(m) * a.cout + n0 + c;
         uint4 rv = make_uint4(0, 0, 0, 0);
         if (a.res != nullptr) rv = ldg_nc16(a.res + off);
+        const uint32_t a0 = stage_u32 + static_cast<uint32_t>((rr * BN + (((2 * g) ^ (rr & 15)) << 2)) * 4);
+        const uint32_t a1 = stage_u32 + static_cast<uint32_t>((rr * BN + (((2 * g + 1) ^ (rr & 15)) << 2)) * 4);
         float v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int k = 0; k < S; ++k) {
-          const float4* src = reinterpret_cast<const float4*>(recv + (static_cast<size_t>(k) * rpc_max + j) * BN + c);
-          const float4 p0 = src[0], p1 = src[1];
-          v[0] += p0.x; v[1] += p0.y; v[2] += p0.z; v[3] += p0.w;
-          v[4] += p1.x; v[5] += p1.y; v[6] += p1.z; v[7] += p1.w;
+#pragma unroll 1
+        for (int k0 = 0; k0 < S; k0 += 4) {  // S <= 8: up to 4 peers' chunks in flight at once
+          float4 p0[4], p1[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (k0 + k < S) {
+              p0[k] = ld_dsmem_f4(dsmem_map(a0, k0 + k));
+              p1[k] = ld_dsmem_f4(dsmem_map(a1, k0 + k));
+            }
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (k0 + k < S) {
+              v[0] += p0[k].x; v[1] += p0[k].y; v[2] += p0[k].z; v[3] += p0[k].w;
+              v[4] += p1[k].x; v[5] += p1[k].y; v[6] += p1[k].z; v[7] += p1[k].w;
+            }
+          }
         }
         float rf[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         if (a.res != nullptr) {
@@ -584,9 +587,9 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
         *reinterpret_cast<uint4*>(a.y + off) = pk;
       }
     }
-    __syncwarp();
+    if (ts && threadIdx.x == 0) ts[10] = gtimer();
+    cluster_sync();  // nobody leaves (or reuses its stage) while a peer may still read it
     if (ts && threadIdx.x == 0) ts[11] = gtimer();
-    cluster_wait();
   }
   if (ts && threadIdx.x == 0) ts[5] = gtimer();
   tc_fence_before();
@@ -828,8 +831,12 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
     // split-K costs one fix-up round trip (~2 us): only worth it for long K
     // loops on grids that leave most of the partition idle
     splits = 1;
+    static const int split_factor = [] {  // A/B knob: CTAs per planned SM for split-K grids
+      const char* e = std::getenv("DARIS_SPLIT_FACTOR");
+      return e ? std::max(1, std::atoi(e)) : 1;
+    }();
     if (tiles * 2 <= budget && num_kb >= 8) {
-      splits = budget / tiles;
+      splits = split_factor * budget / tiles;
       const int max_by_k = num_kb / 4;  // keep >= 4 K blocks per split
       if (splits > max_by_k) splits = max_by_k;
       if (splits > 32) splits = 32;

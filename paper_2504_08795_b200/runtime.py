@@ -147,7 +147,9 @@ class Executor:
     def cluster_partition(self) -> int:
         """1-based context of the first partition that holds a co-scheduled SM
         group (8-CTA clusters launch there), e.g. for single-partition tools."""
-        return next((p["context"] for p in self.partitions if p["group_size"] >= 8), 1)
+        ctx = next((p["context"] for p in self.partitions if p["group_size"] >= 8), 1)
+        K.CLUSTER_SPLITK = self.partitions[ctx - 1]["group_size"] >= 8   # the tool runs there only
+        return ctx
 
     def stream(self, context: int, stream: int) -> int:
         out = C.c_void_p()

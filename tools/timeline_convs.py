@@ -100,11 +100,13 @@ def main():
                                  statistics.median((a[:, 8] - a[:, 4]).tolist())]
         if op.layer.name in args.dump:
             print(f"--- {op.layer.name}: per CTA (us from the layer's first release): sm start released "
-                  f"prod_done acc_ready epi_done exit")
+                  f"prod_done acc_ready epi_done exit [cluster: pre_sync post_sync recv_done reduce_done]")
             order = sorted(range(a.shape[0]), key=lambda c: a[c, 0].item())
             for c in order:
+                extra = (" | " + " ".join(f"{a[c, k].item() - released:7.2f}" for k in (8, 9, 10, 11))
+                         if raw[c, 8] > 0 else "")
                 print(f"  cta {c:3d} sm {int(raw_sm[c]):3d} " + " ".join(
-                    f"{a[c, k].item() - released:7.2f}" for k in (0, 2, 3, 4, 5, 6)))
+                    f"{a[c, k].item() - released:7.2f}" for k in (0, 2, 3, 4, 5, 6)) + extra)
         prev_end = end
         rows.append(row)
     total = rows[-1]["end"] - rows[0]["released"]
