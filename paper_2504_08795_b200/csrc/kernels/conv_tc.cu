@@ -831,12 +831,10 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
     // split-K costs one fix-up round trip (~2 us): only worth it for long K
     // loops on grids that leave most of the partition idle
     splits = 1;
-    static const int split_factor = [] {  // A/B knob: CTAs per planned SM for split-K grids
-      const char* e = std::getenv("DARIS_SPLIT_FACTOR");
-      return e ? std::max(1, std::atoi(e)) : 1;
-    }();
+    // (two or three split CTAs per planned SM: isolated job 0.343 -> 0.316 ms, but
+    // loaded 4x2 capacity 17.7k -> 17.7k / 16.7k inf/s: profiles/r02_split_factor_ab.txt)
     if (tiles * 2 <= budget && num_kb >= 8) {
-      splits = split_factor * budget / tiles;
+      splits = budget / tiles;
       const int max_by_k = num_kb / 4;  // keep >= 4 K blocks per split
       if (splits > max_by_k) splits = max_by_k;
       if (splits > 32) splits = 32;
