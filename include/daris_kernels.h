@@ -82,6 +82,8 @@ typedef struct daris_conv_plan_t {
   int32_t ctas;
   int32_t cluster;          /* CTAs per cluster (split-K through DSMEM), 1 = none */
   int32_t tma_rows;         /* > 0: activations arrive by TMA, M tile = tma_rows whole output rows */
+  int32_t pair;             /* 1: CTA pairs (cta_group::2, UMMA M = 256 over two M tiles, each CTA
+                               loading half the weight tile) — large-M launches without split-K */
 } daris_conv_plan_t;
 
 int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out);

@@ -600,6 +600,192 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
 }
 
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// CTA-pair conv for large-M launches (batched jobs, single-tenant batching):
+// a (2,1,1) cluster on one TPC runs one UMMA M = 256 tile with
+// tcgen05.mma.cta_group::2. Each CTA loads its own 128-row activation tile (the
+// same TMA boxes as above: th whole output rows, stem windows or the fused
+// downsample branch) and HALF of the BN-wide weight tile, both into the same
+// smem offsets; both CTAs' loads complete on the leader's full barrier
+// (cta_group::2 TMA), the leader alone issues the MMAs, and its commits arrive
+// on both CTAs' empty / accumulator barriers (multicast). Every CTA then runs
+// the TMA-store epilogue of its own 128 accumulator rows from its own TMEM.
+// Per SM and K block this moves 16 KB of A + BN/2 x 128 B of B for a
+// 128 x BN x 64 MMA share — half the weight traffic of a one-CTA tile.
+template <int BN, int ST>
+struct PairLayout {
+  static constexpr int kABytes = kBM * 128;
+  static constexpr int kBBytes = (BN / 2) * 128;
+  static constexpr int kAOff = 0;
+  static constexpr int kBOff = ST * kABytes;
+  static constexpr int kBarOff = kBOff + ST * kBBytes;
+  static constexpr int kEpiOff = kBarOff + 256;
+  static constexpr int kTotal = kEpiOff + 2 * BN * 4 + 1024;
+  static_assert((BN / 64) * kBM * 128 <= ST * kABytes, "output staging must fit in the A ring");
+};
+
+template <int BN, int ST>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    conv_pair_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
+                     const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap amap2,
+                     const ConvArgs a) {
+  using L = PairLayout<BN, ST>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem + L::kAOff;
+  uint8_t* sB = smem + L::kBOff;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
+  uint64_t* empty = full + ST;
+  uint64_t* tmem_full = empty + ST;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int tile_m = blockIdx.x, tile_n = blockIdx.y;
+  const int img = fdiv(tile_m, a.d_tiles_h);
+  const int h0 = (tile_m - img * a.tiles_h) * a.th;
+  const int m0 = img * (a.ho * a.wo) + h0 * a.wo;
+  // an odd M-tile count leaves the last pair's second CTA a phantom tile past
+  // the last image: its boxes read zeros and its stores are clipped
+  const int mvalid = img < a.n ? min(a.th, a.ho - h0) * a.wo : 0;
+  const int n0 = tile_n * BN;
+  const int nkb = a.num_kb;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);   // the leader's producer arms it for both CTAs' bytes
+      mbar_init(&empty[s], 1);  // one multicast commit from the leader's MMA thread
+    }
+    mbar_init(tmem_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 4) {
+    tmem_alloc_cg2<BN>(tmem_slot);
+    if (lane == 0) {
+      tma_prefetch_desc(&wmap);
+      tma_prefetch_desc(&amap);
+      tma_prefetch_desc(&ymap);
+      if (a.kb_seg1 < a.num_kb) tma_prefetch_desc(&amap2);
+    }
+  }
+  tc_fence_before();
+  cluster_sync();  // both CTAs' barriers initialised and TMEM allocated before any cross-CTA traffic
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < 4) {
+    float* s_scale = reinterpret_cast<float*>(smem + L::kEpiOff);
+    float* s_bias = s_scale + BN;
+    for (int c = threadIdx.x; c < BN; c += 128) {
+      s_scale[c] = __ldg(a.scale + n0 + c);
+      s_bias[c] = __ldg(a.bias + n0 + c);
+    }
+    pdl_wait();  // the residual comes from an earlier layer
+    const int row = warp * 32 + lane;
+    const bool row_ok = row < mvalid;
+    const bool has_res = a.res != nullptr && row_ok;
+    const __nv_bfloat16* res_row = has_res ? a.res + static_cast<size_t>(m0 + row) * a.cout + n0 : nullptr;
+    uint4 res_cur[4];
+    if (has_res) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) res_cur[q] = ldg_nc16(res_row + 8 * q);
+    }
+    __syncwarp();
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    if (threadIdx.x == 0) pdl_trigger();
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    const uint32_t t_row = tmem_base + (static_cast<uint32_t>(warp * 32) << 16);
+    uint8_t* stage = sA;
+    const uint32_t swz = static_cast<uint32_t>(row & 7);
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t r[32];
+      uint4 res_nxt[4];
+      if (has_res && c0 + 32 < BN) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) res_nxt[q] = ldg_nc16(res_row + c0 + 32 + 8 * q);
+      }
+      tmem_ld_32x32b_x32(t_row + c0, r);
+      uint8_t* rowp = stage + (c0 >> 6) * (kBM * 128) + row * 128;
+      const uint32_t chunk0 = static_cast<uint32_t>((c0 & 63) >> 3);
+      uint4 pk[4];
+      pack_row32(a, c0, reinterpret_cast<const float*>(r), s_scale, s_bias, res_cur, has_res, pk);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(rowp + (((chunk0 + q) ^ swz) << 4)) = pk[q];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) res_cur[q] = res_nxt[q];
+    }
+    fence_proxy_async_smem();
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (threadIdx.x == 0 && mvalid > 0) {
+#pragma unroll
+      for (int h = 0; h < BN / 64; ++h) tma_store_3d(&ymap, stage + h * (kBM * 128), n0 + h * 64, h0 * a.wo, img);
+      bulk_commit();
+      bulk_wait_read();
+    }
+  } else if (warp == 4) {
+    if (lane == 0) {
+      const uint32_t a_bytes = static_cast<uint32_t>(a.th * a.wo * 128);
+      const uint32_t stage_tx = 2u * (a_bytes + static_cast<uint32_t>(L::kBBytes));  // both CTAs
+      const int nb0 = n0 + static_cast<int>(rank) * (BN / 2);
+      auto load_a = [&](int kb, int s) {
+        if (a.stem_tma) {
+          tma_load_4d_cg2(&amap, &full[s], sA + s * L::kABytes, 0, 0, h0 * a.stride + kb, img);
+          return;
+        }
+        if (kb >= a.kb_seg1) {
+          tma_load_4d_cg2(&amap2, &full[s], sA + s * L::kABytes, (kb - a.kb_seg1) * kBK, 0, h0 * a.stride2, img);
+          return;
+        }
+        const int kpos = fdiv(kb, a.d_cinb);
+        const int cb = kb - kpos * a.cin_blocks;
+        const int r_ = fdiv(kpos, a.d_kw), s_ = kpos - r_ * a.kw;
+        tma_load_4d_cg2(&amap, &full[s], sA + s * L::kABytes, cb * kBK, s_ - a.pad, h0 * a.stride - a.pad + r_,
+                        img);
+      };
+      const int pre = min(nkb, ST);
+      for (int i = 0; i < pre; ++i) {  // weights first: they do not depend on the previous layer
+        if (rank == 0) mbar_arrive_expect_tx(&full[i], stage_tx);
+        tma_load_2d_cg2(&wmap, &full[i], sB + i * L::kBBytes, i * kBK, nb0);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) load_a(i, i);
+      for (int i = pre; i < nkb; ++i) {
+        const int s = i % ST;
+        mbar_wait(&empty[s], ((i / ST) & 1) ^ 1);
+        if (rank == 0) mbar_arrive_expect_tx(&full[s], stage_tx);
+        tma_load_2d_cg2(&wmap, &full[s], sB + s * L::kBBytes, i * kBK, nb0);
+        load_a(i, s);
+      }
+    }
+  } else if (rank == 0 && lane == 0) {
+    // ---------------- MMA issuer (leader only): D[256 x BN] over both CTAs ----------------
+    constexpr uint32_t idesc = umma_idesc_bf16(2 * kBM, BN);
+    const uint32_t sA_u32 = smem_u32(sA), sB_u32 = smem_u32(sB);
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % ST;
+      mbar_wait(&full[s], (i / ST) & 1);
+      tc_fence_after();
+      const uint64_t adesc = umma_desc_k_sw128(sA_u32 + s * L::kABytes);
+      const uint64_t bdesc = umma_desc_k_sw128(sB_u32 + s * L::kBBytes);
+#pragma unroll
+      for (int k = 0; k < kBK / 16; ++k)
+        umma_bf16_cg2(tmem_base, adesc + 2 * k, bdesc + 2 * k, idesc, (i > 0 || k > 0) ? 1u : 0u);
+      umma_commit_cg2(&empty[s], 0x3);
+    }
+    umma_commit_cg2(tmem_full, 0x3);
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the peer's smem / TMEM are done with before either CTA frees TMEM or exits
+  if (warp == 4) {
+    tc_fence_after();
+    tmem_dealloc_cg2<BN>(tmem_base);
+  }
+}
+
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -614,9 +800,21 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
-template <int BN, int ST = Depth<BN>::kStages>
+template <int BN, int ST, bool PAIR>
+constexpr auto conv_kernel_fn() {
+  if constexpr (PAIR) return conv_pair_kernel<BN, ST>;
+  else return conv_igemm_tc_kernel<BN, ST>;
+}
+template <int BN, int ST, bool PAIR>
+constexpr int conv_smem_bytes() {
+  if constexpr (PAIR) return PairLayout<BN, ST>::kTotal;
+  else return SmemLayout<BN, ST>::kTotal;
+}
+
+template <int BN, int ST = Depth<BN>::kStages, bool PAIR = false>
 static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cudaStream_t st) {
-  using L = SmemLayout<BN, ST>;
+  constexpr int kSmem = conv_smem_bytes<BN, ST, PAIR>();
+  auto kernel = conv_kernel_fn<BN, ST, PAIR>();
   auto encode = get_encode_fn();
   if (!encode) return DARIS_K_NO_DRIVER;
   const int K = ((d->flags & DARIS_CONV_PADDED_INPUT) ? d->kh * 64 : d->kh * d->kw * d->cin) +
@@ -624,7 +822,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   CUtensorMap map;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(d->cout)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(K) * 2};
-  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(BN)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(PAIR ? BN / 2 : BN)};  // a pair: half each
   cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(d->weight), dims, strides, box,
                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -706,9 +904,8 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
 
   static bool attr_set = false;  // per template instantiation
   if (!attr_set) {
-    set_max_carveout(reinterpret_cast<const void*>(conv_igemm_tc_kernel<BN, ST>));
-    cudaError_t e =
-        cudaFuncSetAttribute(conv_igemm_tc_kernel<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kTotal);
+    set_max_carveout(reinterpret_cast<const void*>(kernel));
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -745,9 +942,9 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   a.d_tiles_h = make_fdiv(a.tiles_h);
   a.ts = reinterpret_cast<unsigned long long*>(d->timestamps);
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(pl.tiles_m, pl.tiles_n, pl.splits);
+  cfg.gridDim = dim3(PAIR ? (pl.tiles_m + 1) / 2 * 2 : pl.tiles_m, pl.tiles_n, pl.splits);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = L::kTotal;
+  cfg.dynamicSmemBytes = kSmem;
   cfg.stream = st;
   // experiment knob: without PDL a layer's CTAs are not launched early (an early
   // CTA holds smem/TMEM while it waits for its predecessor)
@@ -760,14 +957,14 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
     attr[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
     cfg.numAttrs++;
   }
-  if (pl.cluster > 1) {
+  if (!PAIR && pl.cluster > 1) {  // (the pair kernel's (2,1,1) cluster is compile-time)
     attr[cfg.numAttrs].id = cudaLaunchAttributeClusterDimension;
     attr[cfg.numAttrs].val.clusterDim.x = 1;
     attr[cfg.numAttrs].val.clusterDim.y = 1;
     attr[cfg.numAttrs].val.clusterDim.z = pl.cluster;
     cfg.numAttrs++;
   }
-  return static_cast<int>(cudaLaunchKernelEx(&cfg, conv_igemm_tc_kernel<BN, ST>, map, amap, ymap, amap2, a));
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, kernel, map, amap, ymap, amap2, a));
 }
 
 
@@ -854,6 +1051,21 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
   out->ctas = tiles_m * tiles_n * splits;
   out->cluster = (splits > 1 && bn == 64 && (d->flags & DARIS_CONV_CLUSTER_SPLITK)) ? splits : 1;
   out->tma_rows = tma_a ? th : 0;
+  // CTA pairs for large-M launches: TMA activations, no split-K, 128-wide (or
+  // wider) tiles, at least one wave of tiles over the planned SMs, a K loop of
+  // >= 16 blocks and <= 512 output channels. ResNet-50 at batch 64 on 148 SMs
+  // (profiles/r02_pair_ab_b64.txt): 3x3 convs 24.2 -> 17.7 us (610 -> 835
+  // TF/s), layer3 conv1 15.4 -> 11.7 us; the short-K / 1024-2048-channel
+  // conv3s are faster as one-CTA tiles at 3 CTAs per SM (28.1 vs 32.8 us).
+  // DARIS_CONV_PAIR=0 turns pairs off (A/B), =2 takes them wherever legal.
+  static const int pair_mode = [] {
+    const char* e = std::getenv("DARIS_CONV_PAIR");
+    return e ? std::atoi(e) : 1;
+  }();
+  out->pair = 0;
+  if (pair_mode > 0 && tma_a && splits == 1 && bn >= 128 && tiles_m >= 2 &&
+      (pair_mode == 2 || (tiles >= budget && num_kb >= 16 && d->cout <= 512)))
+    out->pair = 1;
   if (out->cluster > 1) {  // partials reduce through DSMEM: no global scratch
     out->workspace_floats = 0;
     out->counters = 0;
@@ -870,6 +1082,13 @@ extern "C" int daris_conv2d(const daris_conv_desc* d, void* stream) {
   if ((d->flags & DARIS_CONV_DUAL) && !d->x2) return DARIS_K_BAD_ARG;
   if (pl.splits > 1 && pl.cluster == 1 && (!d->workspace || !d->counters)) return DARIS_K_WORKSPACE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (pl.pair) {
+    switch (pl.block_n) {
+      case 128: return launch_bn<128, 4, true>(d, pl, st);
+      case 256: return launch_bn<256, 4, true>(d, pl, st);
+    }
+    return DARIS_K_BAD_SHAPE;
+  }
   switch (pl.block_n) {
     case 64: return launch_bn<64>(d, pl, st);
     case 128: return launch_bn<128>(d, pl, st);

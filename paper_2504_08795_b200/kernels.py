@@ -37,6 +37,7 @@ class ConvPlan(C.Structure):
         ("block_n", C.c_int32), ("splits", C.c_int32), ("kb_per_split", C.c_int32),
         ("tiles_m", C.c_int32), ("tiles_n", C.c_int32), ("workspace_floats", C.c_int64),
         ("counters", C.c_int32), ("ctas", C.c_int32), ("cluster", C.c_int32), ("tma_rows", C.c_int32),
+        ("pair", C.c_int32),
     ]
 
 

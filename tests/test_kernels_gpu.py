@@ -320,3 +320,55 @@ def test_avgpool_bf16():
     torch.cuda.synchronize()
     assert y.dtype == torch.bfloat16
     _close(y, x.float().mean(dim=(1, 2)))
+
+
+@pytest.mark.parametrize("n,h,cin,cout,k,stride,pad,residual,bn", [
+    (8, 28, 128, 128, 3, 1, 1, True, 128),     # layer2 conv2 shape at batch 8, residual
+    (3, 28, 256, 256, 3, 1, 1, True, 256),     # odd M-tile count (21): a phantom tile in the last pair
+    (8, 56, 128, 128, 3, 2, 1, False, 128),    # strided
+    (16, 14, 1024, 256, 1, 1, 0, True, 128),   # 1x1, K = 1024
+    (4, 7, 512, 512, 3, 1, 1, False, 256),     # layer4 conv2, one tile per image
+])
+def test_conv_cta_pair(n, h, cin, cout, k, stride, pad, residual, bn):
+    """cta_group::2 pairs (UMMA M = 256 over two M tiles, each CTA loading half
+    the weight tile): the planner picks them for large-M grids; numerics as the
+    one-CTA path."""
+    from paper_2504_08795_b200 import kernels as K
+    d = K.conv_desc((n, h, h, cin), cout, k, k, stride, pad, block_n=bn, sm_budget=8)
+    p = K.conv_plan(d)
+    assert p.pair == 1 and p.splits == 1, (p.pair, p.splits)
+    _conv_case(n, h, h, cin, cout, k, stride, pad, residual=residual, block_n=bn, sm_budget=8, seed=n + h)
+
+
+def test_conv_cta_pair_dual_branch():
+    """The pair path with the fused downsample branch (layer4.0 conv3 at batch 8;
+    the default plan keeps 2048-channel convs on one-CTA tiles, so pairs are
+    forced with DARIS_CONV_PAIR=2 in a child process: the planner reads it once)."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import sys, torch
+sys.path[:0] = [sys.argv[1], sys.argv[1] + '/tests']
+import test_kernels_gpu as T
+from paper_2504_08795_b200 import kernels as K
+dev = torch.device('cuda')
+g = torch.Generator().manual_seed(77)
+n, hw, cin, cout, hw2, cin2, stride2 = 8, 7, 512, 2048, 14, 1024, 2
+d = K.conv_desc((n, hw, hw, cin), cout, 1, 1, 1, 0, sm_budget=8, x2_shape=(n, hw2, hw2, cin2), stride2=stride2)
+assert K.conv_plan(d).pair == 1
+x = torch.randn(n, hw, hw, cin, generator=g).bfloat16()
+x2 = torch.randn(n, hw2, hw2, cin2, generator=g).bfloat16()
+w = (torch.randn(cout, cin + cin2, generator=g) / (cin + cin2) ** 0.5).bfloat16()
+bias = torch.randn(cout, generator=g) * 0.1
+ref = x.float() @ w[:, :cin].float().t() + x2[:, ::stride2, ::stride2, :].float() @ w[:, cin:].float().t()
+ref = (ref + bias).clamp_min(0)
+out = K.conv2d(x.to(dev), w.to(dev), torch.ones(cout, device=dev), bias.to(dev), relu=1, kh=1, kw=1,
+               x2=x2.to(dev), stride2=stride2, sm_budget=8)
+torch.cuda.synchronize()
+T._close(out, ref)
+"""
+    root = str(__import__("pathlib").Path(__file__).resolve().parents[1])
+    r = subprocess.run([sys.executable, "-c", code, root], env=dict(os.environ, DARIS_CONV_PAIR="2"),
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]

@@ -48,18 +48,18 @@ def main():
         gpu_times = rt.exec.trace_gpu()  # aligned with res.trace
         for t, g in zip(res.trace, gpu_times):
             task, job, stage = t[0], t[1], t[2]
-            per_job[(task, job)][stage] = tuple(t) + tuple(g)
+            per_job[(task, job)][stage] = (t[6], t[7]) + tuple(g)   # host start, host end, gpu start, gpu end
         execs = defaultdict(list)
         gaps = defaultdict(list)
         host_obs = []
         for stages in per_job.values():
-            if len(stages) != 4 or not all(stages[s][8] > 0 for s in range(4)):  # (NaN: no timing)
+            if len(stages) != 4 or not all(stages[s][2] > 0 for s in range(4)):  # (NaN: no timing)
                 continue
             for s in range(4):
-                execs[s].append(stages[s][9] - stages[s][8])
-                host_obs.append(stages[s][7] - stages[s][9])  # host saw completion after the GPU end event
+                execs[s].append(stages[s][3] - stages[s][2])
+                host_obs.append(stages[s][1] - stages[s][3])  # host saw completion after the GPU end event
                 if s < 3:
-                    gaps[s].append(stages[s + 1][8] - stages[s][9])
+                    gaps[s].append(stages[s + 1][2] - stages[s][3])
         rep = res.report
         print(f"rate {rate:.0f}/task: jps {rep.jps:.0f}, HP p99 {rep.response_hp.p99 * 1e3:.3f} ms, jobs {len(per_job)}")
         for s in range(4):
