@@ -1063,7 +1063,7 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
     return e ? std::atoi(e) : 1;
   }();
   out->pair = 0;
-  if (pair_mode > 0 && tma_a && splits == 1 && bn >= 128 && tiles_m >= 2 &&
+  if (pair_mode > 0 && tma_a && splits == 1 && (bn >= 128 || pair_mode == 2) && tiles_m >= 2 &&
       (pair_mode == 2 || (tiles >= budget && num_kb >= 16 && d->cout <= 512)))
     out->pair = 1;
   if (out->cluster > 1) {  // partials reduce through DSMEM: no global scratch
@@ -1084,6 +1084,7 @@ extern "C" int daris_conv2d(const daris_conv_desc* d, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (pl.pair) {
     switch (pl.block_n) {
+      case 64: return launch_bn<64, 4, true>(d, pl, st);
       case 128: return launch_bn<128, 4, true>(d, pl, st);
       case 256: return launch_bn<256, 4, true>(d, pl, st);
     }
