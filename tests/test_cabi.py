@@ -98,6 +98,12 @@ def test_gpu_library_is_tcgen05_tma_sm100a():
     assert "sm_100a" in sass
     for mnemonic in ("UTCHMMA", "UTMALDG", "UTMASTG"):
         assert mnemonic in sass, mnemonic
+    # the CTA-pair conv kernel: 2-SM MMAs, 2-SM TMA loads, multicast commits
+    for mnemonic in ("UTCHMMA.2CTA", "UTMALDG.4D.2CTA", "UTCBAR.2CTA.MULTICAST"):
+        assert mnemonic in sass, mnemonic
+    # the classifier layers run on the tensor cores too (linear_tc_kernel)
+    lin = sass[sass.find("linear_tc_kernel"):]
+    assert "UTCHMMA" in lin[:200000]
     res = subprocess.run([cuobjdump, "-res-usage", str(lib)], capture_output=True, text=True, check=True).stdout
     regs = [int(r) for r in re.findall(r"conv_igemm_tc_kernel\S*:\s*\n\s*REG:(\d+)", res)]
     assert regs and max(regs) <= 96, regs
