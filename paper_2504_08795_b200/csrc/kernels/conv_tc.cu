@@ -90,6 +90,7 @@ struct ConvArgs {
   int tma_a;          // 1: activations arrive by TMA (4-D box = th whole output rows of one image)
   int th, tiles_h;    // TMA mode: output rows per M tile, M tiles per image
   int tma_c;          // 1: the epilogue stages the bf16 tile in smem and stores it with TMA (splits == 1)
+  int res_tma;        // 1: the residual tile arrives by TMA into the ring stage the K loop never uses
   int stem_tma;       // 1: 8-channel stem from a zero-bordered input, one TMA window box per kernel row
   int kb_seg1;        // K blocks of the primary input; blocks >= kb_seg1 come from x2 (DARIS_CONV_DUAL)
   int stride2;        // x2 sampling stride
@@ -178,7 +179,7 @@ template <int BN, int ST>
 __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
     conv_igemm_tc_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
                          const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap amap2,
-                         const ConvArgs a) {
+                         const __grid_constant__ CUtensorMap rmap, const ConvArgs a) {
   using L = SmemLayout<BN, ST>;
   constexpr int kStages = L::kStages;
   constexpr int kLag = L::kLag;
@@ -191,6 +192,14 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
   uint64_t* tmem_full = empty + kStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
+  uint64_t* res_bar = tmem_full + 2;  // the residual tile has landed (res_tma)
+  // res_tma: residual half h (64 channels x 128 rows, 128B-swizzled like the output
+  // staging) in the LAST ring stage — A stage for h = 0, B stage for h = 1 (BN = 128)
+  uint8_t* res_half0 = sA + (kStages - 1) * L::kABytes;
+  uint8_t* res_half1 = sB + (kStages - 1) * L::kBBytes;
+  // output staging: half 0 in A stage 0, half 1 in B stage 0 at BN = 128 (clear of
+  // the residual); contiguous from A stage 0 otherwise
+  auto out_half = [&](int h) -> uint8_t* { return (BN == 128 && h == 1) ? sB : sA + h * (kBM * 128); };
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -226,6 +235,7 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tmem_full, 1);
+    mbar_init(res_bar, 1);
     fence_barrier_init();
   }
   if (warp == 4) {
@@ -235,6 +245,7 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
       if (a.tma_a) tma_prefetch_desc(&amap);
       if (a.tma_c) tma_prefetch_desc(&ymap);
       if (a.kb_seg1 < a.num_kb) tma_prefetch_desc(&amap2);
+      if (a.res_tma) tma_prefetch_desc(&rmap);
     }
   }
   tc_fence_before();
@@ -323,7 +334,7 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
     const __nv_bfloat16* res_row = has_res ? a.res + static_cast<size_t>(m) * a.cout + n0 : nullptr;
     // this thread's first residual chunk: in flight while the last loads land / MMAs drain
     uint4 res_cur[4];
-    if (has_res) {
+    if (has_res && !a.res_tma) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) res_cur[q] = ldg_nc16(res_row + 8 * q);
     }
@@ -344,10 +355,10 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
       // 128 B rows, 128B-swizzled (conflict-free 16 B writes, one row per
       // thread), then one TMA store per half: coalesced, asynchronous, and
       // rows past the image / tensor end are clipped by the tensor map.
-      uint8_t* stage = sA;
       const uint32_t swz = static_cast<uint32_t>(row & 7);
       const int c1 = a.tma_a ? h0 * a.wo : m0;
       const int c2 = a.tma_a ? img : 0;
+      if (a.res_tma) mbar_wait(res_bar, 0);
       // (the residual by chunk, the next chunk's loads in flight while this one is
       // packed: all of a row at once through cp.async into the idle B ring after
       // the accumulator is ready measured slower — layer1 conv3 9.1 -> 10.1 us at
@@ -357,26 +368,34 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t r[32];
         uint4 res_nxt[4];
-        if (has_res && c0 + 32 < BN) {
+        const uint32_t chunk0 = static_cast<uint32_t>((c0 & 63) >> 3);
+        if (a.res_tma) {
+          if (has_res) {  // this chunk of the row from the TMA-staged residual (same swizzle)
+            const uint8_t* rp = (c0 < 64 ? res_half0 : res_half1) + row * 128;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) res_cur[q] = *reinterpret_cast<const uint4*>(rp + (((chunk0 + q) ^ swz) << 4));
+          }
+        } else if (has_res && c0 + 32 < BN) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) res_nxt[q] = ldg_nc16(res_row + c0 + 32 + 8 * q);
         }
         tmem_ld_32x32b_x32(t_row + c0, r);
-        uint8_t* rowp = stage + (c0 >> 6) * (kBM * 128) + row * 128;
-        const uint32_t chunk0 = static_cast<uint32_t>((c0 & 63) >> 3);
+        uint8_t* rowp = out_half(c0 >> 6) + row * 128;
         uint4 pk[4];
         pack_row32(a, c0, reinterpret_cast<const float*>(r), s_scale, s_bias, res_cur, has_res, pk);
 #pragma unroll
         for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(rowp + (((chunk0 + q) ^ swz) << 4)) = pk[q];
+        if (!a.res_tma) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) res_cur[q] = res_nxt[q];
+          for (int q = 0; q < 4; ++q) res_cur[q] = res_nxt[q];
+        }
       }
       fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the TMA engine
       asm volatile("bar.sync 1, 128;" ::: "memory");
       if (threadIdx.x == 0) {
 #pragma unroll
         for (int h = 0; h < BN / 64; ++h)
-          tma_store_3d(&ymap, stage + h * (kBM * 128), n0 + h * 64, c1, c2);
+          tma_store_3d(&ymap, out_half(h), n0 + h * 64, c1, c2);
         bulk_commit();
         bulk_wait_read();
       }
@@ -465,6 +484,11 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
         tma_load_2d(&wmap, &full[i], sB + i * L::kBBytes, (kb_begin + i) * kBK, n0);
       }
       pdl_wait();
+      if (a.res_tma) {  // stage nkb..kStages-1 is never used by the K loop: the residual goes there
+        mbar_arrive_expect_tx(res_bar, static_cast<uint32_t>((BN / 64) * a.box_rows * 128));
+        tma_load_3d(&rmap, res_bar, res_half0, n0, h0 * a.wo, img);
+        if (BN == 128) tma_load_3d(&rmap, res_bar, res_half1, n0 + 64, h0 * a.wo, img);
+      }
       for (int i = 0; i < pre; ++i) load_a(i, i);
       for (int i = pre; i < nkb; ++i) {
         const int s = i % kStages;
@@ -628,7 +652,7 @@ template <int BN, int ST>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     conv_pair_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
                      const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap amap2,
-                     const ConvArgs a) {
+                     const __grid_constant__ CUtensorMap /*rmap: unused*/, const ConvArgs a) {
   using L = PairLayout<BN, ST>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -941,6 +965,26 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   a.tiles_h = (d->ho + a.th - 1) / a.th;
   a.d_tiles_h = make_fdiv(a.tiles_h);
   a.ts = reinterpret_cast<unsigned long long*>(d->timestamps);
+  // the residual tile by TMA into the ring stage(s) a short K loop never touches
+  // (K blocks < ring depth: ResNet layer1 / layer2 conv3), issued right after the
+  // dependency wait so it lands during the mainloop instead of being read chunk
+  // by chunk in the epilogue
+  CUtensorMap rmap;
+  std::memset(&rmap, 0, sizeof(rmap));
+  a.res_tma = 0;
+  if (!PAIR && tma_c && pl.tma_rows > 0 && d->residual && BN <= 128 && a.num_kb < ST) {
+    const cuuint64_t rows = static_cast<cuuint64_t>(d->ho) * d->wo;
+    cuuint64_t rdims[3] = {static_cast<cuuint64_t>(d->cout), rows, static_cast<cuuint64_t>(d->n)};
+    cuuint64_t rstr[2] = {static_cast<cuuint64_t>(d->cout) * 2, rows * d->cout * 2};
+    cuuint32_t rbox[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
+    cuuint32_t restr[3] = {1, 1, 1};
+    if (encode(&rmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(d->residual), rdims, rstr, rbox, restr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return DARIS_K_BAD_ARG;
+    static const bool res_tma_off = std::getenv("DARIS_NO_RES_TMA") != nullptr;  // A/B knob
+    a.res_tma = res_tma_off ? 0 : 1;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(PAIR ? (pl.tiles_m + 1) / 2 * 2 : pl.tiles_m, pl.tiles_n, pl.splits);
   cfg.blockDim = dim3(kThreads);
@@ -964,7 +1008,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
     attr[cfg.numAttrs].val.clusterDim.z = pl.cluster;
     cfg.numAttrs++;
   }
-  return static_cast<int>(cudaLaunchKernelEx(&cfg, kernel, map, amap, ymap, amap2, a));
+  return static_cast<int>(cudaLaunchKernelEx(&cfg, kernel, map, amap, ymap, amap2, rmap, a));
 }
 
 
