@@ -711,7 +711,9 @@ def cpu_reference(seconds: float) -> dict:
     gpu = {"total_sms": 1, "n_contexts": 1, "n_streams": 1, "oversubscription": 1.0, "policy": "mps-str",
            "kappa": 0.0}
     horizon = max(seconds, 4 * job_t * 8)
+    t_sched = time.perf_counter()
     recs, _, rep, _ = O.simulate(tasks, gpu, seed=0, duration=horizon, warmup_frac=0.0, reps=2)
+    t_sched = time.perf_counter() - t_sched
     order = [(r[2], r[4]) for r in recs if r[1] == "stage_start"]
     t0 = time.perf_counter()
     done = 0
@@ -728,7 +730,22 @@ def cpu_reference(seconds: float) -> dict:
     return {"value": round(done / elapsed, 3), "unit": UNIT, "cores": torch.get_num_threads(), "kind": "port",
             "sample": f"{done} ResNet-50 b1 fp32 inferences (torch CPU), stages dispatched in the oracle "
                       f"scheduler's order for the 8-task C2 mix, {elapsed:.1f} s",
-            "sim_jps_at_cpu_knee": round(rep["jps"], 2), "hp_miss_sim": rep["missed_hp"]}
+            "sim_jps_at_cpu_knee": round(rep["jps"], 2), "hp_miss_sim": rep["missed_hp"],
+            "cpu_model": _cpu_model(), "host_cpus": os.cpu_count(),
+            "scheduler_dispatches_per_s": round(len(order) / t_sched, 1),
+            "scheduler_note": "the oracle restatement of the reference scheduler (pure Python, 1 thread), "
+                              "stage dispatches per second of its event loop for this mix"}
+
+
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def reference(args) -> dict | None:
