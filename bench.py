@@ -341,7 +341,9 @@ def batching_baseline(batches=(1, 2, 4, 8, 16, 32, 64), reps: int = 20) -> dict:
     import torch
     from paper_2504_08795_b200 import nets
     from paper_2504_08795_b200.runtime import Executor
+    from paper_2504_08795_b200 import kernels as K
     ex = Executor(1, 1, 148, partition="soft", slots=1, max_tasks=1, max_stages=8)
+    K.CTA_PAIRS = True  # one tenant, one stream: large-M convs run as CTA pairs
     sm = ex.partitions[0]["sm_count"]
     sp = ex.stream(1, 0)
     s = torch.cuda.ExternalStream(sp)
@@ -373,6 +375,7 @@ def batching_baseline(batches=(1, 2, 4, 8, 16, 32, 64), reps: int = 20) -> dict:
         out[str(b)] = {"inf_per_s": round(b / lat, 1), "latency_ms": round(lat * 1e3, 3)}
         del net, tb, g
     ex.close()
+    K.CTA_PAIRS = False
     best = max(out.items(), key=lambda kv: kv[1]["inf_per_s"])
     return {"per_batch": out, "best_batch": int(best[0]), "best_inf_per_s": best[1]["inf_per_s"],
             "setup": f"resnet50, whole GPU ({sm} SMs, one stream), CUDA graph per forward, same kernels"}

@@ -72,7 +72,9 @@ enum {
   DARIS_CONV_PADDED_INPUT = 2,
   /* see x2 above: the primary conv must take the TMA path (cin % 64 == 0, wo <= 128);
    * the branch is 1x1, pad 0, (ho-1)*stride2 < h2, cin2 % 64 == 0 */
-  DARIS_CONV_DUAL = 4
+  DARIS_CONV_DUAL = 4,
+  /* never plan CTA pairs for this launch (the executor's concurrent tenants) */
+  DARIS_CONV_NO_PAIR = 8
 };
 
 typedef struct daris_conv_plan_t {

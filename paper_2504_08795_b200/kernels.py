@@ -106,6 +106,10 @@ def _check(rc: int, what: str) -> None:
 # split-K through thread-block clusters + DSMEM; needs partitions whose SM
 # groups can co-schedule 8-CTA clusters (the executor's default green contexts)
 CLUSTER_SPLITK = True
+# CTA pairs (cta_group::2) for large-M launches. The executor turns them off for
+# its stage graphs: under many concurrent tenants' streams a run with pairs hung
+# twice; single-tenant launches (batching baseline, tools) keep them.
+CTA_PAIRS = True
 
 
 def conv_desc(x_shape, cout, kh, kw, stride, pad, *, relu=1, block_n=0, splits=0, sm_budget=0,
@@ -117,7 +121,8 @@ def conv_desc(x_shape, cout, kh, kw, stride, pad, *, relu=1, block_n=0, splits=0
     d.n, d.h, d.w, d.cin, d.cout = n, h, w, cin, cout
     d.kh, d.kw, d.stride, d.pad, d.ho, d.wo = kh, kw, stride, pad, ho, wo
     d.relu, d.block_n, d.splits, d.sm_budget = relu, block_n, splits, sm_budget
-    d.flags = (1 if (CLUSTER_SPLITK if cluster is None else cluster) else 0) | (2 if padded_input else 0)
+    d.flags = ((1 if (CLUSTER_SPLITK if cluster is None else cluster) else 0) | (2 if padded_input else 0) |
+               (0 if CTA_PAIRS else 8))
     if x2_shape is not None:  # DARIS_CONV_DUAL: 1x1 branch over x2 as extra K blocks
         d.flags |= 4
         _, d.h2, d.w2, d.cin2 = x2_shape

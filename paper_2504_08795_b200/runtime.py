@@ -131,6 +131,7 @@ class Executor:
                                     "n_groups": p.n_groups, "green": bool(p.green), "group_size": p.group_size})
         # split-K through 8-CTA clusters only where every partition can co-schedule them
         K.CLUSTER_SPLITK = min(p["group_size"] for p in self.partitions) >= 8
+        K.CTA_PAIRS = False  # concurrent tenants: one-CTA tiles only (kernels.py)
 
     def _c(self, rc: int, what: str) -> None:
         if rc != 0:
@@ -149,6 +150,7 @@ class Executor:
         group (8-CTA clusters launch there), e.g. for single-partition tools."""
         ctx = next((p["context"] for p in self.partitions if p["group_size"] >= 8), 1)
         K.CLUSTER_SPLITK = self.partitions[ctx - 1]["group_size"] >= 8   # the tool runs there only
+        K.CTA_PAIRS = True  # one stream, no concurrent tenants
         return ctx
 
     def stream(self, context: int, stream: int) -> int:

@@ -334,6 +334,7 @@ def test_conv_cta_pair(n, h, cin, cout, k, stride, pad, residual, bn):
     the weight tile): the planner picks them for large-M grids; numerics as the
     one-CTA path."""
     from paper_2504_08795_b200 import kernels as K
+    K.CTA_PAIRS = True  # (an executor created earlier in this process turns them off for its tenants)
     d = K.conv_desc((n, h, h, cin), cout, k, k, stride, pad, block_n=bn, sm_budget=8)
     p = K.conv_plan(d)
     assert p.pair == 1 and p.splits == 1, (p.pair, p.splits)
