@@ -175,7 +175,7 @@ __device__ __forceinline__ void finalize_row32(const ConvArgs& a, int m, int col
   for (int q = 0; q < 4; ++q) yp[q] = pk[q];
 }
 
-template <int BN, int ST>
+template <int BN, int ST, bool RT = false>  // RT: the residual tile arrives by TMA (ConvArgs::res_tma)
 __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
     conv_igemm_tc_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
                          const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap amap2,
@@ -245,7 +245,7 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
       if (a.tma_a) tma_prefetch_desc(&amap);
       if (a.tma_c) tma_prefetch_desc(&ymap);
       if (a.kb_seg1 < a.num_kb) tma_prefetch_desc(&amap2);
-      if (a.res_tma) tma_prefetch_desc(&rmap);
+      if (RT) tma_prefetch_desc(&rmap);
     }
   }
   tc_fence_before();
@@ -334,7 +334,7 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
     const __nv_bfloat16* res_row = has_res ? a.res + static_cast<size_t>(m) * a.cout + n0 : nullptr;
     // this thread's first residual chunk: in flight while the last loads land / MMAs drain
     uint4 res_cur[4];
-    if (has_res && !a.res_tma) {
+    if (has_res && !RT) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) res_cur[q] = ldg_nc16(res_row + 8 * q);
     }
@@ -358,7 +358,7 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
       const uint32_t swz = static_cast<uint32_t>(row & 7);
       const int c1 = a.tma_a ? h0 * a.wo : m0;
       const int c2 = a.tma_a ? img : 0;
-      if (a.res_tma) mbar_wait(res_bar, 0);
+      if constexpr (RT) mbar_wait(res_bar, 0);
       // (the residual by chunk, the next chunk's loads in flight while this one is
       // packed: all of a row at once through cp.async into the idle B ring after
       // the accumulator is ready measured slower — layer1 conv3 9.1 -> 10.1 us at
@@ -369,7 +369,7 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
         uint32_t r[32];
         uint4 res_nxt[4];
         const uint32_t chunk0 = static_cast<uint32_t>((c0 & 63) >> 3);
-        if (a.res_tma) {
+        if constexpr (RT) {
           if (has_res) {  // this chunk of the row from the TMA-staged residual (same swizzle)
             const uint8_t* rp = (c0 < 64 ? res_half0 : res_half1) + row * 128;
 #pragma unroll
@@ -385,7 +385,7 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
         pack_row32(a, c0, reinterpret_cast<const float*>(r), s_scale, s_bias, res_cur, has_res, pk);
 #pragma unroll
         for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(rowp + (((chunk0 + q) ^ swz) << 4)) = pk[q];
-        if (!a.res_tma) {
+        if constexpr (!RT) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) res_cur[q] = res_nxt[q];
         }
@@ -484,7 +484,7 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
         tma_load_2d(&wmap, &full[i], sB + i * L::kBBytes, (kb_begin + i) * kBK, n0);
       }
       pdl_wait();
-      if (a.res_tma) {  // stage nkb..kStages-1 is never used by the K loop: the residual goes there
+      if constexpr (RT) {  // stage nkb..kStages-1 is never used by the K loop: the residual goes there
         mbar_arrive_expect_tx(res_bar, static_cast<uint32_t>((BN / 64) * a.box_rows * 128));
         tma_load_3d(&rmap, res_bar, res_half0, n0, h0 * a.wo, img);
         if (BN == 128) tma_load_3d(&rmap, res_bar, res_half1, n0 + 64, h0 * a.wo, img);
@@ -824,10 +824,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
-template <int BN, int ST, bool PAIR>
+template <int BN, int ST, bool PAIR, bool RT = false>
 constexpr auto conv_kernel_fn() {
   if constexpr (PAIR) return conv_pair_kernel<BN, ST>;
-  else return conv_igemm_tc_kernel<BN, ST>;
+  else return conv_igemm_tc_kernel<BN, ST, RT>;
 }
 template <int BN, int ST, bool PAIR>
 constexpr int conv_smem_bytes() {
@@ -926,11 +926,18 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
     if (r != CUDA_SUCCESS) return DARIS_K_BAD_ARG;
   }
 
+  auto set_attrs = [&](auto fn) -> cudaError_t {
+    set_max_carveout(reinterpret_cast<const void*>(fn));
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  };
   static bool attr_set = false;  // per template instantiation
   if (!attr_set) {
-    set_max_carveout(reinterpret_cast<const void*>(kernel));
-    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaError_t e = set_attrs(kernel);
     if (e != cudaSuccess) return e;
+    if constexpr (!PAIR && BN <= 128) {
+      e = set_attrs(conv_kernel_fn<BN, ST, false, true>());
+      if (e != cudaSuccess) return e;
+    }
     attr_set = true;
   }
   ConvArgs a;
@@ -1007,6 +1014,11 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
     attr[cfg.numAttrs].val.clusterDim.y = 1;
     attr[cfg.numAttrs].val.clusterDim.z = pl.cluster;
     cfg.numAttrs++;
+  }
+  if constexpr (!PAIR && BN <= 128) {
+    if (a.res_tma)
+      return static_cast<int>(
+          cudaLaunchKernelEx(&cfg, conv_kernel_fn<BN, ST, false, true>(), map, amap, ymap, amap2, rmap, a));
   }
   return static_cast<int>(cudaLaunchKernelEx(&cfg, kernel, map, amap, ymap, amap2, rmap, a));
 }
