@@ -160,6 +160,12 @@ int daris_dwconv(const void* x, void* y, const void* weight, const float* scale,
                  int32_t h, int32_t w, int32_t c, int32_t k, int32_t stride, int32_t pad, int32_t ho, int32_t wo,
                  int32_t relu, void* stream);
 
+/* Debug builds (-DDARIS_PAIR_DEBUG) only: host-mapped words where a CTA-pair
+ * kernel's mbarrier wait that has not completed after 2 s records its site
+ * (word 0: count; words 4..: site | rank << 4 | parity << 5 | blockIdx.x << 8 |
+ * blockIdx.y << 20). Returns DARIS_K_BAD_ARG in release builds. */
+int daris_debug_pair_watch(void* host_mapped_words);
+
 /* Number of SMs on the current device (cached). */
 int daris_device_sms(void);
 

@@ -636,6 +636,39 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
 // the TMA-store epilogue of its own 128 accumulator rows from its own TMEM.
 // Per SM and K block this moves 16 KB of A + BN/2 x 128 B of B for a
 // 128 x BN x 64 MMA share — half the weight traffic of a one-CTA tile.
+#ifdef DARIS_PAIR_DEBUG
+// Debug build only: a pair-kernel mbarrier wait that has not completed after 2 s
+// records (site, rank, block) into host-mapped memory (daris_debug_pair_watch)
+// and keeps waiting, so a host watchdog can read where a hung launch sits.
+__device__ unsigned int* g_pair_watch = nullptr;
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ void pair_wait(uint64_t* bar, uint32_t parity, int site) {
+  const unsigned long long t0 = gtimer();
+  bool reported = false;
+  while (!mbar_try(bar, parity)) {
+    if (!reported && gtimer() - t0 > 2000000000ull && g_pair_watch) {
+      reported = true;
+      const unsigned int i = atomicAdd(g_pair_watch, 1u);
+      if (i < 60)
+        g_pair_watch[4 + i] = static_cast<unsigned int>(site) | (cluster_rank() << 4) | (parity << 5) |
+                              (blockIdx.x << 8) | (blockIdx.y << 20);
+      __threadfence_system();
+    }
+  }
+}
+#define PAIR_WAIT(bar, parity, site) pair_wait(bar, parity, site)
+#else
+#define PAIR_WAIT(bar, parity, site) mbar_wait(bar, parity)
+#endif
+
 template <int BN, int ST>
 struct PairLayout {
   static constexpr int kABytes = kBM * 128;
@@ -716,7 +749,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int q = 0; q < 4; ++q) res_cur[q] = ldg_nc16(res_row + 8 * q);
     }
     __syncwarp();
-    mbar_wait(tmem_full, 0);
+    PAIR_WAIT(tmem_full, 0, 1);
     tc_fence_after();
     if (threadIdx.x == 0) pdl_trigger();
     asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -778,7 +811,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int i = 0; i < pre; ++i) load_a(i, i);
       for (int i = pre; i < nkb; ++i) {
         const int s = i % ST;
-        mbar_wait(&empty[s], ((i / ST) & 1) ^ 1);
+        PAIR_WAIT(&empty[s], ((i / ST) & 1) ^ 1, 2);
         if (rank == 0) mbar_arrive_expect_tx(&full[s], stage_tx);
         tma_load_2d_cg2(&wmap, &full[s], sB + s * L::kBBytes, i * kBK, nb0);
         load_a(i, s);
@@ -790,7 +823,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t sA_u32 = smem_u32(sA), sB_u32 = smem_u32(sB);
     for (int i = 0; i < nkb; ++i) {
       const int s = i % ST;
-      mbar_wait(&full[s], (i / ST) & 1);
+      PAIR_WAIT(&full[s], (i / ST) & 1, 3);
       tc_fence_after();
       const uint64_t adesc = umma_desc_k_sw128(sA_u32 + s * L::kABytes);
       const uint64_t bdesc = umma_desc_k_sw128(sB_u32 + s * L::kBBytes);
@@ -1025,6 +1058,17 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
 
 
 }  // namespace daris
+
+extern "C" int daris_debug_pair_watch(void* host_mapped_words) {
+#ifdef DARIS_PAIR_DEBUG
+  void* dev = nullptr;
+  if (host_mapped_words && cudaHostGetDevicePointer(&dev, host_mapped_words, 0) != cudaSuccess) return DARIS_K_BAD_ARG;
+  return static_cast<int>(cudaMemcpyToSymbol(daris::g_pair_watch, &dev, sizeof(dev)));
+#else
+  (void)host_mapped_words;
+  return DARIS_K_BAD_ARG;  // built without DARIS_PAIR_DEBUG
+#endif
+}
 
 extern "C" int daris_device_sms(void) {
   static int sms = 0;

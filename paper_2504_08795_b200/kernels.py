@@ -79,10 +79,11 @@ def lib() -> C.CDLL:
         L.daris_linear_plan.argtypes = [C.POINTER(LinearDesc), C.POINTER(LinearPlan)]
         L.daris_linear_tc.argtypes = [C.POINTER(LinearDesc), vp]
         L.daris_avgpool_bf16.argtypes = [vp, vp, i32, i32, i32, vp]
+        L.daris_debug_pair_watch.argtypes = [vp]
         for name in ("daris_conv_plan", "daris_conv2d", "daris_stem_im2col", "daris_pack_nhwc",
                      "daris_maxpool", "daris_avgpool", "daris_linear", "daris_dwconv",
                      "daris_pack_nhwc_bordered", "daris_device_sms", "daris_linear_plan", "daris_linear_tc",
-                     "daris_avgpool_bf16"):
+                     "daris_avgpool_bf16", "daris_debug_pair_watch"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
