@@ -378,11 +378,14 @@ class DarisRuntime:
         # Not the partition: with n_contexts x n_streams jobs in flight every SM
         # is shared, and a grid sized for the whole partition spends its extra
         # CTAs on split-K fix-ups that buy isolated latency but cost throughput.
-        # Planning for the device's share per concurrent job (x1.25) measured
-        # +42 % closed-loop capacity at 4x2 OS=2 and ~2x at 16 streams
-        # (tools/capacity_probe.py, profiles/r01_capacity_*). DARIS_PLAN_SMS overrides.
+        # Planning for the device's share per concurrent job measured +42 %
+        # closed-loop capacity at 4x2 OS=2 and ~2x at 16 streams (round 1, x1.25,
+        # profiles/r01_capacity_*). With partitions over all 148 SMs and the
+        # pulled split-K the best share moved up: x1.75 (C2: 32 SMs) vs x1.25
+        # (23): knee 12.9k vs 12.3k inf/s over two runs each, p99 HP 0.38 vs
+        # 0.43 ms (profiles/r02_plan_share_ab.txt). DARIS_PLAN_SMS overrides.
         self.partition_sms = min(p["sm_count"] for p in self.exec.partitions)
-        share = int(round(1.25 * gpu.total_sms / (gpu.n_contexts * gpu.n_streams)))
+        share = int(round(1.75 * gpu.total_sms / (gpu.n_contexts * gpu.n_streams)))
         self.sm_budget = int(os.environ.get("DARIS_PLAN_SMS", "0")) or max(8, min(self.partition_sms, share))
         # per-priority planning (experiment knobs): HP jobs' grids may be planned wider
         self.plan_hp = int(os.environ.get("DARIS_PLAN_SMS_HP", "0")) or self.sm_budget

@@ -24,7 +24,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--model", default="resnet50")
     ap.add_argument("--sms", type=int, default=74, help="partition size (rounded to whole SM groups)")
-    ap.add_argument("--plan", type=int, default=23, help="SMs the layer grids are planned for")
+    ap.add_argument("--plan", type=int, default=32, help="SMs the layer grids are planned for (C2: 32)")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--batch", type=int, default=1)
     args = ap.parse_args()
