@@ -383,9 +383,13 @@ class DarisRuntime:
         # profiles/r01_capacity_*). With partitions over all 148 SMs and the
         # pulled split-K the best share moved up: x1.75 (C2: 32 SMs) vs x1.25
         # (23): knee 12.9k vs 12.3k inf/s over two runs each, p99 HP 0.38 vs
-        # 0.43 ms (profiles/r02_plan_share_ab.txt). DARIS_PLAN_SMS overrides.
+        # 0.43 ms (profiles/r02_plan_share_ab.txt). Batched jobs keep x1.25: their
+        # grids are wide anyway, and the C2 schedule with batch-16 jobs fell
+        # 35.9k -> 30.5k inf/s at x1.75 (profiles/r02_bench_plan32.json).
+        # DARIS_PLAN_SMS overrides.
         self.partition_sms = min(p["sm_count"] for p in self.exec.partitions)
-        share = int(round(1.75 * gpu.total_sms / (gpu.n_contexts * gpu.n_streams)))
+        factor = 1.75 if max(t.batch for t in self.tasks) == 1 else 1.25
+        share = int(round(factor * gpu.total_sms / (gpu.n_contexts * gpu.n_streams)))
         self.sm_budget = int(os.environ.get("DARIS_PLAN_SMS", "0")) or max(8, min(self.partition_sms, share))
         # per-priority planning (experiment knobs): HP jobs' grids may be planned wider
         self.plan_hp = int(os.environ.get("DARIS_PLAN_SMS_HP", "0")) or self.sm_budget
