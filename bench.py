@@ -177,7 +177,7 @@ def daris_batched(args, gpu, mine, log, batch: int = 4) -> dict:
     rate_x = knee_search(rt, guess, args.probe_seconds, args.step_seconds, log, criterion="ok_excl")
     rate_x = all_reduce([rate_x], "min")[0]
     rate_x, _, s_x, _, _, attempts_x = timed_knee(rt, rate_x, args, log, f"batched b{batch} excl",
-                                                  criterion="ok_excl")
+                                                  criterion="ok_excl", step_up=MAX_STEP_UP)
     done_x = all_reduce([s_x["inf_per_s"]], "sum")[0]
     rate, res, s, _, _, attempts = timed_knee(rt, rate_x, args, log, f"batched b{batch}", pause_floor=pause_floor)
     done = all_reduce([s["inf_per_s"]], "sum")[0]   # images (batch per job, engine.py:153-220)
@@ -383,6 +383,8 @@ def batching_baseline(batches=(1, 2, 4, 8, 16, 32, 64), reps: int = 20) -> dict:
 
 PROBE_WARMUP = 0.25   # warm-up share of a knee-search probe
 STEP_DOWN = 0.85      # rate factor after a timed run with a failing window
+STEP_UP = 1.08        # rate factor after a passing timed run (pause-excluded knee, up to MAX_STEP_UP times)
+MAX_STEP_UP = 2
 
 
 def run_windows(rt, warmup_s: float, step: float, n: int):
@@ -474,16 +476,18 @@ def knee_search(rt, build_rate: float, probe_s: float, step: float, log, set_rat
 
 
 def timed_knee(rt, rate: float, args, log, tag: str, set_rate=None, clock_index=None, criterion: str = "ok",
-               pause_floor=None):
+               pause_floor=None, step_up: int = 0):
     """The timed measurement: `warmup` + `steps` windows of `step_seconds`, one
     continuous run, which must meet `criterion` (summarize). A failing run is
     NOT re-measured at the same rate: the rate steps down (x STEP_DOWN) and the
     whole run repeats, up to `timed_attempts` runs. For the strict criterion,
     a run that failed only in windows with a GPU-wide pause steps straight down
     to `pause_floor(max pause)` when that is lower (no HP job of period T can
-    ride out a pause longer than T minus its response time). All ranks decide
-    together (min over ranks). Returns (rate, result, summary, clocks, wall,
-    attempts)."""
+    ride out a pause longer than T minus its response time). With `step_up`,
+    a passing run is followed by up to `step_up` runs at x STEP_UP while they
+    keep passing (the short knee-search probes are noisy; every reported rate is
+    still one whole continuous run that passed). All ranks decide together (min
+    over ranks). Returns (rate, result, summary, clocks, wall, attempts)."""
     set_rate = set_rate or rt.set_rate
     step = args.step_seconds
     attempts = []
@@ -507,9 +511,16 @@ def timed_knee(rt, rate: float, args, log, tag: str, set_rate=None, clock_index=
                          "inf_per_s": round(s["inf_per_s"], 1)})
         log(f"{tag} rate={rate:.1f} {criterion}={ok} inf/s={s['inf_per_s']:.0f} failed={s['windows_failed']} "
             f"(without pause {s['windows_failed_without_pause']}) pauses={s['stalls']} wall={wall:.1f}s")
-        out = (rate, res, s, clk.summary(), wall)
         if ok:
+            out = (rate, res, s, clk.summary(), wall)
+            if step_up > 0 and a + 1 < args.timed_attempts:
+                step_up -= 1
+                rate *= STEP_UP
+                continue
             break
+        if out is not None and out[2][criterion]:  # a step-up failed: keep the last passing run
+            break
+        out = (rate, res, s, clk.summary(), wall)
         nxt = rate * STEP_DOWN
         if pause_floor is not None and fails[1] == 0 and longest > 0:
             nxt = min(nxt, all_reduce([pause_floor(res, longest)], "min")[0])
@@ -566,7 +577,7 @@ def ours(args, make_runtime=None) -> dict | None:
     rate_x = knee_search(rt, guess, args.probe_seconds, step, log, criterion="ok_excl")
     rate_x = all_reduce([rate_x], "min")[0]
     rate_x, res_x, summ_x, _, _, attempts_x = timed_knee(rt, rate_x, args, log, "timed-excl", clock_index=local,
-                                                         criterion="ok_excl")
+                                                         criterion="ok_excl", step_up=MAX_STEP_UP)
     done_x = all_reduce([summ_x["inf_per_s"] * window], "sum")[0]
     # (2) the headline: strict, every window of the continuous run feasible
     rate, res, summ, clocks, wall, attempts = timed_knee(rt, rate_x, args, log, "timed", clock_index=local,
@@ -594,7 +605,7 @@ def ours(args, make_runtime=None) -> dict | None:
                                                            criterion="ok", pause_floor=pause_floor)
     e_done = all_reduce([summ_e["inf_per_s"] * window], "sum")[0]
     e2e_rate_x, _, summ_ex, _, _, attempts_ex = timed_knee(rt, rate_x, args, log, "e2e-excl", clock_index=local,
-                                                           criterion="ok_excl")
+                                                           criterion="ok_excl", step_up=MAX_STEP_UP)
     ex_done = all_reduce([summ_ex["inf_per_s"] * window], "sum")[0]
     st_e = res_e.stats
     frac_timed = window / (window + warm)

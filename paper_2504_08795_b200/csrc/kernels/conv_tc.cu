@@ -1063,7 +1063,9 @@ extern "C" int daris_debug_pair_watch(void* host_mapped_words) {
 #ifdef DARIS_PAIR_DEBUG
   void* dev = nullptr;
   if (host_mapped_words && cudaHostGetDevicePointer(&dev, host_mapped_words, 0) != cudaSuccess) return DARIS_K_BAD_ARG;
-  return static_cast<int>(cudaMemcpyToSymbol(daris::g_pair_watch, &dev, sizeof(dev)));
+  cudaError_t e = cudaMemcpyToSymbol(daris::g_pair_watch, &dev, sizeof(dev));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(daris::g_wait_watch, &dev, sizeof(dev));
+  return static_cast<int>(e);
 #else
   (void)host_mapped_words;
   return DARIS_K_BAD_ARG;  // built without DARIS_PAIR_DEBUG

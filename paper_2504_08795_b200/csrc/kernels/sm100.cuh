@@ -32,6 +32,40 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                "r"(bytes)
                : "memory");
 }
+#ifdef DARIS_PAIR_DEBUG
+// debug builds: every mbarrier wait of every kernel reports itself once to
+// host-mapped words (conv_tc.cu: daris_debug_pair_watch) after 2 s without
+// completing: (barrier smem offset, grid dims, block index)
+static __device__ unsigned int* g_wait_watch = nullptr;  // per translation unit (no -rdc)
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  unsigned long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  bool reported = false;
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (!reported && t - t0 > 2000000000ull && g_wait_watch) {
+      reported = true;
+      const unsigned int i = atomicAdd(g_wait_watch + 1, 1u);
+      if (i < 200) {
+        unsigned int* w = g_wait_watch + 64 + 4 * i;
+        w[0] = smem_u32(bar) & 0xFFFFu;
+        w[1] = gridDim.x | (gridDim.y << 12) | (gridDim.z << 24);
+        w[2] = blockIdx.x | (blockIdx.y << 12) | (blockIdx.z << 24);
+        w[3] = threadIdx.x | (blockDim.x << 16);
+      }
+      __threadfence_system();
+    }
+  }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -41,6 +75,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#endif
 
 // ---------------------------------------------------------------- programmatic dependent launch
 // Wait until the preceding kernel in the stream (and, transitively, all earlier

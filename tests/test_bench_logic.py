@@ -152,3 +152,16 @@ def test_conv_algorithmic_bytes_resnet50():
     wbytes = sum(op.layer.weight.numel() * 2 for op in convs)
     assert wbytes < nbytes < wbytes + 60e6
     assert sum(op.flops for op in convs) / nbytes < 1642e12 / 6547.8e9
+
+
+def test_pause_excluded_knee_steps_up_while_passing():
+    """step_up: after a passing continuous run the rate rises x1.08 (at most
+    twice) while runs keep passing; the last passing run is reported."""
+    rt = FakeRuntime()            # cliff at 1000/task
+    args = SimpleNamespace(step_seconds=0.5, warmup=2, steps=20, timed_attempts=8)
+    rate, res, s, *_ = bench.timed_knee(rt, 880.0, args, lambda m: None, "t", criterion="ok_excl", step_up=2)
+    assert [round(r, 1) for r in rt.runs] == [880.0, 950.4, 1026.4]   # third run fails at the cliff
+    assert abs(rate - 950.4) < 1e-6 and s["ok_excl"]
+    rt = FakeRuntime()
+    rate, *_ = bench.timed_knee(rt, 500.0, args, lambda m: None, "t", criterion="ok_excl", step_up=2)
+    assert abs(rate - 500.0 * 1.08 ** 2) < 1e-6 and len(rt.runs) == 3
