@@ -175,6 +175,44 @@ __device__ __forceinline__ void finalize_row32(const ConvArgs& a, int m, int col
   for (int q = 0; q < 4; ++q) yp[q] = pk[q];
 }
 
+#ifdef DARIS_PAIR_DEBUG
+// Debug build only: a pair-kernel mbarrier wait that has not completed after 2 s
+// records (site, rank, block) into host-mapped memory (daris_debug_pair_watch)
+// and keeps waiting, so a host watchdog can read where a hung launch sits.
+__device__ unsigned int* g_pair_watch = nullptr;
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ void pair_wait(uint64_t* bar, uint32_t parity, int site) {
+  const unsigned long long t0 = gtimer();
+  bool reported = false;
+  while (!mbar_try(bar, parity)) {
+    if (!reported && gtimer() - t0 > 2000000000ull && g_pair_watch) {
+      reported = true;
+      const unsigned int i = atomicAdd(g_pair_watch, 1u);
+      if (i < 60)
+        g_pair_watch[4 + i] = static_cast<unsigned int>(site) | (cluster_rank() << 4) | (parity << 5) |
+                              (blockIdx.x << 8) | (blockIdx.y << 20);
+      __threadfence_system();
+    }
+  }
+}
+#define PAIR_WAIT(bar, parity, site) pair_wait(bar, parity, site)
+// in-flight counters (host-mapped words 32..47): +1 entering / -1 leaving a blocking op
+#define DBG_IN(k) do { if (g_pair_watch) atomicAdd(g_pair_watch + 32 + (k), 1u); } while (0)
+#define DBG_OUT(k) do { if (g_pair_watch) atomicSub(g_pair_watch + 32 + (k), 1u); } while (0)
+#else
+#define PAIR_WAIT(bar, parity, site) mbar_wait(bar, parity)
+#define DBG_IN(k) do {} while (0)
+#define DBG_OUT(k) do {} while (0)
+#endif
+
 template <int BN, int ST, bool RT = false>  // RT: the residual tile arrives by TMA (ConvArgs::res_tma)
 __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
     conv_igemm_tc_kernel(const __grid_constant__ CUtensorMap wmap, const __grid_constant__ CUtensorMap amap,
@@ -239,7 +277,9 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
     fence_barrier_init();
   }
   if (warp == 4) {
+    if (lane == 0) DBG_IN(4);
     tmem_alloc<BN>(tmem_slot);
+    if (lane == 0) DBG_OUT(4);
     if (lane == 0) {
       tma_prefetch_desc(&wmap);
       if (a.tma_a) tma_prefetch_desc(&amap);
@@ -636,38 +676,6 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
 // the TMA-store epilogue of its own 128 accumulator rows from its own TMEM.
 // Per SM and K block this moves 16 KB of A + BN/2 x 128 B of B for a
 // 128 x BN x 64 MMA share — half the weight traffic of a one-CTA tile.
-#ifdef DARIS_PAIR_DEBUG
-// Debug build only: a pair-kernel mbarrier wait that has not completed after 2 s
-// records (site, rank, block) into host-mapped memory (daris_debug_pair_watch)
-// and keeps waiting, so a host watchdog can read where a hung launch sits.
-__device__ unsigned int* g_pair_watch = nullptr;
-__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ void pair_wait(uint64_t* bar, uint32_t parity, int site) {
-  const unsigned long long t0 = gtimer();
-  bool reported = false;
-  while (!mbar_try(bar, parity)) {
-    if (!reported && gtimer() - t0 > 2000000000ull && g_pair_watch) {
-      reported = true;
-      const unsigned int i = atomicAdd(g_pair_watch, 1u);
-      if (i < 60)
-        g_pair_watch[4 + i] = static_cast<unsigned int>(site) | (cluster_rank() << 4) | (parity << 5) |
-                              (blockIdx.x << 8) | (blockIdx.y << 20);
-      __threadfence_system();
-    }
-  }
-}
-#define PAIR_WAIT(bar, parity, site) pair_wait(bar, parity, site)
-#else
-#define PAIR_WAIT(bar, parity, site) mbar_wait(bar, parity)
-#endif
 
 template <int BN, int ST>
 struct PairLayout {
@@ -718,7 +726,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     fence_barrier_init();
   }
   if (warp == 4) {
+    if (lane == 0) DBG_IN(0);
     tmem_alloc_cg2<BN>(tmem_slot);
+    if (lane == 0) DBG_OUT(0);
     if (lane == 0) {
       tma_prefetch_desc(&wmap);
       tma_prefetch_desc(&amap);
@@ -727,7 +737,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   }
   tc_fence_before();
+  if (threadIdx.x == 0) DBG_IN(1);
   cluster_sync();  // both CTAs' barriers initialised and TMEM allocated before any cross-CTA traffic
+  if (threadIdx.x == 0) DBG_OUT(1);
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -807,7 +819,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (rank == 0) mbar_arrive_expect_tx(&full[i], stage_tx);
         tma_load_2d_cg2(&wmap, &full[i], sB + i * L::kBBytes, i * kBK, nb0);
       }
+      DBG_IN(3);
       pdl_wait();
+      DBG_OUT(3);
       for (int i = 0; i < pre; ++i) load_a(i, i);
       for (int i = pre; i < nkb; ++i) {
         const int s = i % ST;
@@ -836,7 +850,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) DBG_IN(2);
   cluster_sync();  // the peer's smem / TMEM are done with before either CTA frees TMEM or exits
+  if (threadIdx.x == 0) DBG_OUT(2);
   if (warp == 4) {
     tc_fence_after();
     tmem_dealloc_cg2<BN>(tmem_base);
