@@ -201,6 +201,16 @@ int daris_complete_ex(daris_handle* h, int32_t job_id, int32_t stage, double t, 
                       int32_t* job_done, int32_t* missed);
 int daris_ready_count(const daris_handle* h, int32_t context, int32_t* out);
 
+/* SM partition layout of the real executor (gpu.py:76-86's ceil_even(OS*SMs/N_c)
+ * made physical): the device is a cyclic sequence of `n_units` SM units (on B200:
+ * the 28-SM split remainder, then fifteen co-scheduled 8-SM groups); partition k
+ * is the run of units between the unit boundaries nearest to k/N_c of the device
+ * and `sm_per_context` SMs further (ties to the lower boundary). OS > 1 gives
+ * overlapping partitions (each SM in about OS of them), OS = 1 tiles the device.
+ * Outputs per context: first unit, number of units, SMs. Pure arithmetic (CPU). */
+int daris_partition_layout(int32_t n_contexts, int32_t sm_per_context, const int32_t* unit_sms, int32_t n_units,
+                           int32_t* first_unit, int32_t* n_taken, int32_t* sm_count);
+
 int daris_ledger(daris_handle* h, int32_t context, daris_ledger_t* out);
 int daris_admission_test(daris_handle* h, int32_t task_id, int32_t job_id, int32_t context, double t,
                          daris_audit* out);

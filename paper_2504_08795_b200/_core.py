@@ -128,6 +128,7 @@ def lib() -> C.CDLL:
             "daris_dispatch": [vp, i32, i32, f64, P(StageRefC), P(i32)],
             "daris_complete": [vp, i32, i32, f64, P(i32), P(i32)],
             "daris_complete_ex": [vp, i32, i32, f64, i32, P(i32), P(i32)],
+            "daris_partition_layout": [i32, i32, P(i32), i32, P(i32), P(i32), P(i32)],
             "daris_ready_count": [vp, i32, P(i32)],
             "daris_ledger": [vp, i32, P(LedgerC)],
             "daris_admission_test": [vp, i32, i32, i32, f64, P(AuditC)],
@@ -194,8 +195,18 @@ EXPORTED_SYMBOLS = (
     "daris_eval_last_error", "daris_eval_window_peak", "daris_eval_stage_fallback", "daris_eval_utilization",
     "daris_eval_deadline_shares", "daris_eval_virtual_deadlines", "daris_eval_ledger", "daris_eval_admission",
     "daris_eval_placement", "daris_eval_predicted_finish", "daris_eval_priority_level", "daris_eval_pick",
-    "daris_eval_next_completion", "daris_eval_advance",
+    "daris_eval_next_completion", "daris_eval_advance", "daris_partition_layout",
 )
+
+
+def partition_layout(n_contexts: int, sm_per_context: int, unit_sms: Sequence[int]) -> list[tuple[int, int, int]]:
+    """The executor's SM partition layout (daris_partition_layout): per context
+    (first unit, units taken, SMs) over the cyclic unit sequence `unit_sms`."""
+    n = len(unit_sms)
+    units = (C.c_int32 * n)(*unit_sms)
+    first, taken, sms = (C.c_int32 * n_contexts)(), (C.c_int32 * n_contexts)(), (C.c_int32 * n_contexts)()
+    _ev(lib().daris_partition_layout(n_contexts, sm_per_context, units, n, first, taken, sms))
+    return [(first[k], taken[k], sms[k]) for k in range(n_contexts)]
 
 
 def gpu_struct(total_sms, n_contexts, n_streams, oversubscription, policy="mps-str", kappa=0.0) -> GpuConfigC:

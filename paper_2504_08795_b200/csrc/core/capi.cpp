@@ -1,8 +1,10 @@
 // C ABI of the DARIS dispatcher (include/daris.h). Exceptions never cross the
 // boundary: every entry point returns a status code that the Python wrapper
 // maps back onto the reference's exception classes.
+#include <cmath>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "core/dispatcher.hpp"
 
@@ -458,3 +460,41 @@ int daris_eval_advance(double* remaining, const double* rates, const int64_t* jo
 }
 
 }  // extern "C"
+
+int daris_partition_layout(int32_t n_contexts, int32_t sm_per_context, const int32_t* unit_sms, int32_t n_units,
+                           int32_t* first_unit, int32_t* n_taken, int32_t* sm_count) {
+  if (n_contexts < 1 || sm_per_context < 1 || n_units < 1 || !unit_sms || !first_unit || !n_taken || !sm_count)
+    return DARIS_E_VALUE;
+  std::vector<int> start(static_cast<size_t>(n_units) + 1, 0);
+  for (int u = 0; u < n_units; ++u) {
+    if (unit_sms[u] < 1) return DARIS_E_VALUE;
+    start[u + 1] = start[u] + unit_sms[u];
+  }
+  const int covered = start[n_units];
+  // nearest unit start to x (modulo the device), ties to the lower
+  auto boundary = [&](double x) {
+    x = std::fmod(x, static_cast<double>(covered));
+    int best = 0;
+    double dist = x;
+    for (int u = 1; u <= n_units; ++u) {
+      if (std::fabs(start[u] - x) < dist) {
+        dist = std::fabs(start[u] - x);
+        best = u;
+      }
+    }
+    return best % n_units;
+  };
+  for (int k = 0; k < n_contexts; ++k) {
+    const double x0 = static_cast<double>(k) * covered / n_contexts;
+    const int u0 = boundary(x0);
+    int taken = (boundary(x0 + sm_per_context) - u0 + n_units) % n_units;
+    if (taken == 0) taken = sm_per_context * 2 >= covered ? n_units : 1;
+    int cov = 0;
+    for (int q = 0; q < taken; ++q) cov += unit_sms[(u0 + q) % n_units];
+    first_unit[k] = u0;
+    n_taken[k] = taken;
+    sm_count[k] = cov;
+  }
+  return DARIS_OK;
+}
+

@@ -196,38 +196,15 @@ int build_partitions(daris_exec* ex) {
   const int gsize = green ? static_cast<int>(groups[0].sm.smCount) : 2;
   for (int g = 0; g < G; ++g) units.push_back({g, gsize});
   const int U = static_cast<int>(units.size());
-  std::vector<int> unit_start(U, 0);
-  int covered_sms = 0;
-  for (int u = 0; u < U; ++u) {
-    unit_start[u] = covered_sms;
-    covered_sms += units[u].sms;
-  }
+  std::vector<int32_t> unit_sms(U), lay_first(c.n_contexts), lay_taken(c.n_contexts), lay_sms(c.n_contexts);
+  for (int u = 0; u < U; ++u) unit_sms[u] = units[u].sms;
+  if (daris_partition_layout(c.n_contexts, c.sm_per_context, unit_sms.data(), U, lay_first.data(), lay_taken.data(),
+                             lay_sms.data()) != DARIS_OK)
+    return fail(ex, "partition layout failed", DARIS_E_INTERNAL);
   for (int k = 0; k < c.n_contexts; ++k) {
     Partition& p = ex->parts[k];
-    // Partition k = the cyclic window of units between the unit boundaries
-    // nearest to k/N_c of the device and sm_per_context SMs further (the
-    // reference's ceil_even(OS * SMs / N_c)): OS > 1 gives overlapping windows,
-    // each SM in about OS of them; OS = 1 tiles the device exactly. 4 x 74 on
-    // B200: 76 / 72 / 72 / 76 SMs, every group and the remainder in two.
-    auto boundary = [&](double x) {  // nearest unit start to x (mod the device), ties to the lower
-      x = std::fmod(x, static_cast<double>(covered_sms));
-      int best = 0;
-      double dist = x;
-      for (int u = 1; u <= U; ++u) {
-        const double at = u < U ? unit_start[u] : covered_sms;
-        if (std::fabs(at - x) < dist) {
-          dist = std::fabs(at - x);
-          best = u;
-        }
-      }
-      return best % U;
-    };
-    const double x0 = static_cast<double>(k) * covered_sms / c.n_contexts;
-    const int u0 = boundary(x0);
-    int taken = (boundary(x0 + c.sm_per_context) - u0 + U) % U;
-    if (taken == 0) taken = c.sm_per_context * 2 >= covered_sms ? U : 1;
-    int cov = 0;
-    for (int q = 0; q < taken; ++q) cov += units[(u0 + q) % U].sms;
+    // the layout rule: daris_partition_layout (include/daris.h, libdaris_core)
+    const int u0 = lay_first[k], taken = lay_taken[k], cov = lay_sms[k];
     // the largest cluster its kernels may launch: a co-scheduled group's size if
     // the partition holds one, else 1 (the remainder's SMs are scattered over
     // GPCs, so an 8-CTA cluster may not fit: split-K then reduces through L2)

@@ -109,3 +109,38 @@ def test_gpu_library_is_tcgen05_tma_sm100a():
     res = subprocess.run([cuobjdump, "-res-usage", str(lib)], capture_output=True, text=True, check=True).stdout
     regs = [int(r) for r in re.findall(r"conv_igemm_tc_kernel\S*:\s*\n\s*REG:(\d+)", res)]
     assert regs and max(regs) <= 96, regs
+
+
+def test_partition_layout_covers_the_device_os_times():
+    """daris_partition_layout (the executor's green-partition rule) over B200's
+    units [28-SM remainder, 15 x 8-SM groups]: for every C4 cell (OS <= N_c) the
+    partitions together cover the device about OS times, every unit is used,
+    each partition is within the largest unit of ceil_even(OS * 148 / N_c), and OS = 1
+    tiles the device exactly when the remainder fits one partition."""
+    import math
+    from paper_2504_08795_b200 import _core
+    units = [28] + [8] * 15
+
+    def ceil_even(x):
+        c = math.ceil(x - 1e-9)
+        return c + (c % 2)
+    for os_ in (1.0, 1.5, 2.0, 3.0):
+        for nc in (2, 4, 8):
+            if os_ > nc:
+                continue
+            spc = min(148, ceil_even(os_ * 148 / nc))
+            lay = _core.partition_layout(nc, spc, units)
+            covered = [0] * len(units)
+            for first, taken, sms in lay:
+                assert sms == sum(units[(first + q) % len(units)] for q in range(taken))
+                assert abs(sms - spc) <= max(units), (os_, nc, spc, lay)   # within the largest unit
+                for q in range(taken):
+                    covered[(first + q) % len(units)] += 1
+            assert min(covered) >= 1, (os_, nc, covered)          # every SM is in some partition
+            total = sum(s for _, _, s in lay)
+            assert abs(total - os_ * 148) <= 0.12 * os_ * 148, (os_, nc, total)
+            if os_ == 1.0 and nc <= 4:
+                assert covered == [1] * len(units) and total == 148, (nc, lay)   # exact tiling
+    # C2 (4 x 2, OS = 2): 76 / 72 / 72 / 76, every unit in exactly two partitions
+    lay = _core.partition_layout(4, 74, units)
+    assert [s for _, _, s in lay] == [76, 72, 72, 76]
