@@ -2,22 +2,30 @@
 //
 // GEMM view: M = n*ho*wo output pixels, N = cout, K = kh*kw*cin with K ordered
 // (kh, kw, cin) so one 64-wide K block is 64 contiguous NHWC channels of one
-// input pixel (128 B). Stems (cin = 8 after padding 3 -> 8 channels) use
-// "pixel chunks": each 16-B chunk of a K block is one kernel position's 8
-// channels, so a 7x7 stem is 7 K blocks gathered straight from NHWC8. Per CTA: a 128 x BN output tile, fp32 accumulator in
-// TMEM (BN columns), a STAGES-deep smem ring.
+// input pixel (128 B). Per CTA: a 128 x BN output tile, fp32 accumulator in
+// TMEM (BN columns), a STAGES-deep smem ring of (activation, weight) K blocks.
 //
-//   warps 0-3  activation producers: cp.async gather of 128 rows x 128 B per
-//              K block straight into the 128B-swizzled UMMA layout (zero-fill
-//              for padding / tail rows), then the epilogue (TMEM -> regs ->
-//              scale/bias/residual/act -> bf16 NHWC stores).
-//   warp 4     weight producer: one TMA 2D box {64, BN} per K block; owns TMEM.
-//   warp 5     MMA issuer: one thread, 4 x tcgen05.mma (K=16) per K block.
+// conv_igemm_tc_kernel (one CTA per tile, up to 3 CTAs per SM at 96 registers):
+//   warps 0-3  epilogue (and, for shapes TMA cannot box — 224-wide VGG rows,
+//              8-channel stems without the padded layout — the activation
+//              gather: cp.async of 128 rows x 128 B straight into the 128B-
+//              swizzled UMMA layout)
+//   warp 4     TMA producer: weights as 2-D boxes {64, BN}; activations as a
+//              4-D box of th whole output rows traversed with the conv stride
+//              (padding = TMA zero fill), the stem's overlapping 128-B windows,
+//              or the fused downsample branch; the residual tile into the ring
+//              stage a short K loop never uses (RT); owns TMEM
+//   warp 5     MMA issuer: one thread, 4 x tcgen05.mma (K = 16) per K block
+// Epilogue: TMEM -> registers -> folded-BN scale/bias, residual, ReLU(6) ->
+// bf16 staged 128B-swizzled in the idle ring -> TMA store.
+// Split-K (small-M layers at batch 1): inside a cluster of <= 8 CTAs every
+// split stages its fp32 partial in its idle ring and, after one cluster
+// barrier, each CTA pulls its share of the valid rows from all peers over DSMEM
+// and runs the epilogue; without clusters, red.global.add into a zeroed tile +
+// a ticket for the last arriver, which re-zeroes both for the next launch.
 //
-// Split-K (small-M layers at batch 1): every split reduces its fp32 partial
-// tile into a zeroed per-tile accumulator with red.global.add.v4.f32 (at L2);
-// the last CTA of a tile (atomic ticket) reads the sum once, runs the epilogue
-// and re-zeroes the accumulator and the ticket for the next launch.
+// conv_pair_kernel (large-M launches): a (2,1,1) cluster runs one UMMA M = 256
+// tile on tcgen05.mma.cta_group::2 — see its comment below.
 //
 // Programmatic dependent launch: weights do not depend on the previous layer,
 // so the TMA warp starts streaming them before griddepcontrol.wait; the
