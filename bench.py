@@ -508,9 +508,11 @@ def timed_knee(rt, rate: float, args, log, tag: str, set_rate=None, clock_index=
         attempts.append({"rate_per_task": round(rate, 2), "windows_failed": int(fails[0]),
                          "windows_failed_without_pause": int(fails[1]), "gpu_pauses": int(fails[2]),
                          "windows_with_pause": int(fails[3]), "longest_pause_ms": round(longest * 1e3, 3),
-                         "inf_per_s": round(s["inf_per_s"], 1)})
+                         "hp_miss": int(s["missed_hp"]), "lp_loss": round(s["lp_loss"], 4),
+                         "rejected_lp": int(s["rejected_lp"]), "inf_per_s": round(s["inf_per_s"], 1)})
         log(f"{tag} rate={rate:.1f} {criterion}={ok} inf/s={s['inf_per_s']:.0f} failed={s['windows_failed']} "
-            f"(without pause {s['windows_failed_without_pause']}) pauses={s['stalls']} wall={wall:.1f}s")
+            f"(without pause {s['windows_failed_without_pause']}) pauses={s['stalls']} miss_hp={s['missed_hp']} "
+            f"lp_loss={s['lp_loss']:.3f} rejected_lp={s['rejected_lp']} wall={wall:.1f}s")
         if ok:
             out = (rate, res, s, clk.summary(), wall)
             if step_up > 0 and a + 1 < args.timed_attempts:
