@@ -598,7 +598,7 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
     }
     cluster_sync();  // every split's partial is staged
     if (ts && threadIdx.x == 0) ts[9] = gtimer();
-    if (warp < 4) {
+    {  // all six warps pull (the TMA and MMA warps are idle by now): more DSMEM loads in flight
       // the tile's valid rows split evenly over the S CTAs (layer4 at batch 1:
       // 49 rows -> 16 / 16 / 17, not 43 / 6 / 0)
       const int r_begin = (split * mvalid) / S, r_end = ((split + 1) * mvalid) / S;
@@ -607,7 +607,7 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
       float* s_bias = s_scale + BN;
       const uint32_t stage_u32 = smem_u32(stage);
       const int items = valid * (BN / 8);  // (row, 8-column group)
-      for (int it = threadIdx.x; it < items; it += 128) {
+      for (int it = threadIdx.x; it < items; it += kThreads) {
         const int j = it / (BN / 8), g = it % (BN / 8);
         const int rr = r_begin + j;
         const int m = m0 + rr;
