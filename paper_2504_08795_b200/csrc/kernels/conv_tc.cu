@@ -126,12 +126,6 @@ struct SmemLayout {
   static constexpr int kTotal = kEpiOff + 2 * BN * 4 + 1024;  // + alignment slack
 };
 
-__device__ __forceinline__ float act_apply(float v, int relu) {
-  if (relu == 1) return fmaxf(v, 0.f);
-  if (relu == 6) return fminf(fmaxf(v, 0.f), 6.f);
-  return v;
-}
-
 __device__ __forceinline__ uint4 ldg_nc16(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
 
 // 32 accumulator columns of one output row -> scale/bias (smem) + residual
@@ -163,12 +157,21 @@ __device__ __forceinline__ void pack_row32(const ConvArgs& a, int c_local, const
       }
     }
   }
+  // one uniform branch per 32 columns (the activation chosen per element
+  // compiled to a uniform compare + branch around every element)
+  if (a.relu == 1) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) o[i] = fmaxf(o[i], 0.f);
+  } else if (a.relu == 6) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) o[i] = fminf(fmaxf(o[i], 0.f), 6.f);
+  }
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    pk[q].x = pack_bf16x2(act_apply(o[8 * q + 0], a.relu), act_apply(o[8 * q + 1], a.relu));
-    pk[q].y = pack_bf16x2(act_apply(o[8 * q + 2], a.relu), act_apply(o[8 * q + 3], a.relu));
-    pk[q].z = pack_bf16x2(act_apply(o[8 * q + 4], a.relu), act_apply(o[8 * q + 5], a.relu));
-    pk[q].w = pack_bf16x2(act_apply(o[8 * q + 6], a.relu), act_apply(o[8 * q + 7], a.relu));
+    pk[q].x = pack_bf16x2(o[8 * q + 0], o[8 * q + 1]);
+    pk[q].y = pack_bf16x2(o[8 * q + 2], o[8 * q + 3]);
+    pk[q].z = pack_bf16x2(o[8 * q + 4], o[8 * q + 5]);
+    pk[q].w = pack_bf16x2(o[8 * q + 6], o[8 * q + 7]);
   }
 }
 
@@ -230,7 +233,9 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
   constexpr int kStages = L::kStages;
   constexpr int kLag = L::kLag;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned by pointer arithmetic on smem_raw (an integer round trip would
+  // lose the shared address space: every smem access would become a generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem + L::kAOff;
   uint8_t* sB = smem + L::kBOff;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
@@ -648,7 +653,14 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
         }
         float o[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = act_apply(v[e] * s_scale[c + e] + s_bias[c + e] + rf[e], a.relu);
+        for (int e = 0; e < 8; ++e) o[e] = v[e] * s_scale[c + e] + s_bias[c + e] + rf[e];
+        if (a.relu == 1) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) o[e] = fmaxf(o[e], 0.f);
+        } else if (a.relu == 6) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) o[e] = fminf(fmaxf(o[e], 0.f), 6.f);
+        }
         uint4 pk;
         pk.x = pack_bf16x2(o[0], o[1]);
         pk.y = pack_bf16x2(o[2], o[3]);
@@ -704,7 +716,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap /*rmap: unused*/, const ConvArgs a) {
   using L = PairLayout<BN, ST>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned by pointer arithmetic on smem_raw (an integer round trip would
+  // lose the shared address space: every smem access would become a generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem + L::kAOff;
   uint8_t* sB = smem + L::kBOff;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);
@@ -1107,9 +1121,62 @@ extern "C" int daris_device_sms(void) {
   return sms;
 }
 
-extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out) {
+namespace daris {
+// A 1x1 stride-1 unpadded convolution is a plain [M, cin] x [cin, cout] GEMM over
+// the NHWC pixels, so its M tiles need not follow image rows: a TMA box of th
+// whole output rows of one image leaves rows of the 128-row tile idle (7x7
+// maps: 49 of 128; 14x14: 126 + 70), while the same tensor viewed as one image
+// of M / w' rows of w' pixels, w' a divisor of M, tiles it almost exactly
+// (ResNet-50 layer4 at batch 64: 64 -> 25 M tiles). Returns the descriptor to
+// plan and launch: `tmp` with that view when it needs strictly fewer M tiles,
+// else `d` (idempotent). DARIS_CONV_FLAT=0 keeps the per-image tiles (A/B).
+static const daris_conv_desc* flat_view(const daris_conv_desc* d, daris_conv_desc* tmp) {
+  static const bool off = [] {
+    const char* e = std::getenv("DARIS_CONV_FLAT");
+    return e && std::atoi(e) == 0;
+  }();
+  const bool dual = (d->flags & DARIS_CONV_DUAL) != 0;
+  if (off || d->kh != 1 || d->kw != 1 || d->stride != 1 || d->pad != 0 || d->h != d->ho || d->w != d->wo ||
+      d->cin % kBK != 0 || (d->flags & DARIS_CONV_PADDED_INPUT) || d->wo > kBM)
+    return d;
+  // the fused downsample (DUAL) samples x2 every stride2 pixels: images stack
+  // along H only if output row r of the stack reads x2 row stride2 * r, i.e.
+  // each image's x2 is exactly stride2 x the output, and the row width stays wo
+  if (dual && (d->h2 != d->stride2 * d->ho || d->w2 != d->stride2 * d->wo)) return d;
+  const int64_t M = static_cast<int64_t>(d->n) * d->ho * d->wo;
+  const int th0 = std::max(1, std::min(d->ho, kBM / d->wo));
+  const int64_t tiles0 = static_cast<int64_t>(d->n) * ((d->ho + th0 - 1) / th0);
+  int64_t best = tiles0;
+  int best_w = 0;
+  for (int w = dual ? d->wo : kBM; w >= (dual ? d->wo : 1); --w) {
+    if (M % w) continue;
+    const int64_t rows = M / w, th = kBM / w;
+    const int64_t tiles = (rows + th - 1) / th;
+    if (tiles < best) best = tiles, best_w = w;
+  }
+  if (!best_w || M / best_w > (int64_t(1) << 30)) return d;
+  // Only where it pays: per-image tiles that waste > 20 % of their rows, or a
+  // grid of more than one wave of resident CTAs (3 per planned SM). A single
+  // wave of 87.5 %-full tiles (batch-1 layer1: 28 -> 25 tiles) gets slightly
+  // slower with fewer, fuller tiles (3.60 -> 3.62, 8.09 -> 8.29 us).
+  const int budget = d->sm_budget > 0 ? d->sm_budget : daris_device_sms();
+  const bool sparse = 5 * M < 4 * tiles0 * kBM;
+  const bool waves = tiles0 * std::max(1, d->cout / 128) > 3 * budget;
+  if (!sparse && !waves) return d;
+  *tmp = *d;
+  tmp->n = 1;
+  tmp->h = tmp->ho = static_cast<int32_t>(M / best_w);
+  tmp->w = tmp->wo = best_w;
+  if (dual) tmp->h2 = d->n * d->h2;  // w2 = stride2 * wo unchanged
+  return tmp;
+}
+}  // namespace daris
+
+extern "C" int daris_conv_plan(const daris_conv_desc* d0, daris_conv_plan_t* out) {
   using namespace daris;
-  if (!d || !out) return DARIS_K_BAD_ARG;
+  if (!d0 || !out) return DARIS_K_BAD_ARG;
+  daris_conv_desc flat;
+  const daris_conv_desc* d = flat_view(d0, &flat);
   if ((d->cin % kBK != 0 && d->cin != 8) || d->cout % 64 != 0 || d->n < 1 || d->ho < 1 || d->wo < 1 ||
       d->kh < 1 || d->kw < 1 || d->stride < 1)
     return DARIS_K_BAD_SHAPE;
@@ -1200,8 +1267,11 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d, daris_conv_plan_t* out)
   return DARIS_K_OK;
 }
 
-extern "C" int daris_conv2d(const daris_conv_desc* d, void* stream) {
+extern "C" int daris_conv2d(const daris_conv_desc* d0, void* stream) {
   using namespace daris;
+  if (!d0) return DARIS_K_BAD_ARG;
+  daris_conv_desc flat;
+  const daris_conv_desc* d = flat_view(d0, &flat);
   daris_conv_plan_t pl;
   int rc = daris_conv_plan(d, &pl);
   if (rc != DARIS_K_OK) return rc;

@@ -82,7 +82,9 @@ __global__ void __launch_bounds__(kLThreads, 1)
                      const LinArgs a) {
   using L = LinLayout<NB, ST>;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned by pointer arithmetic on smem_raw (an integer round trip would
+  // lose the shared address space: every smem access would become a generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem + L::kAOff;
   uint8_t* sB = smem + L::kBOff;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::kBarOff);

@@ -81,6 +81,28 @@ def test_conv_tile_width_rule():
     assert bn((64, 14, 14, 256), 256, 3, 148) == 128
 
 
+def test_conv_flat_m_tiles_for_1x1():
+    """daris_conv_plan (host-only): 1x1 stride-1 convolutions tile M as a flat
+    [pixels, channels] GEMM when that needs fewer 128-row tiles than whole image
+    rows per tile; spatial kernels and batch-1 shapes that gain nothing keep
+    their per-image plans."""
+    from paper_2504_08795_b200 import kernels as K
+
+    def plan(shape, cout, k, stride=1, budget=148):
+        return K.conv_plan(K.conv_desc(shape, cout, k, k, stride, k // 2, sm_budget=budget))
+
+    assert plan((64, 7, 7, 512), 2048, 1).tiles_m == 25        # 3136 px: 64 images -> 25 tiles
+    assert plan((64, 14, 14, 256), 1024, 1).tiles_m == 98      # 12544 px = 98 x 128
+    assert plan((64, 56, 56, 64), 256, 1).tiles_m == 1568      # 2 rows of 56 (112) -> 128 flat rows
+    assert plan((64, 14, 14, 256), 256, 3).tiles_m == 128      # 3x3: per-image row tiles (9 + 5 rows)
+    assert plan((1, 14, 14, 1024), 256, 1, budget=32).tiles_m == 2   # batch 1: no gain, unchanged
+    assert plan((1, 7, 7, 512), 2048, 1, budget=32).tiles_m == 1
+    assert plan((1, 56, 56, 256), 64, 1, budget=32).tiles_m == 28  # one wave of 87.5 %-full tiles: kept
+    # the fused downsample (1x1 stride 2 over a 2x larger x2): images stack along H, rows stay 7 wide
+    dual = K.conv_desc((64, 7, 7, 512), 2048, 1, 1, 1, 0, sm_budget=148, x2_shape=(64, 14, 14, 1024), stride2=2)
+    assert K.conv_plan(dual).tiles_m == 25                      # 448 rows of 7 in boxes of 18 rows (was 64)
+
+
 def test_gpu_library_is_tcgen05_tma_sm100a():
     """The built kernel library is sm_100a SASS that issues tcgen05 MMAs
     (UTCHMMA) and TMA loads/stores (UTMALDG/UTMASTG), and the conv kernels keep

@@ -226,7 +226,9 @@ def test_stem_tma_window_mode_matches_conv(k, stride, pad, hw, batch):
 
 
 @pytest.mark.parametrize("n,hw,cin,cout,hw2,cin2,stride2,sm", [(1, 28, 128, 512, 56, 256, 2, 23), (1, 56, 64, 256, 56, 64, 1, 23),
-                                                              (2, 7, 512, 2048, 14, 1024, 2, 23), (1, 14, 256, 1024, 28, 512, 2, 72)])
+                                                              (2, 7, 512, 2048, 14, 1024, 2, 23), (1, 14, 256, 1024, 28, 512, 2, 72),
+                                                              # images stacked along H (flat 1x1 tiling): tiles span images
+                                                              (64, 7, 512, 2048, 14, 1024, 2, 148), (5, 14, 256, 1024, 28, 512, 2, 148)])
 def test_conv_dual_branch_matches_sum_of_convs(n, hw, cin, cout, hw2, cin2, stride2, sm):
     """DARIS_CONV_DUAL: a 1x1 conv over x plus a 1x1 stride-s branch over x2 in one
     GEMM (the ResNet downsample folded into the block's last conv)."""
@@ -270,6 +272,10 @@ def test_linear_wide_k(batch, k, o, x_bf16, relu):
     (8, 56, 256, 128, 3, 2, 1, 6, False, 128),   # strided, ReLU6
     (32, 14, 256, 1024, 1, 1, 0, 0, True, 128),  # two-image-row tiles, no activation
     (4, 28, 128, 128, 3, 1, 1, 1, True, 64),
+    # 1x1 convs tiled as a flat pixel GEMM (fewer M tiles than per-image rows)
+    (64, 7, 512, 2048, 1, 1, 0, 1, True, 128),   # layer4 conv3 at batch 64: 25 tiles, last one 64 rows
+    (8, 7, 2048, 512, 1, 1, 0, 1, False, 0),     # layer4 conv1 at batch 8
+    (3, 14, 256, 1024, 1, 1, 0, 1, True, 128),   # 588 px as 14 rows of 42: 5 tiles (was 6), ragged tail
 ])
 def test_conv_large_m(n, h, cin, cout, k, stride, pad, relu, residual, bn):
     """Batched (large-M) launches on a small SM budget: many waves of tiles."""
