@@ -13,8 +13,8 @@
 //   warp 4     TMA producer: weights as 2-D boxes {64, BN}; activations as a
 //              4-D box of th whole output rows traversed with the conv stride
 //              (padding = TMA zero fill), the stem's overlapping 128-B windows,
-//              or the fused downsample branch; the residual tile into the ring
-//              stage a short K loop never uses (RT); owns TMEM
+//              or the fused downsample branch; the residual tile into a ring
+//              stage the K loop leaves free (RT); owns TMEM
 //   warp 5     MMA issuer: one thread, 4 x tcgen05.mma (K = 16) per K block
 // Epilogue: TMEM -> registers -> folded-BN scale/bias, residual, ReLU(6) ->
 // bf16 staged 128B-swizzled in the idle ring -> TMA store.
@@ -244,13 +244,6 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
   int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
   uint64_t* res_bar = tmem_full + 2;  // the residual tile has landed (res_tma)
-  // res_tma: residual half h (64 channels x 128 rows, 128B-swizzled like the output
-  // staging) in the LAST ring stage — A stage for h = 0, B stage for h = 1 (BN = 128)
-  uint8_t* res_half0 = sA + (kStages - 1) * L::kABytes;
-  uint8_t* res_half1 = sB + (kStages - 1) * L::kBBytes;
-  // output staging: half 0 in A stage 0, half 1 in B stage 0 at BN = 128 (clear of
-  // the residual); contiguous from A stage 0 otherwise
-  auto out_half = [&](int h) -> uint8_t* { return (BN == 128 && h == 1) ? sB : sA + h * (kBM * 128); };
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -279,6 +272,19 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
   const int kb_begin = split * a.kb_per_split;
   const int kb_end = min(a.num_kb, kb_begin + a.kb_per_split);
   const int nkb = kb_end - kb_begin;
+  // RT: residual half h (64 channels x 128 rows, 128B-swizzled like the output
+  // staging) in ring stage rs — A slot for h = 0, B slot for h = 1 (BN = 128) —
+  // the stage K block nkb would take: unused by a K loop shorter than the ring,
+  // else the first stage the MMAs free (its load overlaps the last K blocks).
+  // Output staging: the bf16 halves in stage st (A slot, then B slot at BN = 128),
+  // clear of the residual; contiguous from A stage 0 without RT.
+  const int rs = nkb % kStages;
+  const int st_stage = RT ? (rs + 1) % kStages : 0;
+  uint8_t* res_half0 = sA + rs * L::kABytes;
+  uint8_t* res_half1 = sB + rs * L::kBBytes;
+  auto out_half = [&](int h) -> uint8_t* {
+    return (BN == 128 && h == 1) ? sB + st_stage * L::kBBytes : sA + st_stage * L::kABytes + h * (kBM * 128);
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -537,10 +543,13 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
         tma_load_2d(&wmap, &full[i], sB + i * L::kBBytes, (kb_begin + i) * kBK, n0);
       }
       pdl_wait();
-      if constexpr (RT) {  // stage nkb..kStages-1 is never used by the K loop: the residual goes there
+      auto load_res = [&]() {
         mbar_arrive_expect_tx(res_bar, static_cast<uint32_t>((BN / 64) * a.box_rows * 128));
         tma_load_3d(&rmap, res_bar, res_half0, n0, h0 * a.wo, img);
         if (BN == 128) tma_load_3d(&rmap, res_bar, res_half1, n0 + 64, h0 * a.wo, img);
+      };
+      if constexpr (RT) {
+        if (nkb < kStages) load_res();  // stage nkb is never used by the K loop
       }
       for (int i = 0; i < pre; ++i) load_a(i, i);
       for (int i = pre; i < nkb; ++i) {
@@ -549,6 +558,12 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
         mbar_arrive_expect_tx(&full[s], L::kBBytes + a_bytes);
         tma_load_2d(&wmap, &full[s], sB + s * L::kBBytes, (kb_begin + i) * kBK, n0);
         load_a(i, s);
+      }
+      if constexpr (RT) {
+        if (nkb >= kStages) {  // as K block nkb would: once the MMAs have freed stage rs
+          mbar_wait(&empty[rs], ((nkb / kStages) & 1) ^ 1);
+          load_res();
+        }
       }
     }
   } else {
@@ -1043,14 +1058,14 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   a.tiles_h = (d->ho + a.th - 1) / a.th;
   a.d_tiles_h = make_fdiv(a.tiles_h);
   a.ts = reinterpret_cast<unsigned long long*>(d->timestamps);
-  // the residual tile by TMA into the ring stage(s) a short K loop never touches
-  // (K blocks < ring depth: ResNet layer1 / layer2 conv3), issued right after the
-  // dependency wait so it lands during the mainloop instead of being read chunk
-  // by chunk in the epilogue
+  // the residual tile by TMA into a ring stage: one a short K loop never touches
+  // (issued right after the dependency wait), else the first stage the MMAs free
+  // after the last K block is loaded, so it lands during the mainloop instead of
+  // being read chunk by chunk in the epilogue
   CUtensorMap rmap;
   std::memset(&rmap, 0, sizeof(rmap));
   a.res_tma = 0;
-  if (!PAIR && tma_c && pl.tma_rows > 0 && d->residual && BN <= 128 && a.num_kb < ST) {
+  if (!PAIR && tma_c && pl.tma_rows > 0 && d->residual && BN <= 128) {
     const cuuint64_t rows = static_cast<cuuint64_t>(d->ho) * d->wo;
     cuuint64_t rdims[3] = {static_cast<cuuint64_t>(d->cout), rows, static_cast<cuuint64_t>(d->n)};
     cuuint64_t rstr[2] = {static_cast<cuuint64_t>(d->cout) * 2, rows * d->cout * 2};
