@@ -178,6 +178,20 @@ def test_maxpool_avgpool_linear_dwconv():
     _close(out, ref.clamp(0, 6))
 
 
+@pytest.mark.parametrize("n,hw,c,k,stride,pad", [(3, 57, 64, 3, 2, 1), (1, 112, 64, 3, 2, 1), (2, 14, 512, 2, 2, 0),
+                                                 (2, 9, 24, 3, 1, 1)])
+def test_maxpool_shapes_exact(n, hw, c, k, stride, pad):
+    """max pooling is exact in bf16: the 3x3 fast path (packed bf16 maxima) and
+    the generic kernel (VGG's 2x2) equal torch bit for bit, border windows included."""
+    from paper_2504_08795_b200 import kernels as K
+    g = torch.Generator().manual_seed(n * hw + c + k)
+    x = torch.randn(n, hw, hw, c, generator=g).bfloat16()
+    ref = F.max_pool2d(x.float().permute(0, 3, 1, 2), k, stride, pad).permute(0, 2, 3, 1)
+    out = K.maxpool(x.cuda(), k, stride, pad)
+    torch.cuda.synchronize()
+    assert torch.equal(out.float().cpu(), ref.bfloat16().float())
+
+
 @pytest.mark.parametrize("k,stride,pad,hw", [(7, 2, 3, 224), (3, 1, 1, 224), (3, 2, 1, 224)])
 def test_stem_pixel_chunk_mode_matches_conv(k, stride, pad, hw):
     """cin == 8 stem mode: NHWC8 input (3 real channels), K = k*k*8 zero-padded by TMA."""
