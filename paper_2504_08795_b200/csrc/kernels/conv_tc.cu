@@ -128,51 +128,43 @@ struct SmemLayout {
 
 __device__ __forceinline__ uint4 ldg_nc16(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
 
-// 32 accumulator columns of one output row -> scale/bias (smem) + residual
-// (already in registers) -> act -> 4 x 16 B of bf16.
+// 32 accumulator columns of one output row -> scale/bias (smem) -> bf16, then
+// the residual add and the activation on packed bf16 pairs -> 4 x 16 B. The
+// residual is added after rounding acc*scale+bias to bf16 (one extra bf16
+// rounding, <= 0.5 ulp): unpacking the residual to fp32, adding and
+// activating per element was ~60 % of the epilogue's instructions, and the
+// epilogue sets the memory-bound layers' time (ResNet-50 b64: see DESIGN §3).
 __device__ __forceinline__ void pack_row32(const ConvArgs& a, int c_local, const float* v, const float* s_scale,
                                            const float* s_bias, const uint4 (&res4)[4], bool use_res,
                                            uint4 (&pk)[4]) {
-  float o[32];
   // scale/bias as 16-B smem vectors (c_local is a multiple of 32: aligned)
   const float4* sc4 = reinterpret_cast<const float4*>(s_scale + c_local);
   const float4* bi4 = reinterpret_cast<const float4*>(s_bias + c_local);
+  __nv_bfloat162 h[16];
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const float4 sc = sc4[q], bi = bi4[q];
-    o[4 * q + 0] = v[4 * q + 0] * sc.x + bi.x;
-    o[4 * q + 1] = v[4 * q + 1] * sc.y + bi.y;
-    o[4 * q + 2] = v[4 * q + 2] * sc.z + bi.z;
-    o[4 * q + 3] = v[4 * q + 3] * sc.w + bi.w;
+    h[2 * q] = __floats2bfloat162_rn(fmaf(v[4 * q + 0], sc.x, bi.x), fmaf(v[4 * q + 1], sc.y, bi.y));
+    h[2 * q + 1] = __floats2bfloat162_rn(fmaf(v[4 * q + 2], sc.z, bi.z), fmaf(v[4 * q + 3], sc.w, bi.w));
   }
   if (use_res) {
+    const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(res4);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t rr[4] = {res4[q].x, res4[q].y, res4[q].z, res4[q].w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = unpack_bf16x2(rr[e]);
-        o[8 * q + 2 * e] += f.x;
-        o[8 * q + 2 * e + 1] += f.y;
-      }
-    }
+    for (int i = 0; i < 16; ++i) h[i] = __hadd2(h[i], r2[i]);
   }
   // one uniform branch per 32 columns (the activation chosen per element
   // compiled to a uniform compare + branch around every element)
   if (a.relu == 1) {
+    const __nv_bfloat162 z = __float2bfloat162_rn(0.f);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) o[i] = fmaxf(o[i], 0.f);
+    for (int i = 0; i < 16; ++i) h[i] = __hmax2(h[i], z);
   } else if (a.relu == 6) {
+    const __nv_bfloat162 z = __float2bfloat162_rn(0.f), six = __float2bfloat162_rn(6.f);
 #pragma unroll
-    for (int i = 0; i < 32; ++i) o[i] = fminf(fmaxf(o[i], 0.f), 6.f);
+    for (int i = 0; i < 16; ++i) h[i] = __hmin2(__hmax2(h[i], z), six);
   }
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    pk[q].x = pack_bf16x2(o[8 * q + 0], o[8 * q + 1]);
-    pk[q].y = pack_bf16x2(o[8 * q + 2], o[8 * q + 3]);
-    pk[q].z = pack_bf16x2(o[8 * q + 4], o[8 * q + 5]);
-    pk[q].w = pack_bf16x2(o[8 * q + 6], o[8 * q + 7]);
-  }
+  for (int q = 0; q < 4; ++q) pk[q] = *reinterpret_cast<const uint4*>(&h[4 * q]);
 }
 
 // ... and straight to this row of the NHWC output (one thread per row).
