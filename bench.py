@@ -387,10 +387,30 @@ STEP_UP = 1.08        # rate factor after a passing timed run (pause-excluded kn
 MAX_STEP_UP = 2
 
 
+class Overloaded:
+    """Stand-in result of a run the executor stopped as overloaded
+    (runtime.BufferSetsExhausted): no report; every window counts as failed."""
+    stalls: list = []
+    overloaded = True
+
+    def __init__(self, why: str):
+        self.why = why
+
+    @staticmethod
+    def windows(n: int) -> list[dict]:
+        return [{"released_hp": 1, "released_lp": 0, "missed_hp": 1, "missed_lp": 0, "rejected_lp": 0,
+                 "lp_loss": 0.0, "completed_images": 0, "stalls": 0} for _ in range(n)]
+
+
 def run_windows(rt, warmup_s: float, step: float, n: int):
     """One continuous run: `warmup_s` of warm-up, then `n` windows of `step`
-    seconds of periodic releases. Returns (result, per-window accounting)."""
-    res = rt.run(duration=warmup_s + n * step, warmup=warmup_s, full_load=rt.afet)
+    seconds of periodic releases. Returns (result, per-window accounting); a run
+    the executor stops as overloaded fails every window (Overloaded)."""
+    from paper_2504_08795_b200.runtime import BufferSetsExhausted
+    try:
+        res = rt.run(duration=warmup_s + n * step, warmup=warmup_s, full_load=rt.afet)
+    except BufferSetsExhausted as e:
+        return Overloaded(str(e)), Overloaded.windows(n)
     return res, res.windows(warmup_s, step, n)
 
 

@@ -1256,7 +1256,10 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d0, daris_conv_plan_t* out
   // >= 16 blocks and <= 512 output channels. ResNet-50 at batch 64 on 148 SMs
   // (profiles/r02_pair_ab_b64.txt): 3x3 convs 24.2 -> 17.7 us (610 -> 835
   // TF/s), layer3 conv1 15.4 -> 11.7 us; the short-K / 1024-2048-channel
-  // conv3s are faster as one-CTA tiles at 3 CTAs per SM (28.1 vs 32.8 us).
+  // conv3s are faster as one-CTA tiles at 3 CTAs per SM (28.1 vs 32.8 us), and
+  // after the epilogue diet so are the memory-bound 1x1 convs with long K
+  // (layer4.0 conv1 18.6 -> 14.3 us, layer3 conv1 equal): pairs for spatial
+  // kernels only (profiles/r02_pair_rule_1x1_ab.txt).
   // DARIS_CONV_PAIR=0 turns pairs off (A/B), =2 takes them wherever legal.
   static const int pair_mode = [] {
     const char* e = std::getenv("DARIS_CONV_PAIR");
@@ -1265,7 +1268,7 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d0, daris_conv_plan_t* out
   out->pair = 0;
   if (pair_mode > 0 && !(d->flags & DARIS_CONV_NO_PAIR) && tma_a && splits == 1 && (bn >= 128 || pair_mode == 2) &&
       tiles_m >= 2 &&
-      (pair_mode == 2 || (tiles >= budget && num_kb >= 16 && d->cout <= 512)))
+      (pair_mode == 2 || (tiles >= budget && num_kb >= 16 && d->cout <= 512 && d->kh * d->kw > 1)))
     out->pair = 1;
   if (out->cluster > 1) {  // partials reduce through DSMEM: no global scratch
     out->workspace_floats = 0;

@@ -108,6 +108,14 @@ class ExecutorError(RuntimeError):
     pass
 
 
+class BufferSetsExhausted(ExecutorError):
+    """The executor stopped a run past the knee: every stream held a stage-0
+    launch waiting for a buffer set of its task while the jobs owning those
+    sets had nothing on the GPU (more live jobs of a task than its buffer
+    slots: an HP backlog, which admission does not bound). The offered rate is
+    infeasible; measurement code treats the run as failing every window."""
+
+
 class Executor:
     """Thin owner of one native daris_exec (partitions, streams, graphs)."""
 
@@ -135,7 +143,9 @@ class Executor:
 
     def _c(self, rc: int, what: str) -> None:
         if rc != 0:
-            raise ExecutorError(f"{what} failed ({rc}): {exec_lib().daris_exec_last_error(self._h).decode()}")
+            msg = exec_lib().daris_exec_last_error(self._h).decode()
+            cls = BufferSetsExhausted if "buffer sets exhausted" in msg else ExecutorError
+            raise cls(f"{what} failed ({rc}): {msg}")
 
     def close(self) -> None:
         if getattr(self, "_h", None):

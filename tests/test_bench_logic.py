@@ -165,3 +165,27 @@ def test_pause_excluded_knee_steps_up_while_passing():
     rt = FakeRuntime()
     rate, *_ = bench.timed_knee(rt, 500.0, args, lambda m: None, "t", criterion="ok_excl", step_up=2)
     assert abs(rate - 500.0 * 1.08 ** 2) < 1e-6 and len(rt.runs) == 3
+
+
+def test_overloaded_run_fails_every_window():
+    """A run the executor stops as overloaded (buffer sets exhausted past the
+    knee: runtime.BufferSetsExhausted) is an infeasible rate, not a crash: every
+    window fails under both criteria, and the knee search steps below it."""
+    from paper_2504_08795_b200.runtime import BufferSetsExhausted
+
+    class Overloading(FakeRuntime):
+        def run(self, duration, warmup, full_load=None):
+            if self.rate >= 900:
+                raise BufferSetsExhausted("daris_exec_run failed (13): buffer sets exhausted: 8 stage-0 launches")
+            return super().run(duration, warmup, full_load)
+
+    rt = Overloading()
+    res, ws = bench.run_windows(rt, 0.1, 0.5, 4)
+    assert len(ws) == 4 and all(window_ok(w) for w in ws)  # below the overload point
+    rt.set_rate(950)
+    res, ws = bench.run_windows(rt, 0.1, 0.5, 4)
+    assert getattr(res, "overloaded", False) and res.stalls == []
+    s = bench.summarize(ws, 0.5)
+    assert not s["ok"] and not s["ok_excl"] and s["windows_failed"] == 4
+    r = bench.knee_search(rt, 500.0, 1.0, 0.5, lambda m: None)
+    assert 0 < r < 900

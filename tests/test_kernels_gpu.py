@@ -346,7 +346,7 @@ def test_avgpool_bf16():
     (8, 28, 128, 128, 3, 1, 1, True, 128),     # layer2 conv2 shape at batch 8, residual
     (3, 28, 256, 256, 3, 1, 1, True, 256),     # odd M-tile count (21): a phantom tile in the last pair
     (8, 56, 128, 128, 3, 2, 1, False, 128),    # strided
-    (16, 14, 1024, 256, 1, 1, 0, True, 128),   # 1x1, K = 1024
+    (16, 14, 256, 256, 3, 1, 1, True, 128),    # layer3 conv2 shape (K = 2304) with a residual
     (4, 7, 512, 512, 3, 1, 1, False, 256),     # layer4 conv2, one tile per image
 ])
 def test_conv_cta_pair(n, h, cin, cout, k, stride, pad, residual, bn):

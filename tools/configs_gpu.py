@@ -34,7 +34,7 @@ sys.path.insert(0, str(ROOT))
 import bench  # noqa: E402
 from paper_2504_08795_b200.gpu import GpuConfig, Policy  # noqa: E402
 from paper_2504_08795_b200.model import Priority  # noqa: E402
-from paper_2504_08795_b200.runtime import DarisRuntime, TaskDef  # noqa: E402
+from paper_2504_08795_b200.runtime import BufferSetsExhausted, DarisRuntime, TaskDef  # noqa: E402
 
 
 def log(m):
@@ -73,7 +73,12 @@ def confirm(rt, set_factor, f: float, seconds: float):
     res = None
     for _ in range(8):
         set_factor(f)
-        res = rt.run(duration=1.0 + n * STEP, warmup=1.0, full_load=rt.afet)
+        try:
+            res = rt.run(duration=1.0 + n * STEP, warmup=1.0, full_load=rt.afet)
+        except BufferSetsExhausted as e:  # overloaded: fails every window, step down
+            log(f"confirm {f:.4g} overloaded: {e}")
+            f *= bench.STEP_DOWN
+            continue
         row = summary(res, 1.0, n)
         log(f"confirm {f:.4g} {row}")
         if row["constraints_met"]:
@@ -189,8 +194,11 @@ def c5(args):
         rt.capture_all()
         rt.afet = rt.calibrate_full_load(0.2)
         nwin = max(1, int(round(args.confirm_seconds / STEP)))
-        res = rt.run(duration=1.0 + nwin * STEP, warmup=1.0, full_load=rt.afet)
-        row = {"config": "c5", "tasks": n, "rate_per_task": rate, **summary(res, 1.0, nwin)}
+        try:
+            res = rt.run(duration=1.0 + nwin * STEP, warmup=1.0, full_load=rt.afet)
+            row = {"config": "c5", "tasks": n, "rate_per_task": rate, **summary(res, 1.0, nwin)}
+        except BufferSetsExhausted as e:
+            row = {"config": "c5", "tasks": n, "rate_per_task": rate, "constraints_met": False, "overloaded": str(e)}
         ok = row["constraints_met"]
         log(f"c5 tasks={n} ok={ok} {row}")
         rt.close()
