@@ -1266,7 +1266,7 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d0, daris_conv_plan_t* out
     return e ? std::atoi(e) : 1;
   }();
   out->pair = 0;
-  if (pair_mode > 0 && !(d->flags & DARIS_CONV_NO_PAIR) && tma_a && splits == 1 && (bn >= 128 || pair_mode == 2) &&
+  if (pair_mode > 0 && !(d->flags & DARIS_CONV_NO_PAIR) && tma_a && !padded && splits == 1 && (bn >= 128 || pair_mode == 2) &&
       tiles_m >= 2 &&
       (pair_mode == 2 || (tiles >= budget && num_kb >= 16 && d->cout <= 512 && d->kh * d->kw > 1)))
     out->pair = 1;
