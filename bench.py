@@ -542,7 +542,8 @@ def timed_knee(rt, rate: float, args, log, tag: str, set_rate=None, clock_index=
             break
         if out is not None and out[2][criterion]:  # a step-up failed: keep the last passing run
             break
-        out = (rate, res, s, clk.summary(), wall)
+        if not getattr(res, "overloaded", False) or out is None:  # report a real run when there is one
+            out = (rate, res, s, clk.summary(), wall)
         nxt = rate * STEP_DOWN
         if pause_floor is not None and fails[1] == 0 and longest > 0:
             nxt = min(nxt, all_reduce([pause_floor(res, longest)], "min")[0])
