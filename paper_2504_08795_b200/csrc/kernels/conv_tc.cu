@@ -97,6 +97,7 @@ struct ConvArgs {
   int cluster_split;  // 1: the splits of a tile form one cluster and reduce through DSMEM
   int tma_a;          // 1: activations arrive by TMA (4-D box = th whole output rows of one image)
   int th, tiles_h;    // TMA mode: output rows per M tile, M tiles per image
+  int ipt;            // TMA mode with th == ho: whole images per M tile (the boxes' image extent)
   int tma_c;          // 1: the epilogue stages the bf16 tile in smem and stores it with TMA (splits == 1)
   int res_tma;        // 1: the residual tile arrives by TMA into the ring stage the K loop never uses
   int stem_tma;       // 1: 8-channel stem from a zero-bordered input, one TMA window box per kernel row
@@ -252,10 +253,11 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
   // (th * wo <= 128 rows; the rest of the 128-row MMA tile is ignored).
   int m0, mvalid, img = 0, h0 = 0;
   if (a.tma_a) {
-    img = fdiv(tile_m, a.d_tiles_h);
-    h0 = (tile_m - img * a.tiles_h) * a.th;
+    const int q = fdiv(tile_m, a.d_tiles_h);
+    img = q * a.ipt;
+    h0 = (tile_m - q * a.tiles_h) * a.th;
     m0 = img * (a.ho * a.wo) + h0 * a.wo;
-    mvalid = min(a.th, a.ho - h0) * a.wo;
+    mvalid = min(a.th, a.ho - h0) * a.wo * min(a.ipt, a.n - img);
   } else {
     m0 = tile_m * kBM;
     mvalid = min(kBM, a.M - m0);
@@ -513,7 +515,7 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
       // block c); its A tile is the 4-D box {64 ch, wo cols, th rows, 1 image}
       // at input (c, s - pad, h0*stride - pad + r, img), traversed with the conv
       // stride; padding comes from TMA's zero fill of out-of-bounds elements.
-      const uint32_t a_bytes = static_cast<uint32_t>(a.th * a.wo * 128);
+      const uint32_t a_bytes = static_cast<uint32_t>(a.th * a.wo * 128 * a.ipt);
       auto load_a = [&](int i, int s) {
         const int kb = kb_begin + i;
         if (a.stem_tma) {  // K block = kernel row kb: windows of th output rows at padded input row h0*s + kb
@@ -536,7 +538,7 @@ __global__ void __maxnreg__(DARIS_CONV_MAXNREG)
       }
       pdl_wait();
       auto load_res = [&]() {
-        mbar_arrive_expect_tx(res_bar, static_cast<uint32_t>((BN / 64) * a.box_rows * 128));
+        mbar_arrive_expect_tx(res_bar, static_cast<uint32_t>((BN / 64) * a.box_rows * 128 * a.ipt));
         tma_load_3d(&rmap, res_bar, res_half0, n0, h0 * a.wo, img);
         if (BN == 128) tma_load_3d(&rmap, res_bar, res_half1, n0 + 64, h0 * a.wo, img);
       };
@@ -737,12 +739,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const int tile_m = blockIdx.x, tile_n = blockIdx.y;
-  const int img = fdiv(tile_m, a.d_tiles_h);
-  const int h0 = (tile_m - img * a.tiles_h) * a.th;
+  const int q_img = fdiv(tile_m, a.d_tiles_h);
+  const int img = q_img * a.ipt;
+  const int h0 = (tile_m - q_img * a.tiles_h) * a.th;
   const int m0 = img * (a.ho * a.wo) + h0 * a.wo;
   // an odd M-tile count leaves the last pair's second CTA a phantom tile past
   // the last image: its boxes read zeros and its stores are clipped
-  const int mvalid = img < a.n ? min(a.th, a.ho - h0) * a.wo : 0;
+  const int mvalid = img < a.n ? min(a.th, a.ho - h0) * a.wo * min(a.ipt, a.n - img) : 0;
   const int n0 = tile_n * BN;
   const int nkb = a.num_kb;
 
@@ -825,7 +828,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 4) {
     if (lane == 0) {
-      const uint32_t a_bytes = static_cast<uint32_t>(a.th * a.wo * 128);
+      const uint32_t a_bytes = static_cast<uint32_t>(a.th * a.wo * 128 * a.ipt);
       const uint32_t stage_tx = 2u * (a_bytes + static_cast<uint32_t>(L::kBBytes));  // both CTAs
       const int nb0 = n0 + static_cast<int>(rank) * (BN / 2);
       auto load_a = [&](int kb, int s) {
@@ -902,6 +905,21 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
+// Whole images per M tile: with one image per tile a map of <= 64 output pixels
+// (ResNet layer4's 7x7 at batch > 1) leaves most of the 128-row tile idle; k =
+// 128 / (ho*wo) images ride in one tile as the TMA boxes' image extent (the
+// rows stay image-major, so A, residual and output boxes line up). Only when
+// a tile already holds whole images (th == ho); stems excluded (their window
+// boxes are per image row). DARIS_CONV_IMGS=0 keeps one image per tile (A/B).
+static int imgs_per_tile(const daris_conv_desc* d, bool tma_a, int th) {
+  static const bool off = [] {
+    const char* e = std::getenv("DARIS_CONV_IMGS");
+    return e && std::atoi(e) == 0;
+  }();
+  if (off || !tma_a || th < d->ho || d->cin == 8 || (d->flags & DARIS_CONV_PADDED_INPUT)) return 1;
+  return std::max(1, std::min(kBM / (d->ho * d->wo), d->n));
+}
+
 template <int BN, int ST, bool PAIR, bool RT = false>
 constexpr auto conv_kernel_fn() {
   if constexpr (PAIR) return conv_pair_kernel<BN, ST>;
@@ -933,6 +951,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   CUtensorMap amap;
   std::memset(&amap, 0, sizeof(amap));
   const bool stem_tma = pl.tma_rows > 0 && d->cin == 8;
+  const int ipt = imgs_per_tile(d, pl.tma_rows > 0, pl.tma_rows);
   if (stem_tma) {
     // zero-bordered NHWC8 input [n][hp][wp][8]: dim0 = the 64-element (128 B) window of
     // kw pixels x 8 channels starting at padded column ow*stride, dim1 = output column
@@ -957,7 +976,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
     cuuint64_t astr[3] = {static_cast<cuuint64_t>(d->cin) * 2, static_cast<cuuint64_t>(d->w) * d->cin * 2,
                           static_cast<cuuint64_t>(d->h) * d->w * d->cin * 2};
     cuuint32_t abox[4] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(d->wo * d->stride),
-                          static_cast<cuuint32_t>(th * d->stride), 1};
+                          static_cast<cuuint32_t>(th * d->stride), static_cast<cuuint32_t>(ipt)};
     cuuint32_t aestr[4] = {1, static_cast<cuuint32_t>(d->stride), static_cast<cuuint32_t>(d->stride), 1};
     r = encode(&amap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(d->x), adims, astr, abox, aestr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -977,7 +996,8 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
                                       : static_cast<cuuint64_t>(d->n) * d->ho * d->wo;
     cuuint64_t ydims[3] = {static_cast<cuuint64_t>(d->cout), rows, per_image ? static_cast<cuuint64_t>(d->n) : 1};
     cuuint64_t ystr[2] = {static_cast<cuuint64_t>(d->cout) * 2, rows * d->cout * 2};
-    cuuint32_t ybox[3] = {64, static_cast<cuuint32_t>(per_image ? pl.tma_rows * d->wo : kBM), 1};
+    cuuint32_t ybox[3] = {64, static_cast<cuuint32_t>(per_image ? pl.tma_rows * d->wo : kBM),
+                          static_cast<cuuint32_t>(per_image ? ipt : 1)};
     cuuint32_t yestr[3] = {1, 1, 1};
     r = encode(&ymap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, d->y, ydims, ystr, ybox, yestr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
@@ -996,7 +1016,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
     cuuint64_t bstr[3] = {static_cast<cuuint64_t>(d->cin2) * 2, static_cast<cuuint64_t>(d->w2) * d->cin2 * 2,
                           static_cast<cuuint64_t>(d->h2) * d->w2 * d->cin2 * 2};
     cuuint32_t bbox[4] = {static_cast<cuuint32_t>(kBK), static_cast<cuuint32_t>(d->wo * d->stride2),
-                          static_cast<cuuint32_t>(th * d->stride2), 1};
+                          static_cast<cuuint32_t>(th * d->stride2), static_cast<cuuint32_t>(ipt)};
     cuuint32_t bestr[4] = {1, static_cast<cuuint32_t>(d->stride2), static_cast<cuuint32_t>(d->stride2), 1};
     r = encode(&amap2, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(d->x2), bdims, bstr, bbox, bestr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -1047,6 +1067,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
   a.stem_tma = stem_tma ? 1 : 0;
   a.box_rows = box_rows;
   a.th = pl.tma_rows > 0 ? pl.tma_rows : 1;
+  a.ipt = ipt;
   a.tiles_h = (d->ho + a.th - 1) / a.th;
   a.d_tiles_h = make_fdiv(a.tiles_h);
   a.ts = reinterpret_cast<unsigned long long*>(d->timestamps);
@@ -1061,7 +1082,7 @@ static int launch_bn(const daris_conv_desc* d, const daris_conv_plan_t& pl, cuda
     const cuuint64_t rows = static_cast<cuuint64_t>(d->ho) * d->wo;
     cuuint64_t rdims[3] = {static_cast<cuuint64_t>(d->cout), rows, static_cast<cuuint64_t>(d->n)};
     cuuint64_t rstr[2] = {static_cast<cuuint64_t>(d->cout) * 2, rows * d->cout * 2};
-    cuuint32_t rbox[3] = {64, static_cast<cuuint32_t>(box_rows), 1};
+    cuuint32_t rbox[3] = {64, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(ipt)};
     cuuint32_t restr[3] = {1, 1, 1};
     if (encode(&rmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(d->residual), rdims, rstr, rbox, restr,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -1204,7 +1225,8 @@ extern "C" int daris_conv_plan(const daris_conv_desc* d0, daris_conv_plan_t* out
                      (d->cin % kBK == 0 && d->wo * d->stride <= 256 && th * d->stride <= 256 &&
                       d->wo <= kBM);
   const int tiles_h = (d->ho + th - 1) / th;
-  const int tiles_m = tma_a ? d->n * tiles_h : (M + kBM - 1) / kBM;
+  const int ipt = imgs_per_tile(d, tma_a, th);
+  const int tiles_m = !tma_a ? (M + kBM - 1) / kBM : ipt > 1 ? (d->n + ipt - 1) / ipt : d->n * tiles_h;
   int bn = d->block_n;
   if (bn == 0) {
     bn = d->cout % 128 == 0 ? 128 : 64;

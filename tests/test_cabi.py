@@ -101,6 +101,11 @@ def test_conv_flat_m_tiles_for_1x1():
     # the fused downsample (1x1 stride 2 over a 2x larger x2): images stack along H, rows stay 7 wide
     dual = K.conv_desc((64, 7, 7, 512), 2048, 1, 1, 1, 0, sm_budget=148, x2_shape=(64, 14, 14, 1024), stride2=2)
     assert K.conv_plan(dual).tiles_m == 25                      # 448 rows of 7 in boxes of 18 rows (was 64)
+    # 3x3 on 7x7 maps: whole images per tile (2 x 49 rows), batch 1 unchanged
+    assert plan((64, 7, 7, 512), 512, 3).tiles_m == 32
+    assert plan((3, 7, 7, 512), 512, 3).tiles_m == 2
+    assert plan((1, 7, 7, 512), 512, 3, budget=32).tiles_m == 1
+    assert plan((8, 14, 14, 256), 256, 3).tiles_m == 16         # 196 px > 64: one image per tile, 2 tiles each
 
 
 def test_gpu_library_is_tcgen05_tma_sm100a():

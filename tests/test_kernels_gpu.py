@@ -290,6 +290,9 @@ def test_linear_wide_k(batch, k, o, x_bf16, relu):
     (64, 7, 512, 2048, 1, 1, 0, 1, True, 128),   # layer4 conv3 at batch 64: 25 tiles, last one 64 rows
     (8, 7, 2048, 512, 1, 1, 0, 1, False, 0),     # layer4 conv1 at batch 8
     (3, 14, 256, 1024, 1, 1, 0, 1, True, 128),   # 588 px as 14 rows of 42: 5 tiles (was 6), ragged tail
+    # 3x3 on 7x7 maps: two whole images per 128-row tile (the last tile holds one)
+    (3, 7, 512, 512, 3, 1, 1, 1, True, 128),
+    (5, 7, 256, 256, 3, 1, 1, 6, False, 64),
 ])
 def test_conv_large_m(n, h, cin, cout, k, stride, pad, relu, residual, bn):
     """Batched (large-M) launches on a small SM budget: many waves of tiles."""
@@ -347,7 +350,7 @@ def test_avgpool_bf16():
     (3, 28, 256, 256, 3, 1, 1, True, 256),     # odd M-tile count (21): a phantom tile in the last pair
     (8, 56, 128, 128, 3, 2, 1, False, 128),    # strided
     (16, 14, 256, 256, 3, 1, 1, True, 128),    # layer3 conv2 shape (K = 2304) with a residual
-    (4, 7, 512, 512, 3, 1, 1, False, 256),     # layer4 conv2, one tile per image
+    (16, 7, 512, 512, 3, 1, 1, False, 256),    # layer4 conv2: two whole images per 128-row tile
 ])
 def test_conv_cta_pair(n, h, cin, cout, k, stride, pad, residual, bn):
     """cta_group::2 pairs (UMMA M = 256 over two M tiles, each CTA loading half
